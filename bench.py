@@ -1,0 +1,504 @@
+"""Benchmark: SwinGS window-training views/s at DyNeRF resolution on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+One step = one training view through the public API (train_swin): active-set
+compaction -> projection -> tile binning -> raster forward -> L1+SSIM ->
+raster backward -> projection backward -> [NCCL allreduce] -> fused Adam +
+SGLD (+ MCMC relocation every 100 iterations, as the reference schedules it).
+
+Workload (default, BASELINE.json configs[2], "DyNeRF-shaped synthetic"):
+300-frame synthetic video, 20 arc cameras at 1352x1014, num_gs = 300k,
+swin_size = 10.  Ground truth is the animated 300k-splat scene rendered by
+the GPU forward; the model is initialised from the frame-0
+point cloud as TrainConfig.init_points does.  Steps run in the window
+[1, 11) after genesis + schedule_expire + mature(1), so every view mixes
+optimizable and matured generations (the steady state).
+
+Rank 0 prints one JSON line.  `value` is whole-job views/s with ground truth
+resident in HBM; `e2e` is the same through train_swin with each step's
+ground truth copied from pinned host memory and the loss read back.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    1: dict(name="synthetic tiny scene: 10k Gaussians, 64x64, 4 cameras, window=4, 20 frames",
+            gt_n=10_000, frames=20, views=4, W=64, H=64, num_gs=10_000, swin=4, dynerf=False),
+    2: dict(name="static single frame: 200k Gaussians, 1352x1014, 20 cameras",
+            gt_n=200_000, frames=1, views=20, W=1352, H=1014, num_gs=200_000, swin=1, dynerf=True),
+    3: dict(name="DyNeRF-shaped synthetic: 300 frames, 20 cameras at 1352x1014, 300k active "
+                 "Gaussians, window=10",
+            gt_n=300_000, frames=300, views=20, W=1352, H=1014, num_gs=300_000, swin=10,
+            dynerf=True),
+    4: dict(name="long video: 1200 frames, window=20, 1M Gaussians, 20 cameras",
+            gt_n=1_000_000, frames=1200, views=20, W=1352, H=1014, num_gs=1_000_000, swin=20,
+            dynerf=True),
+}
+METRIC = "window training views/sec (1352x1014)"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+
+
+def load_peaks():
+    if PEAKS.exists():
+        d = json.loads(PEAKS.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits", "-lms", "200"],
+                                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        while not self._stop.is_set():
+            line = p.stdout.readline()
+            if not line:
+                break
+            self.samples.append([x.strip() for x in line.split(",")])
+        p.terminate()
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=3)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
+
+
+def build_workload(cfg_id: int, dp, device_resident=True):
+    import torch
+
+    from paper_2409_07759_b200 import synth, train
+
+    c = CONFIGS[cfg_id]
+    if c["dynerf"]:
+        scene = synth.dynerf_scene(c["gt_n"], c["frames"], c["views"], c["W"], c["H"], seed=7)
+    else:
+        cams = synth.arc_cameras(c["views"], c["W"], c["H"], arc_degrees=36.0)
+        scene = synth.make_scene(7, c["frames"], cams, c["gt_n"])
+    ds = synth.device_video(scene)
+    pts = init_points(scene, c)
+    tmp = tempfile.NamedTemporaryFile("w", suffix=".xyz", delete=False)
+    np.savetxt(tmp, pts)
+    tmp.close()
+    cfg = train.TrainConfig(swin_size=c["swin"], num_gs=c["num_gs"], genesis_iterations=2,
+                            window_iterations=2, relocate_period=100, rng_seed=0,
+                            init_points=tmp.name)
+    state = train.init_state(cfg)
+    os.unlink(tmp.name)
+    state.dp = dp
+    # genesis -> staggered lifespans -> first window slide (steady state)
+    train.train_swin(0, cfg.swin_size, state, ds, iterations=2)
+    st = 0
+    if c["frames"] > 1:
+        train.schedule_expire(state)
+        train.mature(1, state, writer=None)
+        st = 1
+    window = (st, st + cfg.swin_size)
+    # ground truth of the window resident in HBM before timing
+    for f in range(window[0], min(window[1], c["frames"])):
+        for v in range(c["views"]):
+            ds.device_frame(f, v)
+    torch.cuda.synchronize()
+    return c, scene, ds, state, window
+
+
+def init_points(scene, c):
+    """x y z r g b of the frame-0 ground-truth splats, resampled to num_gs
+    (the TrainConfig.init_points recipe both arms start from)."""
+    g0 = scene.gaussians_at(0)
+    pts = np.concatenate([g0.means, g0.colors], axis=1)
+    rng = np.random.default_rng(0)
+    if len(pts) < c["num_gs"]:
+        pts = np.concatenate([pts, pts[rng.integers(0, len(pts), c["num_gs"] - len(pts))]])
+    return pts[: c["num_gs"]]
+
+
+class HostFeed:
+    """Dataset view whose ground truth is copied from pinned host memory on
+    every access (the e2e arm)."""
+
+    def __init__(self, ds, window, views):
+        import torch
+
+        self.ds = ds
+        self.cameras = ds.cameras
+        self.total_frames = ds.total_frames
+        self.host = {}
+        for f in range(window[0], min(window[1], ds.total_frames)):
+            for v in range(views):
+                self.host[(f, v)] = ds.device_frame(f, v).cpu().pin_memory()
+        self.h2d_bytes = 0
+        self.torch = torch
+
+    @property
+    def n_views(self):
+        return self.ds.n_views
+
+    def device_frame(self, frame, view):
+        h = self.host[(frame, view)]
+        self.h2d_bytes += h.numel()
+        return h.to("cuda", non_blocking=True)
+
+
+class LossReadback:
+    """train_swin progress hook: read the step's loss sums back to the host."""
+
+    def __init__(self, model):
+        self.model = model
+        self.d2h_bytes = 0
+        self.values = []
+
+    def update(self, _n):
+        s = self.model.last_sums.cpu()
+        self.d2h_bytes += s.numel() * s.element_size()
+        self.values.append(float(s[0]))
+
+
+def time_steps(state, ds, window, steps, dp, progress=None):
+    import torch
+
+    from paper_2409_07759_b200 import train
+
+    if dp is not None:
+        dp.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record()
+    train.train_swin(window[0], window[1], state, ds, iterations=steps, progress=progress)
+    end.record()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    if dp is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dp.dist.all_reduce(t, op=dp.dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dp.barrier()
+    return ms
+
+
+def count_launches(state, ds, window):
+    """Kernels launched by one training step, from the torch profiler (ours =
+    everything not emitted by torch's own ATen kernels)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    from paper_2409_07759_b200 import train
+
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        train.train_swin(window[0], window[1], state, ds, iterations=1)
+        torch.cuda.synchronize()
+    ours = aten = 0
+    names = {}
+    for e in prof.events():
+        if e.device_type != torch.autograd.DeviceType.CUDA:
+            continue
+        n = e.name
+        if "memcpy" in n.lower() or "memset" in n.lower():
+            continue
+        if "at::" in n or "at_cuda_detail" in n:
+            aten += 1
+        else:
+            ours += 1
+            names[n[:60]] = names.get(n[:60], 0) + 1
+    return ours, aten, names
+
+
+def roofline_pass(state, ds, window, steps):
+    """Raster fwd+bwd kernel time (CUDA events on the launch stream) and
+    K_used per view over `steps` extra (untimed) steps."""
+    import torch
+
+    from paper_2409_07759_b200 import train
+
+    model = state.device
+    pipe = model.pipe
+    pipe.enable_timing(True)
+    k_used, k_pairs, n_act = [], [], []
+
+    class Hook:
+        def update(self, _n):
+            k_used.append(pipe.k_used())
+            k_pairs.append(pipe.n_pairs)
+            n_act.append(pipe.n)
+
+    train.train_swin(window[0], window[1], state, ds, iterations=steps, progress=Hook())
+    ms = pipe.kernel_ms()
+    pipe.enable_timing(False)
+    torch.cuda.synchronize()
+    return ms, float(np.mean(k_used)), float(np.mean(k_pairs)), float(np.mean(n_act))
+
+
+# --------------------------------------------------------------------------- CPU
+def cpu_reference_view(c, state_np, n_threads, crop=128, n_crops=4, seed=0):
+    """The oracle port (oracle/, the reference algorithm in fp64 C/numpy) timed
+    on the host: one training view of the workload, with the pixel loops run
+    on `n_crops` crop cameras of crop x crop pixels spread over the image and
+    extrapolated by P / P_crop; per-Gaussian stages timed at full size."""
+    from oracle import splat_oracle as O
+
+    W, H = c["W"], c["H"]
+    cams = _arc_cams_np(c)
+    cam = cams[0]
+    means, quats, scales, opac, cols, opt_params = state_np
+    rng = np.random.default_rng(seed)
+    t0 = time.perf_counter()
+    cache = O.project_arrays(cam, means, quats, scales, opac, cols)
+    t_proj = time.perf_counter() - t0
+    t_pix = 0.0
+    xs = [W // 4, 3 * W // 4]
+    ys = [H // 4, 3 * H // 4]
+    centers = [(x, y) for y in ys for x in xs][:n_crops]
+    for (xc, yc) in centers:
+        ccam = _Cam(crop, crop, cam.fx, cam.fy, cam.cx - (xc - crop // 2), cam.cy - (yc - crop // 2),
+                    cam.rotation, cam.translation)
+        gt = O.linear_from_u8(rng.integers(0, 256, (crop, crop, 3), dtype=np.uint8))
+        t1 = time.perf_counter()
+        cc = O.project_arrays(ccam, means, quats, scales, opac, cols)
+        t2 = time.perf_counter()
+        if cc is None:
+            continue
+        img = O.blend_forward(cc, crop, crop, nthreads=n_threads)
+        n_opt = len(opt_params["mean"])
+        _, gimg, reg = O.loss(img, gt, opac[:n_opt], scales[:n_opt])
+        g2d = O.blend_backward(cc, crop, crop, gimg, nthreads=n_threads)
+        t3 = time.perf_counter()
+        t_pix += t3 - t2
+        t_proj_c = t2 - t1
+    t_pix = t_pix / max(len(centers), 1) * (W * H) / (crop * crop)
+    # per-Gaussian stages at full size: projection backward + optimizer + SGLD
+    p = len(cache["src"])
+    zeros = [np.zeros((p, 2)), np.zeros((p, 3)), np.zeros(p), np.zeros((p, 3))]
+    t4 = time.perf_counter()
+    grads = O.projection_backward(cam, cache, len(means), *zeros)
+    n_opt = len(opt_params["mean"])
+    g_opt = {k: grads[k][:n_opt] for k in O.PARAM_GROUPS}
+    params = {k: v.copy() for k, v in opt_params.items()}
+    m = {k: np.zeros_like(v) for k, v in params.items()}
+    v = {k: np.zeros_like(x) for k, x in params.items()}
+    O.optimizer_step(params, m, v, 0, g_opt)
+    O.sgld_perturb([params], 1.6e-4, 5e4, [rng.standard_normal((n_opt, 3))])
+    t_gauss = time.perf_counter() - t4 + t_proj
+    return t_pix + t_gauss, {"t_pixel_extrapolated_s": t_pix, "t_per_gaussian_s": t_gauss,
+                             "crops": len(centers), "crop": crop}
+
+
+class _Cam:
+    def __init__(self, width, height, fx, fy, cx, cy, rotation, translation):
+        self.width, self.height, self.fx, self.fy, self.cx, self.cy = width, height, fx, fy, cx, cy
+        self.rotation, self.translation = rotation, translation
+
+
+def _arc_cams_np(c):
+    n, W, H = c["views"], c["W"], c["H"]
+    focal = 70.0 * W / 64 if c["dynerf"] else 70.0
+    half = np.radians(36.0) / 2
+    out = []
+    for ang in (np.linspace(-half, half, n) if n > 1 else [0.0]):
+        center = np.array([3 * np.sin(ang), 0.25 * np.sin(2.1 * ang), -3 * np.cos(ang)])
+        fwd = -center / np.linalg.norm(center)
+        right = np.cross([0.0, 1.0, 0.0], fwd)
+        right /= np.linalg.norm(right)
+        up = np.cross(fwd, right)
+        R = np.stack([right, up, fwd])
+        out.append(_Cam(W, H, focal, focal, W / 2, H / 2, R, -R @ center))
+    return out
+
+
+def cpu_state(c):
+    """Host copy of a config's model: the trainer's init from the frame-0
+    point cloud (same recipe as the GPU arm), direct space."""
+    from paper_2409_07759_b200.synth import make_scene
+    from oracle import splat_oracle as O
+
+    k = (300.0 / c["gt_n"]) ** (1 / 3) if c["dynerf"] else 1.0
+    scene = make_scene(7, c["frames"], [], c["gt_n"], scale_range=(0.045 * k, 0.1 * k))
+    pts = init_points(scene, c)
+    n = c["num_gs"]
+    means, cols = pts[:, :3].copy(), pts[:, 3:6].copy()
+    from scipy.spatial import cKDTree
+
+    dist, _ = cKDTree(means).query(means, k=2)
+    nn = np.maximum(dist[:, 1], 1e-5)
+    quats = np.tile([1.0, 0, 0, 0], (len(means), 1))
+    scales = np.repeat(nn[:, None], 3, axis=1)
+    opac = np.full(len(means), 0.1)
+    sl = n // c["swin"]
+    opt = {"mean": means[:sl].copy(), "quat": quats[:sl].copy(),
+           "log_scale": np.log(scales[:sl]), "opacity_logit": np.full(sl, float(O.logit(0.1))),
+           "color": cols[:sl].copy()}
+    return means, quats, scales, opac, cols, opt
+
+
+def run_reference(args, c):
+    from oracle import splat_oracle as O
+
+    O.build_oracle()
+    threads = O.default_threads()
+    st = cpu_state(c)
+    for _ in range(args.warmup):
+        cpu_reference_view(c, st, threads, crop=64, n_crops=1)
+    times = []
+    info = {}
+    for _ in range(args.steps):
+        t, info = cpu_reference_view(c, st, threads)
+        times.append(t)
+    tv = float(np.mean(times))
+    value = 1.0 / tv
+    sample = (f"crop-extrapolated: {info.get('crops')} crops of {info.get('crop')}^2 px "
+              f"(pixel loops scaled by P/P_crop) + full-size per-Gaussian stages")
+    return {
+        "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tv * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": c["name"], "width": c["W"], "height": c["H"],
+                   "num_gs": c["num_gs"], "swin_size": c["swin"], "threads": threads},
+        "cpu_baseline": {"value": value, "unit": "views/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    c = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args, c)), flush=True)
+        return
+
+    import torch
+
+    from paper_2409_07759_b200.parallel import init_from_env
+
+    dp = init_from_env("nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    world = 1 if dp is None else dp.world_size
+    c, scene, ds, state, window = build_workload(args.config, dp)
+    from paper_2409_07759_b200 import train
+
+    train.train_swin(window[0], window[1], state, ds, iterations=args.warmup)
+    with ClockSampler(local) as clocks:
+        ms = time_steps(state, ds, window, args.steps, dp)
+    views_per_s = world * args.steps / (ms / 1e3)
+    out = {
+        "metric": METRIC, "value": views_per_s, "unit": "views/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (SURVEY.md §8(d) DyNeRF-shaped recipe, GPU-rendered ground truth)",
+        "config": {"workload": c["name"], "width": c["W"], "height": c["H"],
+                   "num_gs": c["num_gs"], "gt_gaussians": c["gt_n"], "swin_size": c["swin"],
+                   "window": list(window), "parallelism": f"dp{world}",
+                   "global_batch": world, "l2": "per-step working set > 126 MB L2 "
+                   "(tile pairs + optimizer state); no explicit flush"},
+        "clocks": clocks.summary(),
+    }
+    if not args.no_e2e:
+        feed = HostFeed(ds, window, c["views"])
+        rb = LossReadback(state.device)
+        train.train_swin(window[0], window[1], state, feed, iterations=2, progress=rb)
+        feed.h2d_bytes = 0
+        rb.d2h_bytes = 0
+        ms_e2e = time_steps(state, feed, window, args.steps, dp, progress=rb)
+        out["e2e"] = {"value": world * args.steps / (ms_e2e / 1e3), "unit": "views/s",
+                      "h2d_bytes_per_step": feed.h2d_bytes // args.steps,
+                      "d2h_bytes_per_step": rb.d2h_bytes // args.steps,
+                      "api": "train.train_swin with pinned-host ground truth"}
+    kms, k_used, k_pairs, n_act = roofline_pass(state, ds, window, min(args.steps, 10))
+    nview = min(args.steps, 10)
+    t_raster = (kms.get("raster_fwd", 0.0) + kms.get("raster_bwd", 0.0)) / nview / 1e3
+    P = c["W"] * c["H"]
+    b_raster = 116.0 * k_used + 52.0 * P
+    peak, peak_kind = load_peaks()
+    achieved = b_raster / t_raster / 1e9 if t_raster > 0 else 0.0
+    out["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                       "frac": achieved / peak, "traffic": None,
+                       "kernel": "raster_fwd + raster_bwd", "peak_source": peak_kind,
+                       "bytes_per_view": b_raster, "K_used": k_used, "K": k_pairs,
+                       "active_splats": n_act, "pixels": P,
+                       "ms_per_view": {"raster_fwd": kms.get("raster_fwd", 0) / nview,
+                                       "raster_bwd": kms.get("raster_bwd", 0) / nview}}
+    ours, aten, names = count_launches(state, ds, window)
+    out["gpu_launches"] = ours * args.steps
+    out["gpu_launches_per_step"] = ours
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import splat_oracle as O
+
+        O.build_oracle()
+        threads = O.default_threads()
+        st = cpu_state(c)
+        t, info = cpu_reference_view(c, st, threads)
+        out["cpu_baseline"] = {"value": 1.0 / t, "unit": "views/s", "cores": threads,
+                               "kind": "port",
+                               "sample": f"oracle (reference algorithm, fp64) on "
+                                         f"{info['crops']} crops of {info['crop']}^2 px, pixel "
+                                         f"loops extrapolated by P/P_crop; per-Gaussian stages "
+                                         f"at full size; {t:.1f} s/view"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dp is not None:
+        dp.barrier()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+/*
+ * swings.h — C ABI of libswings.so, the B200 (sm_100a) implementation of
+ * SwinGS's sliding-window training hot path.
+ *
+ * Conventions
+ *  - Every compute entry point is `int ss_*(..., cudaStream_t stream)`.
+ *    Return 0 (SS_OK) or an SS_ERR_* code; ss_last_error() gives the text.
+ *    The Python host maps SS_ERR_INVALID to the reference's
+ *    InvalidParameterError (core.py:22) and everything else to RuntimeError.
+ *  - Array pointers are caller-owned DEVICE memory unless the name says
+ *    `host`.  The library never allocates; scratch comes from caller
+ *    workspaces sized by the *_workspace_bytes queries.
+ *  - Calls are stream ordered and never synchronize the host.
+ *  - Struct arguments (ss_camera, ss_store, ss_step_hyper) are HOST structs
+ *    passed by pointer and copied into kernel parameters.
+ *  - Gaussian rows are 14 doubles: mean[3] quat[4](w,x,y,z) scale[3]
+ *    opacity color[3] (core.py:153-176).  Rows of the optimizable store hold
+ *    log-scale and opacity-logit instead (train.py:155-161).
+ *
+ * Each entry point names the reference interface it replaces
+ * (path:line under /root/reference/pkg/src/splatstream/).
+ */
+#ifndef SWINGS_H
+#define SWINGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ss_stream_t; /* == cudaStream_t */
+
+enum {
+  SS_OK = 0,
+  SS_ERR_INVALID = 1,   /* bad shape / parameter -> InvalidParameterError   */
+  SS_ERR_CUDA = 2,      /* CUDA runtime error                               */
+  SS_ERR_CAPACITY = 3,  /* caller buffer too small for the data             */
+  SS_ERR_WORKSPACE = 4  /* workspace smaller than the *_workspace_bytes query */
+};
+
+#define SS_ROW 14        /* doubles per Gaussian row                       */
+#define SS_GRAD_ROW 14   /* floats per optimization-space gradient row     */
+#define SS_G2D_ROW 12    /* floats per 2D-gradient record (9 used)         */
+#define SS_TILE 16       /* tile edge in pixels                            */
+
+/* Pinhole camera, core.py:95-127 (rot is row-major world-to-camera). */
+typedef struct {
+  int32_t width, height;
+  double fx, fy, cx, cy;
+  double rot[9];
+  double trans[3];
+} ss_camera;
+
+/* The Gaussian store: optimizable rows (optimization space) followed by
+ * matured rows (direct space).  An active row id r < n_opt addresses
+ * opt[r]; r >= n_opt addresses mat[r - n_opt]. */
+typedef struct {
+  const double* opt;
+  int64_t n_opt;
+  const double* mat;
+  int64_t n_mat;
+} ss_store;
+
+/* Per-generation optimizer table entry (device array), train.py:321-344. */
+typedef struct {
+  int32_t active;   /* generation stepped this iteration                   */
+  int32_t pad;
+  double bc1, bc2;  /* 1 - b1^t, 1 - b2^t for the generation's own adam_t   */
+  double gscale;    /* gamma^windows_trained on the mean gradient          */
+} ss_gen_step;
+
+/* Optimizer + SGLD hyper-parameters (host struct), train.py:42-75. */
+typedef struct {
+  double lr[5];          /* mean, quat, log_scale, opacity_logit, color     */
+  double beta1, beta2, eps;
+  double opacity_reg, scale_reg;
+  double n_reg;          /* #active optimizable rows (divisor), loss.py:110-111 */
+  double noise_scale;    /* noise_lr * lr_mean, train.py:264                 */
+  double gate_center, gate_sharpness;
+  int32_t sgd;           /* 1 = plain SGD (train.py:322-324)                 */
+  int32_t sgld;          /* 1 = apply the SGLD perturbation                  */
+  uint64_t seed;         /* Philox key for eta when eta == NULL              */
+  uint64_t counter;      /* Philox counter (iteration index)                 */
+} ss_step_hyper;
+
+const char* ss_last_error(void);
+int ss_version(void);
+int ss_device_sm_count(void);
+
+/* ---- a-2 active-set compaction: core.py:280-282, train.py:347-350, 380-386.
+ * Candidates are the n_opt optimizable rows in row order, then the matured
+ * rows in archive (FIFO) order: logical matured row c lives at physical row
+ * mat_block_map[c / block_rows] * block_rows + c % block_rows.  Keeps rows
+ * with row_start <= frame < row_expire (per physical row; matured rows at
+ * index n_opt + physical).  Writes active row ids (n_opt + physical for
+ * matured) to out_rows and out_counts[0] = #active, [1] = #active opt. */
+size_t ss_compact_workspace_bytes(int64_t n_candidates);
+int ss_compact_active(const int32_t* row_start, const int32_t* row_expire, int64_t n_opt,
+                      int64_t n_mat_logical, const int32_t* mat_block_map, int32_t block_rows,
+                      int32_t frame, int32_t* out_rows, int32_t* out_counts, void* ws,
+                      size_t ws_bytes, ss_stream_t stream);
+
+/* ---- a-3 EWA projection / cull / conic / bbox: raster.py:76-173.
+ * For active index i (row = rows ? rows[i] : i): rec_a = (u, v, inv0, inv1),
+ * rec_b = (inv2, alpha, r, g), rec_c = b (float32, rounded once from fp64);
+ * depth_key = fp64 z bits (UINT64_MAX when culled); bbox = (x0,x1,y0,y1)
+ * pixels, half open; n_tiles = 16x16 tiles the bbox touches (0 when culled). */
+int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_t n, const ss_camera* cam,
+                   void* rec_a, void* rec_b, float* rec_c, uint64_t* depth_key, int32_t* bbox,
+                   int32_t* n_tiles, ss_stream_t stream);
+
+/* ---- a-4 binning: raster.py:153 global (z, src) order reproduced per tile.
+ * (1) stable radix sort of the 64-bit depth keys -> order (rank -> i);
+ * (2) tile counts in rank order, exclusive scan -> offsets[0..n], K = offsets[n];
+ * (3) emit (tile id, i) pairs in rank order; (4) stable radix sort by tile id;
+ * (5) per-tile [start, end) ranges.  Equivalent to sorting the keys
+ * tile << 21 | rank. */
+size_t ss_binning_workspace_bytes(int32_t n, int64_t max_pairs, int32_t n_tiles);
+int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* order, void* ws,
+                   size_t ws_bytes, ss_stream_t stream);
+int ss_tile_offsets(const int32_t* order, const int32_t* n_tiles, int32_t n, int32_t* offsets,
+                    void* ws, size_t ws_bytes, ss_stream_t stream);
+int ss_emit_tile_pairs(const int32_t* order, const int32_t* offsets, const int32_t* bbox,
+                       int32_t n, int32_t tiles_x, uint32_t* keys, int32_t* vals,
+                       ss_stream_t stream);
+/* *out_sel (HOST int) = 0 when the sorted pairs are in keys/vals, 1 when in
+ * keys_alt/vals_alt. */
+int ss_sort_tile_pairs(uint32_t* keys, int32_t* vals, uint32_t* keys_alt, int32_t* vals_alt,
+                       int64_t n_pairs, int32_t n_tiles, int32_t* out_sel, void* ws,
+                       size_t ws_bytes, ss_stream_t stream);
+int ss_tile_ranges(const uint32_t* sorted_keys, int64_t n_pairs, int32_t n_tiles,
+                   int32_t* ranges, ss_stream_t stream);
+
+/* ---- a-5 blend forward: _kernels.py:20-53.  img is (H, W, 3) float32;
+ * t_final / n_contrib per pixel feed the backward. */
+int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                  const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                  float* img, float* t_final, int32_t* n_contrib, ss_stream_t stream);
+
+/* ---- a-6 blend backward: _kernels.py:56-130.  Accumulates into g2d
+ * (n x 12 floats: g_mean2d[2] g_inv2d[3] g_alpha g_color[3] pad[3]),
+ * which the caller zeroes. */
+int ss_raster_bwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                  const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                  const float* dimg, const float* t_final, const int32_t* n_contrib, float* g2d,
+                  ss_stream_t stream);
+
+/* ---- a-7 projection backward: raster.py:249-348.  For active i with
+ * trainable (mask ? mask[i] : 1) and row < trainable_rows, writes the
+ * optimization-space gradient row grads[out_row] (14 floats: mean[3]
+ * quat[4] log_scale[3] opacity_logit color[3]); out_row = row.  Culled
+ * rows are left untouched (caller zeroes). */
+int ss_project_bwd(const ss_store* store, const int32_t* rows, int32_t n, const ss_camera* cam,
+                   const float* g2d, const uint64_t* depth_key, const uint8_t* trainable_mask,
+                   int64_t trainable_rows, float* grads, ss_stream_t stream);
+
+/* ---- a-8 loss: loss.py:73-118 (photometric part; regularizers are fused
+ * into ss_adam_sgld_step).  pred (H,W,3) f32; ground truth either u8 sRGB
+ * decoded through lut[256] (raster.py:428-432) or f32 linear.  Writes dimg
+ * (H,W,3) f32 and out_sums[0] = sum|pred-gt|, out_sums[1] = sum SSIM map
+ * (float64, deterministic). */
+size_t ss_loss_workspace_bytes(int32_t width, int32_t height);
+int ss_loss_l1_ssim(const float* pred, const uint8_t* gt_u8, const float* lut,
+                    const float* gt_f32, int32_t width, int32_t height, double ssim_weight,
+                    float* dimg, double* out_sums, void* ws, size_t ws_bytes,
+                    ss_stream_t stream);
+
+/* ---- a-9/a-10 fused Adam (or SGD) + projections + SGLD:
+ * train.py:321-344, 400-415, 246-264, loss.py:105-111.
+ * Rows r in [0, n_rows) belong to generation r / rows_per_gen; only rows of
+ * generations with gens[g].active are touched.  eta (n_rows x 3, float64) is
+ * injected when non-NULL, else drawn from Philox(seed, counter, row). */
+int ss_adam_sgld_step(double* opt, const float* grads, double* adam_m, double* adam_v,
+                      int64_t n_rows, int32_t rows_per_gen, const ss_gen_step* gens,
+                      const ss_step_hyper* hyper, const double* eta, ss_stream_t stream);
+
+/* SGLD alone (train.py:246-264) on the rows of active generations. */
+int ss_sgld(double* opt, int64_t n_rows, int32_t rows_per_gen, const ss_gen_step* gens,
+            const ss_step_hyper* hyper, const double* eta, ss_stream_t stream);
+
+/* ---- a-11 MCMC relocation: train.py:267-318.  Candidates are the rows of
+ * active generations in row order; dead = sigmoid(logit) < threshold.
+ * uniforms (n_dead float64, the draws numpy's choice() consumes) are
+ * injected when non-NULL, else Philox(seed, counter).  out_counts[0] = #dead,
+ * [1] = #alive (device).  Moves nothing when either count is zero. */
+size_t ss_relocate_workspace_bytes(int64_t n_rows);
+int ss_relocate(double* opt, double* adam_m, double* adam_v, int64_t n_rows,
+                int32_t rows_per_gen, const ss_gen_step* gens, double threshold,
+                const double* uniforms, uint64_t seed, uint64_t counter, int32_t* out_counts,
+                void* ws, size_t ws_bytes, ss_stream_t stream);
+
+/* Direct-space snapshot of optimizable rows (train.py:155-161 + 474):
+ * dst[i] = (mean, quat, exp(log_scale), sigmoid(logit), color) of src[i]. */
+int ss_to_direct(const double* src, double* dst, int64_t n, ss_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWINGS_H */

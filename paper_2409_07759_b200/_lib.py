@@ -1,0 +1,132 @@
+"""ctypes binding of libswings.so (include/swings.h).
+
+The product path has no CPU fallback: if the library or a CUDA device is
+missing, ``lib()`` raises.  Torch tensors only provide device memory and the
+current stream; every call passes raw pointers and sizes.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import POINTER, Structure, c_double, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
+
+from ._build import LIB, build, needs_build
+from .core import InvalidParameterError
+
+SS_OK, SS_ERR_INVALID, SS_ERR_CUDA, SS_ERR_CAPACITY, SS_ERR_WORKSPACE = 0, 1, 2, 3, 4
+SS_ROW = 14
+SS_GRAD_ROW = 14
+SS_G2D_ROW = 12
+SS_TILE = 16
+
+
+class SSCamera(Structure):
+    _fields_ = [("width", c_int32), ("height", c_int32), ("fx", c_double), ("fy", c_double),
+                ("cx", c_double), ("cy", c_double), ("rot", c_double * 9), ("trans", c_double * 3)]
+
+
+class SSStore(Structure):
+    _fields_ = [("opt", c_void_p), ("n_opt", c_int64), ("mat", c_void_p), ("n_mat", c_int64)]
+
+
+class SSGenStep(Structure):
+    _fields_ = [("active", c_int32), ("pad", c_int32), ("bc1", c_double), ("bc2", c_double),
+                ("gscale", c_double)]
+
+
+class SSStepHyper(Structure):
+    _fields_ = [("lr", c_double * 5), ("beta1", c_double), ("beta2", c_double), ("eps", c_double),
+                ("opacity_reg", c_double), ("scale_reg", c_double), ("n_reg", c_double),
+                ("noise_scale", c_double), ("gate_center", c_double),
+                ("gate_sharpness", c_double), ("sgd", c_int32), ("sgld", c_int32),
+                ("seed", c_uint64), ("counter", c_uint64)]
+
+
+P = c_void_p
+I32 = c_int32
+I64 = c_int64
+
+_SIGNATURES = {
+    "ss_last_error": ([], ctypes.c_char_p),
+    "ss_version": ([], c_int),
+    "ss_device_sm_count": ([], c_int),
+    "ss_compact_workspace_bytes": ([I64], c_size_t),
+    "ss_compact_active": ([P, P, I64, I64, P, I32, I32, P, P, P, c_size_t, P], c_int),
+    "ss_project_fwd": ([POINTER(SSStore), P, I32, POINTER(SSCamera), P, P, P, P, P, P, P], c_int),
+    "ss_binning_workspace_bytes": ([I32, I64, I32], c_size_t),
+    "ss_depth_order": ([P, I32, P, P, c_size_t, P], c_int),
+    "ss_tile_offsets": ([P, P, I32, P, P, c_size_t, P], c_int),
+    "ss_emit_tile_pairs": ([P, P, P, I32, I32, P, P, P], c_int),
+    "ss_sort_tile_pairs": ([P, P, P, P, I64, I32, POINTER(I32), P, c_size_t, P], c_int),
+    "ss_tile_ranges": ([P, I64, I32, P, P], c_int),
+    "ss_raster_fwd": ([P, P, P, P, P, I32, I32, P, P, P, P], c_int),
+    "ss_raster_bwd": ([P, P, P, P, P, I32, I32, P, P, P, P, P], c_int),
+    "ss_project_bwd": ([POINTER(SSStore), P, I32, POINTER(SSCamera), P, P, P, I64, P, P], c_int),
+    "ss_loss_workspace_bytes": ([I32, I32], c_size_t),
+    "ss_loss_l1_ssim": ([P, P, P, P, I32, I32, c_double, P, P, P, c_size_t, P], c_int),
+    "ss_adam_sgld_step": ([P, P, P, P, I64, I32, P, POINTER(SSStepHyper), P, P], c_int),
+    "ss_sgld": ([P, I64, I32, P, POINTER(SSStepHyper), P, P], c_int),
+    "ss_relocate_workspace_bytes": ([I64], c_size_t),
+    "ss_relocate": ([P, P, P, I64, I32, P, c_double, P, c_uint64, c_uint64, P, P, c_size_t, P],
+                    c_int),
+    "ss_to_direct": ([P, P, I64, P], c_int),
+}
+
+_LIB = None
+
+
+class SwingsError(RuntimeError):
+    """A CUDA-side failure reported by libswings.so."""
+
+
+def lib():
+    """Load libswings.so (building it first when sources are newer)."""
+    global _LIB
+    if _LIB is None:
+        if needs_build():
+            build()
+        handle = ctypes.CDLL(str(LIB))
+        for name, (args, res) in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.argtypes = args
+            fn.restype = res
+        _LIB = handle
+    return _LIB
+
+
+def exported_symbols():
+    return list(_SIGNATURES)
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == SS_OK:
+        return
+    msg = lib().ss_last_error().decode(errors="replace")
+    if rc == SS_ERR_INVALID:
+        raise InvalidParameterError(f"{what}: {msg}")
+    raise SwingsError(f"{what}: rc={rc}: {msg}")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None for None)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def camera_struct(cam) -> SSCamera:
+    c = SSCamera()
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    rot = [float(v) for v in cam.rotation.reshape(-1)]
+    tr = [float(v) for v in cam.translation.reshape(-1)]
+    c.rot = (c_double * 9)(*rot)
+    c.trans = (c_double * 3)(*tr)
+    return c

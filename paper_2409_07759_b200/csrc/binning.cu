@@ -1,0 +1,173 @@
+// a-4 binning: the reference's global stable (z, src) order (raster.py:153)
+// restricted per 16x16 tile.
+//
+//   depth order : stable LSD radix sort of 64-bit fp64-z keys (CUB onesweep)
+//   offsets     : tile counts gathered in rank order, exclusive scan -> K
+//   emit        : (tile id, i) pairs written in rank order (warp per splat)
+//   pair sort   : stable radix sort on the tile-id bits only; stability keeps
+//                 rank order inside a tile, so the result equals sorting the
+//                 SURVEY's 34-bit keys tile << 21 | rank
+//   ranges      : boundary detection over the sorted tile ids
+#include <cub/cub.cuh>
+
+#include "ss_common.cuh"
+
+namespace ss {
+
+__global__ void iota_kernel(int32_t* v, int32_t n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+__global__ void gather_counts_kernel(const int32_t* __restrict__ order,
+                                     const int32_t* __restrict__ n_tiles, int32_t n,
+                                     int32_t* __restrict__ out) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) out[k] = n_tiles[order[k]];
+  if (k == n) out[k] = 0;
+}
+
+// One warp per splat in rank order; lanes stride over the splat's tiles.
+__global__ void emit_pairs_kernel(const int32_t* __restrict__ order,
+                                  const int32_t* __restrict__ offsets,
+                                  const int4* __restrict__ bbox, int32_t n, int32_t tiles_x,
+                                  uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (k >= n) return;
+  const int32_t off = offsets[k];
+  const int32_t cnt = offsets[k + 1] - off;
+  if (cnt == 0) return;
+  const int32_t i = order[k];
+  const int4 bb = bbox[i];
+  const int tx0 = bb.x / kTile, tx1 = (bb.y - 1) / kTile + 1;
+  const int ty0 = bb.z / kTile;
+  const int w = tx1 - tx0;
+  for (int j = lane; j < cnt; j += 32) {
+    const int ty = ty0 + j / w, tx = tx0 + j % w;
+    keys[off + j] = (uint32_t)(ty * tiles_x + tx);
+    vals[off + j] = i;
+  }
+}
+
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int64_t n_pairs,
+                                   int2* __restrict__ ranges) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pairs) return;
+  const uint32_t t = keys[p];
+  if (p == 0 || keys[p - 1] != t) ranges[t].x = (int32_t)p;
+  if (p == n_pairs - 1 || keys[p + 1] != t) ranges[t].y = (int32_t)(p + 1);
+}
+
+static int bits_for(int64_t v) {
+  int b = 1;
+  while ((1ll << b) < v) ++b;
+  return b;
+}
+
+}  // namespace ss
+
+using namespace ss;
+
+// Workspace layout: [cub temp | n+1 int32 scratch | n uint64 keys A | n uint64 keys B | n int32 vals]
+static size_t cub_bytes(int32_t n, int64_t max_pairs) {
+  size_t a = 0, b = 0, c = 0;
+  cub::DoubleBuffer<uint64_t> dk(nullptr, nullptr);
+  cub::DoubleBuffer<int32_t> dv(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, a, dk, dv, n > 0 ? n : 1, 0, 64);
+  cub::DoubleBuffer<uint32_t> pk(nullptr, nullptr);
+  cub::DoubleBuffer<int32_t> pv(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, b, pk, pv, (int)(max_pairs > 0 ? max_pairs : 1), 0, 16);
+  cub::DeviceScan::ExclusiveSum(nullptr, c, (int32_t*)nullptr, (int32_t*)nullptr, n + 1);
+  size_t m = a > b ? a : b;
+  return m > c ? m : c;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+extern "C" size_t ss_binning_workspace_bytes(int32_t n, int64_t max_pairs, int32_t n_tiles) {
+  (void)n_tiles;
+  size_t nn = (size_t)(n > 0 ? n : 1);
+  return align256(cub_bytes(n, max_pairs)) + align256((nn + 1) * 4) + 2 * align256(nn * 8) +
+         align256(nn * 4) + 1024;
+}
+
+extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* order, void* ws,
+                              size_t ws_bytes, cudaStream_t stream) {
+  if (n < 0) return set_error(SS_ERR_INVALID, "ss_depth_order: n < 0");
+  if (n == 0) return SS_OK;
+  if (ws_bytes < ss_binning_workspace_bytes(n, 1, 1))
+    return set_error(SS_ERR_WORKSPACE, "ss_depth_order: workspace too small");
+  char* w = (char*)ws;
+  const size_t nn = (size_t)n;
+  const size_t tb = align256(cub_bytes(n, 1));
+  uint64_t* keys_a = (uint64_t*)(w + tb + align256((nn + 1) * 4));
+  uint64_t* keys_b = (uint64_t*)((char*)keys_a + align256(nn * 8));
+  int32_t* vals_in = (int32_t*)((char*)keys_b + align256(nn * 8));
+  cudaMemcpyAsync(keys_a, depth_key, nn * 8, cudaMemcpyDeviceToDevice, stream);
+  iota_kernel<<<grid_for(n, 256), 256, 0, stream>>>(vals_in, n);
+  cub::DoubleBuffer<uint64_t> dk(keys_a, keys_b);
+  cub::DoubleBuffer<int32_t> dv(vals_in, order);
+  size_t tmp_bytes = tb;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(w, tmp_bytes, dk, dv, n, 0, 64, stream);
+  if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_depth_order: %s", cudaGetErrorString(e));
+  if (dv.Current() != order)
+    cudaMemcpyAsync(order, dv.Current(), nn * 4, cudaMemcpyDeviceToDevice, stream);
+  return check_launch("ss_depth_order");
+}
+
+extern "C" int ss_tile_offsets(const int32_t* order, const int32_t* n_tiles, int32_t n,
+                               int32_t* offsets, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  if (n < 0) return set_error(SS_ERR_INVALID, "ss_tile_offsets: n < 0");
+  size_t need = ss_binning_workspace_bytes(n, 1, 1);
+  if (ws_bytes < need) return set_error(SS_ERR_WORKSPACE, "ss_tile_offsets: workspace too small");
+  char* w = (char*)ws;
+  size_t tb = align256(cub_bytes(n, 1));
+  int32_t* cnt = (int32_t*)(w + tb);
+  gather_counts_kernel<<<grid_for(n + 1, 256), 256, 0, stream>>>(order, n_tiles, n, cnt);
+  size_t tmp_bytes = tb;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(w, tmp_bytes, cnt, offsets, n + 1, stream);
+  if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_tile_offsets: %s", cudaGetErrorString(e));
+  return check_launch("ss_tile_offsets");
+}
+
+extern "C" int ss_emit_tile_pairs(const int32_t* order, const int32_t* offsets,
+                                  const int32_t* bbox, int32_t n, int32_t tiles_x, uint32_t* keys,
+                                  int32_t* vals, cudaStream_t stream) {
+  if (n < 0 || tiles_x <= 0) return set_error(SS_ERR_INVALID, "ss_emit_tile_pairs: bad sizes");
+  if (n == 0) return SS_OK;
+  emit_pairs_kernel<<<grid_for((int64_t)n * 32, 256), 256, 0, stream>>>(
+      order, offsets, (const int4*)bbox, n, tiles_x, keys, vals);
+  return check_launch("ss_emit_tile_pairs");
+}
+
+extern "C" int ss_sort_tile_pairs(uint32_t* keys, int32_t* vals, uint32_t* keys_alt,
+                                  int32_t* vals_alt, int64_t n_pairs, int32_t n_tiles,
+                                  int32_t* out_sel, void* ws, size_t ws_bytes,
+                                  cudaStream_t stream) {
+  if (n_pairs < 0 || n_tiles <= 0 || n_pairs > 0x7fffffffll)
+    return set_error(SS_ERR_INVALID, "ss_sort_tile_pairs: bad sizes");
+  *out_sel = 0;
+  if (n_pairs == 0) return SS_OK;
+  cub::DoubleBuffer<uint32_t> dk(keys, keys_alt);
+  cub::DoubleBuffer<int32_t> dv(vals, vals_alt);
+  size_t tmp_bytes = 0;
+  int bits = bits_for(n_tiles);
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int)n_pairs, 0, bits, stream);
+  if (tmp_bytes > ws_bytes) return set_error(SS_ERR_WORKSPACE, "ss_sort_tile_pairs: workspace");
+  cudaError_t e =
+      cub::DeviceRadixSort::SortPairs(ws, tmp_bytes, dk, dv, (int)n_pairs, 0, bits, stream);
+  if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_sort_tile_pairs: %s", cudaGetErrorString(e));
+  *out_sel = dk.selector;
+  return check_launch("ss_sort_tile_pairs");
+}
+
+extern "C" int ss_tile_ranges(const uint32_t* sorted_keys, int64_t n_pairs, int32_t n_tiles,
+                              int32_t* ranges, cudaStream_t stream) {
+  if (n_pairs < 0 || n_tiles <= 0) return set_error(SS_ERR_INVALID, "ss_tile_ranges: bad sizes");
+  cudaMemsetAsync(ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, stream);
+  if (n_pairs > 0)
+    tile_ranges_kernel<<<grid_for(n_pairs, 256), 256, 0, stream>>>(sorted_keys, n_pairs,
+                                                                    (int2*)ranges);
+  return check_launch("ss_tile_ranges");
+}

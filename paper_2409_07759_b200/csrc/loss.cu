@@ -1,0 +1,278 @@
+// a-8 photometric loss: (1-w) L1 + w (1 - SSIM) with its exact image
+// gradient (loss.py:29-60, 73-96).
+//
+// Two shared-memory tiled passes over 32x32 pixel tiles, channel by channel:
+//   pass 1: load x (prediction) and y (ground truth, u8 sRGB through the
+//           256-entry linearisation LUT, raster.py:428-432) with a 5-px halo,
+//           separable 11-tap blur of x, y, xx, xy, yy (zero padding), SSIM
+//           map and its partials ds/dmu, ds/dmxx, ds/dmxy -> global scratch;
+//           per-block fp64 sums of |x - y| and of the SSIM map.
+//   pass 2: separable blur of the three partial maps, combine into
+//           dL/dx = (1-w) sign(x-y)/N - w (B(ds_dmu) + 2x B(ds_dmxx) + y B(ds_dmxy))/N.
+//   pass 3: one block reduces the per-block sums in a fixed order.
+#include "ss_common.cuh"
+
+namespace ss {
+
+constexpr int kLT = 32;             // output tile edge
+constexpr int kHalo = 5;            // 11 taps
+constexpr int kLR = kLT + 2 * kHalo;  // 42: loaded region edge
+constexpr int kLP = kLR + 1;        // padded row pitch
+constexpr int kLossThreads = 256;
+
+__constant__ float c_win[11];
+
+__device__ __forceinline__ float gt_value(const uint8_t* gt_u8, const float* lut,
+                                          const float* gt_f32, int64_t idx) {
+  return gt_u8 ? lut[gt_u8[idx]] : gt_f32[idx];
+}
+
+struct LossArgs {
+  const float* pred;
+  const uint8_t* gt_u8;
+  const float* lut;
+  const float* gt_f32;
+  int width, height;
+  float* maps;        // 3 quantities x 3 channels x H x W
+  double* partials;   // 2 per block
+};
+
+__global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
+  __shared__ float s_x[kLR][kLP];
+  __shared__ float s_y[kLR][kLP];
+  __shared__ float s_v[5][kLT][kLP];
+  __shared__ double s_red[2][kLossThreads / 32];
+  const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
+  const int W = a.width, H = a.height;
+  const int64_t plane = (int64_t)W * H;
+  double l1 = 0.0, ss = 0.0;
+  for (int ch = 0; ch < 3; ++ch) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kLR * kLR; idx += kLossThreads) {
+      const int r = idx / kLR, q = idx % kLR;
+      const int gy = y0 - kHalo + r, gx = x0 - kHalo + q;
+      float xv = 0.f, yv = 0.f;
+      if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+        const int64_t e = ((int64_t)gy * W + gx) * 3 + ch;
+        xv = a.pred[e];
+        yv = gt_value(a.gt_u8, a.lut, a.gt_f32, e);
+      }
+      s_x[r][q] = xv;
+      s_y[r][q] = yv;
+    }
+    __syncthreads();
+    // vertical pass (axis 0, loss.py:31)
+    for (int idx = threadIdx.x; idx < kLT * kLR; idx += kLossThreads) {
+      const int r = idx / kLR, q = idx % kLR;
+      float mx = 0.f, my = 0.f, mxx = 0.f, mxy = 0.f, myy = 0.f;
+#pragma unroll
+      for (int t = 0; t < 11; ++t) {
+        const float w = c_win[t];
+        const float xv = s_x[r + t][q], yv = s_y[r + t][q];
+        mx += w * xv;
+        my += w * yv;
+        mxx += w * (xv * xv);
+        mxy += w * (xv * yv);
+        myy += w * (yv * yv);
+      }
+      s_v[0][r][q] = mx;
+      s_v[1][r][q] = my;
+      s_v[2][r][q] = mxx;
+      s_v[3][r][q] = mxy;
+      s_v[4][r][q] = myy;
+    }
+    __syncthreads();
+    // horizontal pass (axis 1, loss.py:32) + SSIM terms (loss.py:39-59)
+    for (int idx = threadIdx.x; idx < kLT * kLT; idx += kLossThreads) {
+      const int r = idx / kLT, c = idx % kLT;
+      const int gy = y0 + r, gx = x0 + c;
+      if (gy >= H || gx >= W) continue;
+      float mu_x = 0.f, mu_y = 0.f, mxx = 0.f, mxy = 0.f, myy = 0.f;
+#pragma unroll
+      for (int t = 0; t < 11; ++t) {
+        const float w = c_win[t];
+        mu_x += w * s_v[0][r][c + t];
+        mu_y += w * s_v[1][r][c + t];
+        mxx += w * s_v[2][r][c + t];
+        mxy += w * s_v[3][r][c + t];
+        myy += w * s_v[4][r][c + t];
+      }
+      const float C1 = 1e-4f, C2 = 9e-4f;
+      const float sig_x = mxx - mu_x * mu_x;
+      const float sig_y = myy - mu_y * mu_y;
+      const float sig_xy = mxy - mu_x * mu_y;
+      const float a1 = 2.f * mu_x * mu_y + C1;
+      const float a2 = 2.f * sig_xy + C2;
+      const float b1 = mu_x * mu_x + mu_y * mu_y + C1;
+      const float b2 = sig_x + sig_y + C2;
+      const float denom = b1 * b2;
+      const float s = (a1 * a2) / denom;
+      const float ds_dmu = (2.f * mu_y * (a2 - a1) - 2.f * mu_x * s * (b2 - b1)) / denom;
+      const float ds_dmxx = -s / b2;
+      const float ds_dmxy = 2.f * a1 / denom;
+      const int64_t pix = (int64_t)gy * W + gx;
+      a.maps[(0 * 3 + ch) * plane + pix] = ds_dmu;
+      a.maps[(1 * 3 + ch) * plane + pix] = ds_dmxx;
+      a.maps[(2 * 3 + ch) * plane + pix] = ds_dmxy;
+      ss += (double)s;
+      l1 += (double)fabsf(s_x[r + kHalo][c + kHalo] - s_y[r + kHalo][c + kHalo]);
+    }
+  }
+  // block reduction of the two sums (fixed order -> deterministic)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_red[0][threadIdx.x >> 5] = l1;
+    s_red[1][threadIdx.x >> 5] = ss;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int i = 0; i < kLossThreads / 32; ++i) {
+      t0 += s_red[0][i];
+      t1 += s_red[1][i];
+    }
+    const int b = blockIdx.y * gridDim.x + blockIdx.x;
+    a.partials[2 * b] = t0;
+    a.partials[2 * b + 1] = t1;
+  }
+}
+
+__global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, float w_ssim,
+                                                                 float* __restrict__ dimg) {
+  __shared__ float s_m[3][kLR][kLP];
+  __shared__ float s_v[3][kLT][kLP];
+  const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
+  const int W = a.width, H = a.height;
+  const int64_t plane = (int64_t)W * H;
+  const float inv_n = 1.0f / (float)((double)plane * 3.0);
+  for (int ch = 0; ch < 3; ++ch) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kLR * kLR; idx += kLossThreads) {
+      const int r = idx / kLR, q = idx % kLR;
+      const int gy = y0 - kHalo + r, gx = x0 - kHalo + q;
+      const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+      const int64_t pix = (int64_t)gy * W + gx;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) s_m[k][r][q] = in ? a.maps[(k * 3 + ch) * plane + pix] : 0.f;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kLT * kLR; idx += kLossThreads) {
+      const int r = idx / kLR, q = idx % kLR;
+      float v0 = 0.f, v1 = 0.f, v2 = 0.f;
+#pragma unroll
+      for (int t = 0; t < 11; ++t) {
+        const float w = c_win[t];
+        v0 += w * s_m[0][r + t][q];
+        v1 += w * s_m[1][r + t][q];
+        v2 += w * s_m[2][r + t][q];
+      }
+      s_v[0][r][q] = v0;
+      s_v[1][r][q] = v1;
+      s_v[2][r][q] = v2;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kLT * kLT; idx += kLossThreads) {
+      const int r = idx / kLT, c = idx % kLT;
+      const int gy = y0 + r, gx = x0 + c;
+      if (gy >= H || gx >= W) continue;
+      float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+#pragma unroll
+      for (int t = 0; t < 11; ++t) {
+        const float w = c_win[t];
+        b0 += w * s_v[0][r][c + t];
+        b1 += w * s_v[1][r][c + t];
+        b2 += w * s_v[2][r][c + t];
+      }
+      const int64_t e = ((int64_t)gy * W + gx) * 3 + ch;
+      const float x = a.pred[e];
+      const float y = gt_value(a.gt_u8, a.lut, a.gt_f32, e);
+      const float grad = (b0 + 2.f * x * b1 + y * b2) * inv_n;
+      const float d = x - y;
+      const float sgn = (d > 0.f) ? 1.f : ((d < 0.f) ? -1.f : 0.f);
+      dimg[e] = (1.f - w_ssim) * sgn * inv_n - w_ssim * grad;
+    }
+  }
+}
+
+__global__ void loss_reduce_kernel(const double* __restrict__ partials, int n_blocks,
+                                   double* __restrict__ out) {
+  __shared__ double s[2][32];
+  double t0 = 0.0, t1 = 0.0;
+  for (int i = threadIdx.x; i < n_blocks; i += blockDim.x) {
+    t0 += partials[2 * i];
+    t1 += partials[2 * i + 1];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+    t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s[0][threadIdx.x >> 5] = t0;
+    s[1][threadIdx.x >> 5] = t1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      a += s[0][i];
+      b += s[1][i];
+    }
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+static bool g_win_ready = false;
+
+static int ensure_window() {
+  if (g_win_ready) return SS_OK;
+  // loss.py:20-26  normalized 11-tap Gaussian, sigma 1.5 (computed in fp64)
+  double w[11], sum = 0.0;
+  for (int i = 0; i < 11; ++i) {
+    double x = i - 5.0;
+    w[i] = exp(-(x * x) / (2.0 * 1.5 * 1.5));
+    sum += w[i];
+  }
+  float wf[11];
+  for (int i = 0; i < 11; ++i) wf[i] = (float)(w[i] / sum);
+  if (cudaMemcpyToSymbol(c_win, wf, sizeof(wf)) != cudaSuccess)
+    return set_error(SS_ERR_CUDA, "ss_loss: cannot upload blur window");
+  g_win_ready = true;
+  return SS_OK;
+}
+
+}  // namespace ss
+
+using namespace ss;
+
+extern "C" size_t ss_loss_workspace_bytes(int32_t width, int32_t height) {
+  size_t plane = (size_t)width * height;
+  size_t nb = (size_t)((width + kLT - 1) / kLT) * ((height + kLT - 1) / kLT);
+  return 9 * plane * sizeof(float) + 2 * nb * sizeof(double) + 256;
+}
+
+extern "C" int ss_loss_l1_ssim(const float* pred, const uint8_t* gt_u8, const float* lut,
+                               const float* gt_f32, int32_t width, int32_t height,
+                               double ssim_weight, float* dimg, double* out_sums, void* ws,
+                               size_t ws_bytes, cudaStream_t stream) {
+  if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_loss: bad size");
+  if (!gt_u8 && !gt_f32) return set_error(SS_ERR_INVALID, "ss_loss: no ground truth");
+  if (gt_u8 && !lut) return set_error(SS_ERR_INVALID, "ss_loss: u8 ground truth needs a LUT");
+  if (ws_bytes < ss_loss_workspace_bytes(width, height))
+    return set_error(SS_ERR_WORKSPACE, "ss_loss: workspace too small");
+  int rc = ensure_window();
+  if (rc) return rc;
+  dim3 grid((width + kLT - 1) / kLT, (height + kLT - 1) / kLT);
+  const size_t plane = (size_t)width * height;
+  LossArgs a{pred, gt_u8, lut, gt_f32, width, height, (float*)ws,
+             (double*)((char*)ws + ((9 * plane * sizeof(float) + 255) & ~(size_t)255))};
+  ssim_fwd_kernel<<<grid, kLossThreads, 0, stream>>>(a);
+  ssim_bwd_kernel<<<grid, kLossThreads, 0, stream>>>(a, (float)ssim_weight, dimg);
+  loss_reduce_kernel<<<1, 1024, 0, stream>>>(a.partials, grid.x * grid.y, out_sums);
+  return check_launch("ss_loss_l1_ssim");
+}

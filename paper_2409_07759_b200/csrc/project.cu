@@ -1,0 +1,315 @@
+// a-3 EWA projection (raster.py:76-173) and a-7 its backward chain
+// (raster.py:249-348).  One thread per active Gaussian, fp64 throughout so
+// the structural outputs (cull set, bbox, depth order) match the reference;
+// the rasterizer record is rounded to fp32 once.
+#include "ss_common.cuh"
+
+namespace ss {
+
+struct CamK {
+  int32_t width, height;
+  double fx, fy, cx, cy;
+  double R[3][3];
+  double T[3];
+};
+
+static CamK to_camk(const ss_camera* c) {
+  CamK k;
+  k.width = c->width;
+  k.height = c->height;
+  k.fx = c->fx;
+  k.fy = c->fy;
+  k.cx = c->cx;
+  k.cy = c->cy;
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) k.R[i][j] = c->rot[3 * i + j];
+    k.T[i] = c->trans[i];
+  }
+  return k;
+}
+
+// Everything the forward computes and the backward re-derives.
+struct Proj {
+  double t[3];
+  double z, ux, uy;
+  double qnorm, qn[4], rq[3][3], m3[3][3], sigma[3][3], mproj[2][3];
+  double a, b, c;  // raw cov2d
+  bool keep;
+};
+
+__device__ __forceinline__ void project_one(const CamK& cam, const Gauss64& g, Proj& p) {
+  // raster.py:86  t = mean R^T + T
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+    p.t[j] = dadd(dadd(dadd(dmul(g.mean[0], cam.R[j][0]), dmul(g.mean[1], cam.R[j][1])),
+                       dmul(g.mean[2], cam.R[j][2])),
+                  cam.T[j]);
+  p.z = p.t[2];
+  const bool in_front = p.z > kNearPlane;  // raster.py:88
+  // raster.py:91-92
+  p.ux = dadd(ddiv(dmul(cam.fx, p.t[0]), p.z), cam.cx);
+  p.uy = dadd(ddiv(dmul(cam.fy, p.t[1]), p.z), cam.cy);
+  // raster.py:94-98
+  const double* q = g.quat;
+  p.qnorm = sqrt(dadd(dadd(dadd(dmul(q[0], q[0]), dmul(q[1], q[1])), dmul(q[2], q[2])),
+                      dmul(q[3], q[3])));
+  const double qd = fmax(p.qnorm, 1e-12);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) p.qn[k] = ddiv(q[k], qd);
+  quat_to_rot(p.qn, p.rq);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) p.m3[a][b] = dmul(p.rq[a][b], g.scale[b]);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      p.sigma[a][c] = dadd(dadd(dmul(p.m3[a][0], p.m3[c][0]), dmul(p.m3[a][1], p.m3[c][1])),
+                           dmul(p.m3[a][2], p.m3[c][2]));
+  // raster.py:101-107  J (2x3) and M = J W
+  const double z2 = dmul(p.z, p.z);
+  double J[2][3] = {{ddiv(cam.fx, p.z), 0.0, ddiv(dmul(-cam.fx, p.t[0]), z2)},
+                    {0.0, ddiv(cam.fy, p.z), ddiv(dmul(-cam.fy, p.t[1]), z2)}};
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      p.mproj[a][c] = dadd(dadd(dmul(J[a][0], cam.R[0][c]), dmul(J[a][1], cam.R[1][c])),
+                           dmul(J[a][2], cam.R[2][c]));
+  // raster.py:108  cov2d = M Sigma M^T
+  double cov[2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      double acc = 0.0;
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          acc = dadd(acc, dmul(dmul(p.mproj[a][b], p.sigma[b][c]), p.mproj[d][c]));
+      cov[a][d] = acc;
+    }
+  p.a = cov[0][0];
+  p.b = cov[0][1];
+  p.c = cov[1][1];
+  // raster.py:114-124  3-sigma cull on the raw covariance
+  const double mid = dmul(0.5, dadd(p.a, p.c));
+  const double disc =
+      sqrt(fmax(dsub(dmul(mid, mid), dsub(dmul(p.a, p.c), dmul(p.b, p.b))), 0.0));
+  const double r3 = dmul(3.0, sqrt(fmax(dadd(mid, disc), 0.0)));
+  const bool on_image = (dadd(p.ux, r3) >= 0.0) && (dsub(p.ux, r3) <= cam.width - 1.0) &&
+                        (dadd(p.uy, r3) >= 0.0) && (dsub(p.uy, r3) <= cam.height - 1.0);
+  p.keep = in_front && on_image;
+}
+
+__global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ rows, int32_t n,
+                                   CamK cam, float4* __restrict__ rec_a,
+                                   float4* __restrict__ rec_b, float* __restrict__ rec_c,
+                                   uint64_t* __restrict__ depth_key, int4* __restrict__ bbox,
+                                   int32_t* __restrict__ n_tiles) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t row = rows ? rows[i] : i;
+  Gauss64 g;
+  load_row(store, row, g);
+  Proj p;
+  project_one(cam, g, p);
+  if (!p.keep) {
+    depth_key[i] = ~0ull;
+    n_tiles[i] = 0;
+    bbox[i] = make_int4(0, 0, 0, 0);
+    rec_a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    rec_b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    rec_c[i] = 0.f;
+    return;
+  }
+  // raster.py:139-150  dilation, conic, 8-sigma bbox of the dilated covariance
+  const double ad = dadd(p.a, kDilation), cd = dadd(p.c, kDilation);
+  const double det = dsub(dmul(ad, cd), dmul(p.b, p.b));
+  const double i0 = ddiv(cd, det), i1 = ddiv(-p.b, det), i2 = ddiv(ad, det);
+  const double mid_d = dmul(0.5, dadd(ad, cd));
+  const double disc_d = sqrt(fmax(dsub(dmul(mid_d, mid_d), det), 0.0));
+  const double r8 = dmul(8.0, sqrt(dadd(mid_d, disc_d)));
+  const int x0 = (int)fmax(ceil(dsub(p.ux, r8)), 0.0);
+  const int x1 = (int)fmin(dadd(floor(dadd(p.ux, r8)), 1.0), (double)cam.width);
+  const int y0 = (int)fmax(ceil(dsub(p.uy, r8)), 0.0);
+  const int y1 = (int)fmin(dadd(floor(dadd(p.uy, r8)), 1.0), (double)cam.height);
+  bbox[i] = make_int4(x0, x1, y0, y1);
+  int nt = 0;
+  if (x1 > x0 && y1 > y0) {
+    const int tx0 = x0 / kTile, tx1 = (x1 - 1) / kTile + 1;
+    const int ty0 = y0 / kTile, ty1 = (y1 - 1) / kTile + 1;
+    nt = (tx1 - tx0) * (ty1 - ty0);
+  }
+  n_tiles[i] = nt;
+  depth_key[i] = (uint64_t)__double_as_longlong(p.z);  // z > 0.01: bits are monotone
+  rec_a[i] = make_float4((float)p.ux, (float)p.uy, (float)i0, (float)i1);
+  rec_b[i] = make_float4((float)i2, (float)g.opacity, (float)g.color[0], (float)g.color[1]);
+  rec_c[i] = (float)g.color[2];
+}
+
+__global__ void project_bwd_kernel(StoreView store, const int32_t* __restrict__ rows, int32_t n,
+                                   CamK cam, const float* __restrict__ g2d,
+                                   const uint64_t* __restrict__ depth_key,
+                                   const uint8_t* __restrict__ mask, int64_t trainable_rows,
+                                   float* __restrict__ grads) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (depth_key[i] == ~0ull) return;  // culled
+  if (mask && !mask[i]) return;
+  const int32_t row = rows ? rows[i] : i;
+  if (row >= trainable_rows) return;
+  Gauss64 g;
+  load_row(store, row, g);
+  Proj p;
+  project_one(cam, g, p);
+  const float* gg = g2d + (int64_t)i * SS_G2D_ROW;
+  const double gm2x = gg[0], gm2y = gg[1];
+  const double gia = gg[2], gib = gg[3], gic = gg[4];
+  const double g_alpha = gg[5];
+  const double ad = p.a + kDilation, cd = p.c + kDilation, b = p.b;
+  const double det = ad * cd - b * b;
+  const double det2 = det * det;
+  // raster.py:262-266
+  const double g_a = (gia * (-cd * cd) + gib * (b * cd) + gic * (-b * b)) / det2;
+  const double g_b = (gia * (2.0 * b * cd) + gib * (-det - 2.0 * b * b) + gic * (2.0 * ad * b)) / det2;
+  const double g_c = (gia * (-b * b) + gib * (ad * b) + gic * (-ad * ad)) / det2;
+  // raster.py:269-280
+  double sm0[3], sm1[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    sm0[r] = p.sigma[r][0] * p.mproj[0][0] + p.sigma[r][1] * p.mproj[0][1] + p.sigma[r][2] * p.mproj[0][2];
+    sm1[r] = p.sigma[r][0] * p.mproj[1][0] + p.sigma[r][1] * p.mproj[1][1] + p.sigma[r][2] * p.mproj[1][2];
+  }
+  double gm[2][3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    gm[0][k] = 2.0 * g_a * sm0[k] + g_b * sm1[k];
+    gm[1][k] = g_b * sm0[k] + 2.0 * g_c * sm1[k];
+  }
+  double gs[3][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      gs[r][c] = g_a * p.mproj[0][r] * p.mproj[0][c] + g_b * p.mproj[0][r] * p.mproj[1][c] +
+                 g_c * p.mproj[1][r] * p.mproj[1][c];
+  // raster.py:283-300  through J entries and the projected centre to camera t
+  double gj[2][3];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      gj[r][c] = gm[r][0] * cam.R[c][0] + gm[r][1] * cam.R[c][1] + gm[r][2] * cam.R[c][2];
+  const double z = p.z, z2 = z * z, z3 = z2 * z;
+  const double xc = p.t[0], yc = p.t[1];
+  double gt[3];
+  gt[0] = gj[0][2] * (-cam.fx / z2);
+  gt[1] = gj[1][2] * (-cam.fy / z2);
+  gt[2] = gj[0][0] * (-cam.fx / z2) + gj[1][1] * (-cam.fy / z2) +
+          gj[0][2] * (2.0 * cam.fx * xc / z3) + gj[1][2] * (2.0 * cam.fy * yc / z3);
+  gt[0] += gm2x * cam.fx / z;
+  gt[1] += gm2y * cam.fy / z;
+  gt[2] += -gm2x * cam.fx * xc / z2 - gm2y * cam.fy * yc / z2;
+  float* out = grads + (int64_t)row * SS_GRAD_ROW;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    out[c] = (float)(gt[0] * cam.R[0][c] + gt[1] * cam.R[1][c] + gt[2] * cam.R[2][c]);
+  // raster.py:303-306  Sigma = M3 M3^T, M3 = R diag(s)
+  double gm3[3][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      gm3[r][k] = (gs[r][0] + gs[0][r]) * p.m3[0][k] + (gs[r][1] + gs[1][r]) * p.m3[1][k] +
+                  (gs[r][2] + gs[2][r]) * p.m3[2][k];
+  double gr[3][3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double g_scale = gm3[0][k] * p.rq[0][k] + gm3[1][k] * p.rq[1][k] + gm3[2][k] * p.rq[2][k];
+    out[7 + k] = (float)(g_scale * g.scale[k]);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) gr[r][k] = gm3[r][k] * g.scale[k];
+  }
+  // raster.py:308-334  dR/dq, then through the normalization
+  const double w = p.qn[0], x = p.qn[1], y = p.qn[2], zz = p.qn[3];
+  const double dr[4][3][3] = {
+      {{0.0, -zz, y}, {zz, 0.0, -x}, {-y, x, 0.0}},
+      {{0.0, y, zz}, {y, -2 * x, -w}, {zz, w, -2 * x}},
+      {{-2 * y, x, w}, {x, 0.0, zz}, {-w, zz, -2 * y}},
+      {{-2 * zz, -w, x}, {w, -2 * zz, y}, {x, y, 0.0}}};
+  double gqn[4];
+#pragma unroll
+  for (int qi = 0; qi < 4; ++qi) {
+    double acc = 0.0;
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) acc += gr[r][k] * (2.0 * dr[qi][r][k]);
+    gqn[qi] = acc;
+  }
+  const double dot = p.qn[0] * gqn[0] + p.qn[1] * gqn[1] + p.qn[2] * gqn[2] + p.qn[3] * gqn[3];
+#pragma unroll
+  for (int qi = 0; qi < 4; ++qi) out[3 + qi] = (float)((gqn[qi] - p.qn[qi] * dot) / p.qnorm);
+  // raster.py:336-343
+  out[10] = (float)(g_alpha * g.opacity * (1.0 - g.opacity));
+  out[11] = gg[6];
+  out[12] = gg[7];
+  out[13] = gg[8];
+}
+
+__global__ void to_direct_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                 int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* s = src + i * SS_ROW;
+  double* d = dst + i * SS_ROW;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) d[k] = s[k];
+#pragma unroll
+  for (int k = 7; k < 10; ++k) d[k] = exp(s[k]);
+  d[10] = 1.0 / (1.0 + exp(-s[10]));
+#pragma unroll
+  for (int k = 11; k < 14; ++k) d[k] = s[k];
+}
+
+}  // namespace ss
+
+using namespace ss;
+
+extern "C" int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_t n,
+                              const ss_camera* cam, void* rec_a, void* rec_b, float* rec_c,
+                              uint64_t* depth_key, int32_t* bbox, int32_t* n_tiles,
+                              cudaStream_t stream) {
+  if (!store || !cam || n < 0) return set_error(SS_ERR_INVALID, "ss_project_fwd: bad arguments");
+  if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0) || !(cam->fy > 0))
+    return set_error(SS_ERR_INVALID, "ss_project_fwd: bad camera");
+  if (n == 0) return SS_OK;
+  StoreView sv{store->opt, store->n_opt, store->mat};
+  project_fwd_kernel<<<grid_for(n, 128), 128, 0, stream>>>(
+      sv, rows, n, to_camk(cam), (float4*)rec_a, (float4*)rec_b, rec_c, depth_key, (int4*)bbox,
+      n_tiles);
+  return check_launch("ss_project_fwd");
+}
+
+extern "C" int ss_project_bwd(const ss_store* store, const int32_t* rows, int32_t n,
+                              const ss_camera* cam, const float* g2d, const uint64_t* depth_key,
+                              const uint8_t* trainable_mask, int64_t trainable_rows,
+                              float* grads, cudaStream_t stream) {
+  if (!store || !cam || n < 0) return set_error(SS_ERR_INVALID, "ss_project_bwd: bad arguments");
+  if (n == 0) return SS_OK;
+  StoreView sv{store->opt, store->n_opt, store->mat};
+  project_bwd_kernel<<<grid_for(n, 128), 128, 0, stream>>>(sv, rows, n, to_camk(cam), g2d,
+                                                            depth_key, trainable_mask,
+                                                            trainable_rows, grads);
+  return check_launch("ss_project_bwd");
+}
+
+extern "C" int ss_to_direct(const double* src, double* dst, int64_t n, cudaStream_t stream) {
+  if (n < 0) return set_error(SS_ERR_INVALID, "ss_to_direct: n < 0");
+  if (n == 0) return SS_OK;
+  to_direct_kernel<<<grid_for(n, 256), 256, 0, stream>>>(src, dst, n);
+  return check_launch("ss_to_direct");
+}

@@ -1,0 +1,113 @@
+// Shared helpers for the libswings.so kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/swings.h"
+
+namespace ss {
+
+constexpr float kAlphaMax = 0.999f;       // _kernels.py:15
+constexpr float kTMin = 1e-4f;            // _kernels.py:16
+constexpr float kMahaMax = 64.0f;         // _kernels.py:17
+constexpr double kNearPlane = 0.01;       // raster.py:31
+constexpr double kDilation = 0.3;         // raster.py:34
+constexpr int kTile = SS_TILE;
+constexpr int kTilePix = kTile * kTile;
+
+int set_error(int code, const char* fmt, ...);
+int check_launch(const char* what);
+
+inline int grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// Row accessor: r < n_opt -> optimizable row (log-scale, logit); else matured.
+struct StoreView {
+  const double* opt;
+  int64_t n_opt;
+  const double* mat;
+};
+
+// Gaussian in direct space, fp64 (core.py:153-176).
+struct Gauss64 {
+  double mean[3];
+  double quat[4];
+  double scale[3];
+  double opacity;
+  double color[3];
+};
+
+__device__ __forceinline__ void load_row(const StoreView& s, int32_t row, Gauss64& g) {
+  const bool opt = row < s.n_opt;
+  const double* p = opt ? s.opt + (int64_t)row * SS_ROW : s.mat + (int64_t)(row - s.n_opt) * SS_ROW;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g.mean[k] = p[k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) g.quat[k] = p[3 + k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g.scale[k] = p[7 + k];
+  g.opacity = p[10];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g.color[k] = p[11 + k];
+  if (opt) {
+    // train.py:155-161: exp(log_scale), 1 / (1 + exp(-logit))
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g.scale[k] = exp(g.scale[k]);
+    g.opacity = 1.0 / (1.0 + exp(-g.opacity));
+  }
+}
+
+// Non-contracted fp64 helpers: structural quantities (z, cull, bbox) follow
+// numpy's separate multiply/add roundings rather than fused FMAs.
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// core.py:231-251 rotation matrix of a unit (w, x, y, z) quaternion, with
+// numpy's rounding sequence (no FMA contraction).
+__device__ __forceinline__ void quat_to_rot(const double q[4], double r[3][3]) {
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  r[0][0] = dsub(1.0, dmul(2.0, dadd(dmul(y, y), dmul(z, z))));
+  r[0][1] = dmul(2.0, dsub(dmul(x, y), dmul(w, z)));
+  r[0][2] = dmul(2.0, dadd(dmul(x, z), dmul(w, y)));
+  r[1][0] = dmul(2.0, dadd(dmul(x, y), dmul(w, z)));
+  r[1][1] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(z, z))));
+  r[1][2] = dmul(2.0, dsub(dmul(y, z), dmul(w, x)));
+  r[2][0] = dmul(2.0, dsub(dmul(x, z), dmul(w, y)));
+  r[2][1] = dmul(2.0, dadd(dmul(y, z), dmul(w, x)));
+  r[2][2] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(y, y))));
+}
+
+// Philox4x32-10 counter-based generator (Salmon et al., SC'11).
+struct Philox4 {
+  uint32_t v[4];
+};
+
+__device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
+                                                  uint32_t c3, uint32_t k0, uint32_t k1) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    uint32_t hi0 = __umulhi(M0, c0), lo0 = M0 * c0;
+    uint32_t hi1 = __umulhi(M1, c2), lo1 = M1 * c2;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    k0 += W0; k1 += W1;
+  }
+  Philox4 r;
+  r.v[0] = c0; r.v[1] = c1; r.v[2] = c2; r.v[3] = c3;
+  return r;
+}
+
+// Uniform in (0, 1] from 32 random bits, fp64 (53-bit from two words).
+__device__ __forceinline__ double u01_53(uint32_t a, uint32_t b) {
+  uint64_t x = ((uint64_t)(a >> 5) << 26) | (uint64_t)(b >> 6);   // 27 + 26 = 53 bits
+  return ((double)x + 1.0) * (1.0 / 9007199254740992.0);
+}
+
+}  // namespace ss

@@ -1,0 +1,395 @@
+"""GPU-resident training state and the per-iteration step (train.py:374-417).
+
+DeviceModel owns
+  opt     (num_gs, 14) f64  optimizable rows, generation i = rows [i*sl, (i+1)*sl)
+  m, v    (num_gs, 14) f64  Adam moments
+  grads   (num_gs, 14) f32  optimization-space gradient (NCCL allreduce buffer)
+  mat     ((swin+1)*sl, 14) f64  ring of matured, direct-space generations
+  row_start / row_expire    per-row lifespans (opt rows, then matured ring rows)
+and sequences the libswings.so calls of one training view.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .core import GaussianArrays
+from .engine import LossBuffers, Store, ViewPipeline, device
+from .raster import srgb_u8_lut
+
+log = logging.getLogger("paper_2409_07759_b200.train")
+
+GEN_DTYPE = np.dtype([("active", "<i4"), ("pad", "<i4"), ("bc1", "<f8"), ("bc2", "<f8"),
+                      ("gscale", "<f8")])
+assert GEN_DTYPE.itemsize == ctypes.sizeof(L.SSGenStep)
+PARAM_KEYS = ("mean", "quat", "log_scale", "opacity_logit", "color")
+COLS = {"mean": (0, 3), "quat": (3, 7), "log_scale": (7, 10), "opacity_logit": (10, 11),
+        "color": (11, 14)}
+
+
+def _views(t: torch.Tensor) -> dict:
+    out = {}
+    for k, (a, b) in COLS.items():
+        out[k] = t[:, a] if b - a == 1 else t[:, a:b]
+    return out
+
+
+def _pack(params: dict) -> np.ndarray:
+    return np.concatenate([np.asarray(params["mean"]), np.asarray(params["quat"]),
+                           np.asarray(params["log_scale"]),
+                           np.asarray(params["opacity_logit"])[:, None],
+                           np.asarray(params["color"])], axis=1).astype(np.float64)
+
+
+def _unpack_into(params: dict, rows: np.ndarray) -> None:
+    for k, (a, b) in COLS.items():
+        src = rows[:, a] if b - a == 1 else rows[:, a:b]
+        params[k][...] = src
+
+
+def _hyper(cfg, n_reg: float, sgld: bool, seed: int, counter: int) -> L.SSStepHyper:
+    h = L.SSStepHyper()
+    h.lr = (ctypes.c_double * 5)(cfg.lr_mean, cfg.lr_quat, cfg.lr_log_scale,
+                                 cfg.lr_opacity_logit, cfg.lr_color)
+    h.beta1, h.beta2, h.eps = cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps
+    h.opacity_reg, h.scale_reg = cfg.opacity_reg, cfg.scale_reg
+    h.n_reg = float(max(n_reg, 1))
+    h.noise_scale = cfg.noise_lr * cfg.lr_mean
+    h.gate_center, h.gate_sharpness = cfg.noise_gate_center, cfg.noise_gate_sharpness
+    h.sgd = 1 if cfg.optimizer == "sgd" else 0
+    h.sgld = 1 if sgld else 0
+    h.seed = seed & 0xFFFFFFFFFFFFFFFF
+    h.counter = counter & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def philox_seed(rng_seed: int) -> int:
+    """Philox key derived from TrainConfig.rng_seed (splitmix64)."""
+    z = (int(rng_seed) + 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+    return z ^ (z >> 31)
+
+
+class DeviceModel:
+    def __init__(self, state):
+        cfg = state.config
+        self.state, self.cfg = state, cfg
+        self.dev = device()
+        L.lib()
+        sl, swin, num_gs = cfg.slice_size, cfg.swin_size, cfg.num_gs
+        self.sl, self.swin, self.num_gs = sl, swin, num_gs
+        dev = self.dev
+        self.opt = torch.empty((num_gs, L.SS_ROW), dtype=torch.float64, device=dev)
+        self.m = torch.zeros_like(self.opt)
+        self.v = torch.zeros_like(self.opt)
+        self.grads = torch.zeros((num_gs, L.SS_GRAD_ROW), dtype=torch.float32, device=dev)
+        for i, gen in enumerate(state.slices):
+            r0, r1 = i * sl, (i + 1) * sl
+            self.opt[r0:r1] = torch.from_numpy(_pack(gen.params))
+            self.m[r0:r1] = torch.from_numpy(_pack(gen.adam_m))
+            self.v[r0:r1] = torch.from_numpy(_pack(gen.adam_v))
+            gen.params = _views(self.opt[r0:r1])
+            gen.adam_m = _views(self.m[r0:r1])
+            gen.adam_v = _views(self.v[r0:r1])
+            gen._rows = (self.opt, r0, r1)
+        self.n_blocks = swin + 1
+        self.mat = torch.zeros((self.n_blocks * sl, L.SS_ROW), dtype=torch.float64, device=dev)
+        self.free_blocks = list(range(self.n_blocks))
+        for mg in state.matured:  # host-only archive entries (state moved late)
+            mg.block = self.free_blocks.pop(0)
+            self.mat[mg.block * sl:(mg.block + 1) * sl] = torch.from_numpy(mg.arrays.rows())
+        n_rows_all = num_gs + self.n_blocks * sl
+        self.row_start = torch.zeros(n_rows_all, dtype=torch.int32, device=dev)
+        self.row_expire = torch.zeros(n_rows_all, dtype=torch.int32, device=dev)
+        self.blk_map = torch.zeros(self.n_blocks, dtype=torch.int32, device=dev)
+        self.active_rows = torch.empty(n_rows_all, dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(2, dtype=torch.int32, device=dev)
+        lib = L.lib()
+        self.ws_compact = torch.empty(int(lib.ss_compact_workspace_bytes(n_rows_all)),
+                                      dtype=torch.uint8, device=dev)
+        self.gen_host = torch.zeros(swin * GEN_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+        self.gen_dev = torch.zeros(swin * GEN_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        self.reloc_ws = torch.empty(int(lib.ss_relocate_workspace_bytes(num_gs)),
+                                    dtype=torch.uint8, device=dev)
+        self.reloc_counts = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.eta = None
+        self.pipe = ViewPipeline()
+        self.lossbuf = LossBuffers()
+        self.lut = torch.from_numpy(srgb_u8_lut().astype(np.float32)).to(dev)
+        self.seed = philox_seed(cfg.rng_seed)
+        self.store = Store(opt=self.opt, mat=self.mat)
+        self.dirty = True
+        self.last_sums = None
+        self.last_counts = (0, 0)
+
+    # ------------------------------------------------------------ bookkeeping
+    def mark_lifespans_dirty(self):
+        self.dirty = True
+
+    def sync_lifespans(self):
+        sl, n_opt = self.sl, self.num_gs
+        for i, gen in enumerate(self.state.slices):
+            self.row_start[i * sl:(i + 1) * sl].fill_(gen.lifespan.start)
+            self.row_expire[i * sl:(i + 1) * sl].fill_(gen.lifespan.expire)
+        for mg in self.state.matured:
+            r0 = n_opt + mg.block * sl
+            self.row_start[r0:r0 + sl].fill_(mg.lifespan.start)
+            self.row_expire[r0:r0 + sl].fill_(mg.lifespan.expire)
+        blocks = [mg.block for mg in self.state.matured]
+        if blocks:
+            self.blk_map[: len(blocks)].copy_(torch.tensor(blocks, dtype=torch.int32))
+        self.dirty = False
+
+    def freeze(self, gen):
+        """Direct-space snapshot of `gen` into a free matured block; returns
+        (block, host GaussianArrays of the same bytes)."""
+        block = self.free_blocks.pop(0)
+        _, r0, r1 = gen._rows
+        dst = self.mat[block * self.sl:(block + 1) * self.sl]
+        L.check(L.lib().ss_to_direct(L.ptr(self.opt[r0:r1]), L.ptr(dst), r1 - r0, L.stream_ptr()),
+                "to_direct")
+        return block, GaussianArrays.from_rows(dst.cpu().numpy())
+
+    def release_block(self, block: int):
+        if block >= 0:
+            self.free_blocks.append(block)
+
+    def _gen_table(self, stepped):
+        cfg = self.cfg
+        tab = self.gen_host.numpy().view(GEN_DTYPE)
+        for i, gen in enumerate(self.state.slices):
+            e = tab[i]
+            if stepped[i]:
+                if cfg.optimizer == "adam":
+                    gen.adam_t += 1
+                t = max(gen.adam_t, 1)
+                e["active"] = 1
+                e["bc1"] = 1.0 - cfg.adam_beta1 ** t
+                e["bc2"] = 1.0 - cfg.adam_beta2 ** t
+                e["gscale"] = (cfg.gradient_scale_decay ** gen.windows_trained
+                               if cfg.gradient_scaling else 1.0)
+            else:
+                e["active"] = 0
+        # the copy completes before the next step rewrites gen_host: every step
+        # synchronizes once (tile-pair count readback) after this point
+        self.gen_dev.copy_(self.gen_host, non_blocking=True)
+
+    # ------------------------------------------------------------------ step
+    def train_step(self, draws, rank, dataset, it):
+        """One training view (train.py:375-417).  `draws` are the (frame, view)
+        samples of every data-parallel rank this iteration; this rank renders
+        draws[rank]; generations active in any drawn frame are stepped."""
+        state, cfg, sl = self.state, self.cfg, self.sl
+        lib = L.lib()
+        sp = L.stream_ptr()
+        if self.dirty:
+            self.sync_lifespans()
+        frame, view = draws[rank]
+        frames = [f for f, _ in draws]
+        live = lambda ls, f: ls.start <= f < ls.expire  # noqa: E731
+        stepped = [any(live(g.lifespan, f) for f in frames) for g in state.slices]
+        self._gen_table(stepped)
+        n_opt_here = sl * sum(live(g.lifespan, frame) for g in state.slices)
+        n_mat_here = sl * sum(live(m.lifespan, frame) for m in state.matured)
+        n = n_opt_here + n_mat_here
+        L.check(lib.ss_compact_active(L.ptr(self.row_start), L.ptr(self.row_expire), self.num_gs,
+                                      len(state.matured) * sl, L.ptr(self.blk_map), sl, frame,
+                                      L.ptr(self.active_rows), L.ptr(self.counts),
+                                      L.ptr(self.ws_compact), self.ws_compact.numel(), sp),
+                "compact_active")
+        self.grads.zero_()
+        cam = dataset.cameras[view]
+        gt = dataset.device_frame(frame, view)
+        img = self.pipe.forward(self.store, self.active_rows, n, cam)
+        dimg, sums = self.lossbuf.run(img, cam.height, cam.width, gt_u8=gt, lut=self.lut,
+                                      ssim_weight=cfg.ssim_weight)
+        self.pipe.backward(dimg, self.grads, trainable_rows=self.num_gs)
+        if state.dp is not None:
+            state.dp.allreduce_grads(self.grads)
+        n_reg = sl * sum(stepped)
+        eta = None
+        if state.noise_source == "numpy":
+            eta = self._numpy_eta(stepped)
+        h = _hyper(cfg, n_reg, True, self.seed, state.iteration)
+        L.check(lib.ss_adam_sgld_step(L.ptr(self.opt), L.ptr(self.grads), L.ptr(self.m),
+                                      L.ptr(self.v), self.num_gs, sl, L.ptr(self.gen_dev),
+                                      ctypes.byref(h), L.ptr(eta), sp), "adam_sgld_step")
+        if it % cfg.relocate_period == 0:
+            self.relocate_device(cfg.dead_opacity_threshold)
+        state.iteration += 1
+        self.last_sums = sums
+        self.last_counts = (n, n_opt_here)
+        return sums
+
+    def _numpy_eta(self, stepped):
+        """eta drawn per stepped generation in list order (train.py:255-258)."""
+        if self.eta is None:
+            self.eta = torch.zeros((self.num_gs, 3), dtype=torch.float64, device=self.dev)
+        sl = self.sl
+        for i, gen in enumerate(self.state.slices):
+            if stepped[i]:
+                e = self.state.rng.standard_normal((sl, 3))
+                self.eta[i * sl:(i + 1) * sl].copy_(torch.from_numpy(e))
+        return self.eta
+
+    def relocate_device(self, threshold: float, uniforms_rng=None) -> int | None:
+        """MCMC relocation over the generations flagged in the current gen
+        table (train.py:267-318).  Philox uniforms unless the state draws from
+        numpy, in which case the reference's choice() uniforms are consumed."""
+        state = self.state
+        lib = L.lib()
+        sp = L.stream_ptr()
+        uniforms = None
+        if state.noise_source == "numpy":
+            tab = self.gen_host.numpy().view(GEN_DTYPE)
+            rows = torch.cat([torch.arange(i * self.sl, (i + 1) * self.sl, device=self.dev)
+                              for i in range(len(state.slices)) if tab[i]["active"]] or
+                             [torch.zeros(0, dtype=torch.int64, device=self.dev)])
+            alpha = 1.0 / (1.0 + torch.exp(-self.opt[rows, 10]))
+            n_dead = int((alpha < threshold).sum().item())
+            n_alive = int(rows.numel()) - n_dead
+            if n_dead == 0:
+                return 0
+            if n_alive == 0:
+                log.warning("relocation skipped: no alive splats above threshold %.4g", threshold)
+                return 0
+            uniforms = torch.from_numpy(state.rng.random(n_dead)).to(self.dev)
+        L.check(lib.ss_relocate(L.ptr(self.opt), L.ptr(self.m), L.ptr(self.v), self.num_gs, self.sl,
+                                L.ptr(self.gen_dev), float(threshold), L.ptr(uniforms), self.seed,
+                                state.iteration, L.ptr(self.reloc_counts), L.ptr(self.reloc_ws),
+                                self.reloc_ws.numel(), sp), "relocate")
+        return None
+
+
+# ---------------------------------------------------------------------------
+# reference-API entry points on explicit generation lists (host or device)
+# ---------------------------------------------------------------------------
+
+def to_direct_host(params) -> GaussianArrays:
+    t = torch.cat([params["mean"], params["quat"], params["log_scale"],
+                   params["opacity_logit"][:, None], params["color"]], dim=1).contiguous()
+    out = torch.empty_like(t)
+    L.check(L.lib().ss_to_direct(L.ptr(t), L.ptr(out), t.shape[0], L.stream_ptr()), "to_direct")
+    return GaussianArrays.from_rows(out.cpu().numpy())
+
+
+class _Batch:
+    """Concatenate the rows of a list of generations onto the device, run
+    kernels on them, and write results back (numpy in place, or torch views)."""
+
+    def __init__(self, gens):
+        self.gens = gens
+        self.sizes = [len(g.params["mean"]) for g in gens]
+        dev = device()
+        parts = []
+        for g in gens:
+            if g.on_device:
+                parts.append(torch.cat([g.params[k].reshape(len(g.params["mean"]), -1)
+                                        for k in PARAM_KEYS], 1))
+            else:
+                parts.append(torch.from_numpy(_pack(g.params)).to(dev))
+        self.t = torch.cat(parts).contiguous() if parts else torch.zeros((0, 14), device=dev,
+                                                                         dtype=torch.float64)
+
+    def moments(self):
+        dev = device()
+        ms, vs = [], []
+        for g in self.gens:
+            if g.on_device:
+                ms.append(torch.cat([g.adam_m[k].reshape(len(g.params["mean"]), -1)
+                                     for k in PARAM_KEYS], 1))
+                vs.append(torch.cat([g.adam_v[k].reshape(len(g.params["mean"]), -1)
+                                     for k in PARAM_KEYS], 1))
+            else:
+                ms.append(torch.from_numpy(_pack(g.adam_m)).to(dev))
+                vs.append(torch.from_numpy(_pack(g.adam_v)).to(dev))
+        return torch.cat(ms).contiguous(), torch.cat(vs).contiguous()
+
+    def write_back(self, t, which="params"):
+        host = t.cpu().numpy()
+        off = 0
+        for g, n in zip(self.gens, self.sizes):
+            tgt = getattr(g, which)
+            block = host[off:off + n]
+            if g.on_device:
+                for k, (a, b) in COLS.items():
+                    src = block[:, a] if b - a == 1 else block[:, a:b]
+                    tgt[k].copy_(torch.from_numpy(np.ascontiguousarray(src)))
+            else:
+                _unpack_into(tgt, block)
+            off += n
+
+
+def _single_gen_table(active=1, bc1=1.0, bc2=1.0, gscale=1.0):
+    tab = np.zeros(1, dtype=GEN_DTYPE)
+    tab[0] = (active, 0, bc1, bc2, gscale)
+    return torch.from_numpy(tab.view(np.uint8)).to(device())
+
+
+def run_sgld(gens, current_mean_lr, noise_lr, rng, gate_center, gate_sharpness):
+    if not gens:
+        return
+    b = _Batch(gens)
+    n = b.t.shape[0]
+    eta = np.concatenate([rng.standard_normal((s, 3)) for s in b.sizes])
+    eta_t = torch.from_numpy(eta).to(device())
+    h = L.SSStepHyper()
+    h.noise_scale = noise_lr * current_mean_lr
+    h.gate_center, h.gate_sharpness = gate_center, gate_sharpness
+    h.sgld = 1
+    L.check(L.lib().ss_sgld(L.ptr(b.t), n, max(n, 1), L.ptr(_single_gen_table()), ctypes.byref(h),
+                            L.ptr(eta_t), L.stream_ptr()), "sgld")
+    b.write_back(b.t)
+
+
+def run_relocate(gens, threshold, rng) -> int:
+    if not gens:
+        return 0
+    b = _Batch(gens)
+    n = b.t.shape[0]
+    alpha = 1.0 / (1.0 + torch.exp(-b.t[:, 10]))
+    n_dead = int((alpha < threshold).sum().item())
+    if n_dead == 0:
+        return 0
+    if n_dead == n:
+        log.warning("relocation skipped: no alive splats above threshold %.4g", threshold)
+        return 0
+    u = torch.from_numpy(rng.random(n_dead)).to(device())
+    m, v = b.moments()
+    lib = L.lib()
+    ws = torch.empty(int(lib.ss_relocate_workspace_bytes(n)), dtype=torch.uint8, device=device())
+    counts = torch.zeros(2, dtype=torch.int32, device=device())
+    L.check(lib.ss_relocate(L.ptr(b.t), L.ptr(m), L.ptr(v), n, n, L.ptr(_single_gen_table()),
+                            float(threshold), L.ptr(u), 0, 0, L.ptr(counts), L.ptr(ws), ws.numel(),
+                            L.stream_ptr()), "relocate")
+    b.write_back(b.t)
+    b.write_back(m, "adam_m")
+    b.write_back(v, "adam_v")
+    return n_dead
+
+
+def run_optimizer_step(gen, grads, config):
+    b = _Batch([gen])
+    n = b.t.shape[0]
+    g = torch.from_numpy(_pack({k: np.asarray(grads[k]) for k in PARAM_KEYS}).astype(np.float32))
+    g = g.to(device())
+    m, v = b.moments()
+    if config.optimizer == "adam":
+        gen.adam_t += 1
+    t = max(gen.adam_t, 1)
+    tab = _single_gen_table(1, 1.0 - config.adam_beta1 ** t, 1.0 - config.adam_beta2 ** t, 1.0)
+    h = _hyper(config, 1, False, 0, 0)
+    h.opacity_reg = h.scale_reg = 0.0
+    L.check(L.lib().ss_adam_sgld_step(L.ptr(b.t), L.ptr(g), L.ptr(m), L.ptr(v), n, max(n, 1),
+                                      L.ptr(tab), ctypes.byref(h), None, L.stream_ptr()),
+            "adam_sgld_step")
+    b.write_back(b.t)
+    if config.optimizer == "adam":
+        b.write_back(m, "adam_m")
+        b.write_back(v, "adam_v")
