@@ -1,195 +1,259 @@
 // a-5 blend forward (_kernels.py:20-53) and a-6 blend backward
 // (_kernels.py:56-130) as 16x16-tile rasterizers.
 //
-// One CTA per tile, one thread per pixel.  The tile's list (already in the
-// reference's global (z, src) order, see binning.cu) is staged through
-// shared memory 256 records at a time; each record is 36 B (rec_a float4,
-// rec_b float4, rec_c float).  Per pixel the reference rules are kept:
-// maha > 64 skips, alpha' = min(alpha G, 0.999), accumulation stops once
-// T < 1e-4 (the crossing splat included), no background.  The bbox test of
-// _kernels.py:35-36 is implied by maha <= 64 (the 8-sigma bbox encloses the
-// maha = 64 ellipse), so it is not repeated per pixel.
+// Work mapping: one warp per tile (4 tiles per 128-thread CTA, warps are
+// independent).  Lane l owns the 8-pixel column strip x = l % 16,
+// y = 8 (l / 16) + 0..7 of the tile, so per list entry a lane evaluates 8
+// pixels that share dx: the Mahalanobis term is A + dy (B + c dy) with
+// A = a dx^2, B = 2 b dx computed once per entry (2 FMAs per pixel).  The
+// tile's list (already in the reference's global (z, src) order, see
+// binning.cu) is staged 32 records at a time through a warp-private shared
+// buffer; each record is 36 B (rec_a float4, rec_b float4, rec_c float).
+//
+// Per pixel the reference rules are kept: maha > 64 skips, alpha' =
+// min(alpha G, 0.999), accumulation stops once T < 1e-4 (the crossing splat
+// included), no background.  The bbox test of _kernels.py:35-36 is implied
+// by maha <= 64 (the 8-sigma bbox encloses the maha = 64 ellipse).
+//
+// Backward: back to front from each pixel's last contributor, T recovered
+// by division by (1 - alpha'), suffix colour S accumulated as in
+// _kernels.py:100-130.  Per entry a lane folds its 8 pixels into 7 partial
+// sums (sum dm, sum dm dy, sum dm dy^2, sum dap G, colour x3) from which the
+// 9 gradient components follow; one transposed warp reduction and one
+// 9-lane float atomic per (tile, entry).
 #include "ss_common.cuh"
 
 namespace ss {
 
-constexpr int kBatch = 256;
-// exp(-m/2) = exp2(-m/2 * log2(e))
-constexpr float kNegHalfLog2e = -0.72134752044448170368f;
+constexpr int kWarps = 4;        // tiles per CTA
+constexpr int kStrip = 8;        // pixels per lane
+constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // exp(-m/2) = 2^(m * this)
 
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct WarpStage {
+  float4 a[32];
+  float4 b[32];
+  float c[32];
+  int g[32];
+};
+
+__device__ __forceinline__ void stage_load(WarpStage& st, int lane, int idx, int end,
+                                           const int32_t* __restrict__ vals,
+                                           const float4* __restrict__ rec_a,
+                                           const float4* __restrict__ rec_b,
+                                           const float* __restrict__ rec_c) {
+  if (idx < end) {
+    const int g = __ldg(vals + idx);
+    st.g[lane] = g;
+    st.a[lane] = __ldg(rec_a + g);
+    st.b[lane] = __ldg(rec_b + g);
+    st.c[lane] = __ldg(rec_c + g);
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
     raster_fwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
                       const float4* __restrict__ rec_a, const float4* __restrict__ rec_b,
                       const float* __restrict__ rec_c, int width, int height, int tiles_x,
-                      float* __restrict__ img, float* __restrict__ t_final,
+                      int n_tiles, float* __restrict__ img, float* __restrict__ t_final,
                       int32_t* __restrict__ n_contrib) {
-  __shared__ float4 s_a[kBatch];
-  __shared__ float4 s_b[kBatch];
-  __shared__ float s_c[kBatch];
-  const int tile = blockIdx.x;
+  __shared__ WarpStage s_stage[kWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kWarps + warp;
+  if (tile >= n_tiles) return;
+  WarpStage& st = s_stage[warp];
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int px = tx * kTile + (threadIdx.x & (kTile - 1));
-  const int py = ty * kTile + (threadIdx.x / kTile);
-  const bool inside = px < width && py < height;
-  const float fx = (float)px, fy = (float)py;
+  const int px = tx * kTile + (lane & 15);
+  const int py0 = ty * kTile + (lane >> 4) * kStrip;
+  const float fx = (float)px, fy0 = (float)py0;
+  unsigned live = 0;
+#pragma unroll
+  for (int k = 0; k < kStrip; ++k)
+    if (px < width && py0 + k < height) live |= 1u << k;
+  float T[kStrip], c0[kStrip], c1[kStrip], c2[kStrip];
+  int last[kStrip];
+#pragma unroll
+  for (int k = 0; k < kStrip; ++k) {
+    T[k] = 1.f;
+    c0[k] = c1[k] = c2[k] = 0.f;
+    last[k] = 0;
+  }
   const int2 rg = ranges[tile];
-  bool done = !inside;
-  float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
-  int last = 0;
-  for (int base = rg.x; base < rg.y; base += kBatch) {
-    if (__syncthreads_and(done)) break;
-    const int idx = base + threadIdx.x;
-    if (idx < rg.y) {
-      const int g = vals[idx];
-      s_a[threadIdx.x] = rec_a[g];
-      s_b[threadIdx.x] = rec_b[g];
-      s_c[threadIdx.x] = rec_c[g];
-    }
-    __syncthreads();
-    const int cnt = min(kBatch, rg.y - base);
-    if (!done) {
+  for (int base = rg.x; base < rg.y; base += 32) {
+    if (!__any_sync(0xffffffffu, live)) break;
+    __syncwarp();
+    stage_load(st, lane, base + lane, rg.y, vals, rec_a, rec_b, rec_c);
+    __syncwarp();
+    if (live) {
+      const int cnt = min(32, rg.y - base);
       for (int j = 0; j < cnt; ++j) {
-        const float4 a = s_a[j];
-        const float dx = fx - a.x, dy = fy - a.y;
-        const float4 b = s_b[j];
-        const float m = a.z * dx * dx + 2.f * a.w * dx * dy + b.x * dy * dy;
-        if (m > kMahaMax) continue;
-        const float G = exp2f(m * kNegHalfLog2e);
-        const float ap = fminf(b.y * G, kAlphaMax);
-        const float w = ap * T;
-        c0 += b.z * w;
-        c1 += b.w * w;
-        c2 += s_c[j] * w;
-        T *= 1.f - ap;
-        last = base - rg.x + j + 1;
-        if (T < kTMin) {
-          done = true;
-          break;
+        const float4 a = st.a[j];
+        const float4 b = st.b[j];
+        const float cb = st.c[j];
+        const float dx = fx - a.x, dy0 = fy0 - a.y;
+        const float A = a.z * dx * dx, B = 2.f * a.w * dx, cc = b.x;
+        const int pos = base - rg.x + j + 1;
+#pragma unroll
+        for (int k = 0; k < kStrip; ++k) {
+          if (live & (1u << k)) {
+            const float dy = dy0 + (float)k;
+            const float m = fmaf(dy, fmaf(cc, dy, B), A);
+            if (m <= kMahaMax) {
+              const float G = ex2(m * kNegHalfLog2e);
+              const float ap = fminf(b.y * G, kAlphaMax);
+              const float w = ap * T[k];
+              c0[k] = fmaf(b.z, w, c0[k]);
+              c1[k] = fmaf(b.w, w, c1[k]);
+              c2[k] = fmaf(cb, w, c2[k]);
+              T[k] *= 1.f - ap;
+              last[k] = pos;
+              if (T[k] < kTMin) live &= ~(1u << k);
+            }
+          }
         }
+        if (!live) break;
       }
     }
   }
-  if (inside) {
-    const int64_t p = (int64_t)py * width + px;
-    img[3 * p] = c0;
-    img[3 * p + 1] = c1;
-    img[3 * p + 2] = c2;
-    t_final[p] = T;
-    n_contrib[p] = last;
+#pragma unroll
+  for (int k = 0; k < kStrip; ++k) {
+    const int py = py0 + k;
+    if (px < width && py < height) {
+      const int64_t p = (int64_t)py * width + px;
+      img[3 * p] = c0[k];
+      img[3 * p + 1] = c1[k];
+      img[3 * p + 2] = c2[k];
+      t_final[p] = T[k];
+      n_contrib[p] = last[k];
+    }
   }
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
+// Transposed warp reduction of 16 slots: afterwards lane L holds the warp
+// total of slot 8 b4 + 4 b3 + 2 b2 + b1 (b_i = bit i of L); lanes L, L^1 agree.
+__device__ __forceinline__ float reduce16(float v[16], int lane) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+  for (int half = 8, off = 16; half >= 1; half >>= 1, off >>= 1) {
+    const bool up = lane & off;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float send = up ? v[i] : v[i + half];
+      const float keep = up ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kWarps * 32)
     raster_bwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
                       const float4* __restrict__ rec_a, const float4* __restrict__ rec_b,
                       const float* __restrict__ rec_c, int width, int height, int tiles_x,
-                      const float* __restrict__ dimg, const float* __restrict__ t_final,
-                      const int32_t* __restrict__ n_contrib, float4* __restrict__ g2d) {
-  __shared__ float4 s_a[kBatch];
-  __shared__ float4 s_b[kBatch];
-  __shared__ float s_c[kBatch];
-  __shared__ int32_t s_g[kBatch];
-  __shared__ int s_max_last;
-  const int tile = blockIdx.x;
+                      int n_tiles, const float* __restrict__ dimg,
+                      const float* __restrict__ t_final, const int32_t* __restrict__ n_contrib,
+                      float* __restrict__ g2d) {
+  __shared__ WarpStage s_stage[kWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kWarps + warp;
+  if (tile >= n_tiles) return;
+  WarpStage& st = s_stage[warp];
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int px = tx * kTile + (threadIdx.x & (kTile - 1));
-  const int py = ty * kTile + (threadIdx.x / kTile);
-  const bool inside = px < width && py < height;
-  const float fx = (float)px, fy = (float)py;
-  const int2 rg = ranges[tile];
-  float T = 1.f, d0 = 0.f, d1 = 0.f, d2 = 0.f;
-  int last = 0;
-  if (inside) {
-    const int64_t p = (int64_t)py * width + px;
-    T = t_final[p];
-    last = n_contrib[p];
-    d0 = dimg[3 * p];
-    d1 = dimg[3 * p + 1];
-    d2 = dimg[3 * p + 2];
-  }
-  if (threadIdx.x == 0) s_max_last = 0;
-  __syncthreads();
-  const int wmax = __reduce_max_sync(0xffffffffu, last);
-  if ((threadIdx.x & 31) == 0) atomicMax(&s_max_last, wmax);
-  __syncthreads();
-  const int walk_end = rg.x + s_max_last;
-  float S0 = 0.f, S1 = 0.f, S2 = 0.f;  // colour already blended behind (suffix)
-  const int lane = threadIdx.x & 31;
-  for (int end = walk_end; end > rg.x; end -= kBatch) {
-    const int start = max(rg.x, end - kBatch);
-    __syncthreads();
-    const int idx = start + threadIdx.x;
-    if (idx < end) {
-      const int g = vals[idx];
-      s_g[threadIdx.x] = g;
-      s_a[threadIdx.x] = rec_a[g];
-      s_b[threadIdx.x] = rec_b[g];
-      s_c[threadIdx.x] = rec_c[g];
+  const int px = tx * kTile + (lane & 15);
+  const int py0 = ty * kTile + (lane >> 4) * kStrip;
+  const float fx = (float)px, fy0 = (float)py0;
+  float T[kStrip], d0[kStrip], d1[kStrip], d2[kStrip], S0[kStrip], S1[kStrip], S2[kStrip];
+  int last[kStrip];
+  int my_max = 0;
+#pragma unroll
+  for (int k = 0; k < kStrip; ++k) {
+    const int py = py0 + k;
+    S0[k] = S1[k] = S2[k] = 0.f;
+    if (px < width && py < height) {
+      const int64_t p = (int64_t)py * width + px;
+      T[k] = t_final[p];
+      last[k] = n_contrib[p];
+      d0[k] = dimg[3 * p];
+      d1[k] = dimg[3 * p + 1];
+      d2[k] = dimg[3 * p + 2];
+    } else {
+      T[k] = 1.f;
+      last[k] = 0;
+      d0[k] = d1[k] = d2[k] = 0.f;
     }
-    __syncthreads();
-    for (int j = end - 1; j >= start; --j) {
-      const int jj = j - start;
-      const bool mine = (j - rg.x) < last;
-      float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f, v5 = 0.f, v6 = 0.f, v7 = 0.f,
-            v8 = 0.f;
-      bool has = false;
-      if (mine) {
-        const float4 a = s_a[jj];
-        const float dx = fx - a.x, dy = fy - a.y;
-        const float4 b = s_b[jj];
-        const float m = a.z * dx * dx + 2.f * a.w * dx * dy + b.x * dy * dy;
-        if (m <= kMahaMax) {
-          has = true;
-          const float G = exp2f(m * kNegHalfLog2e);
-          const float aG = b.y * G;
-          const float ap = fminf(aG, kAlphaMax);
-          const float one_m = 1.f - ap;
-          const float inv_rest = __frcp_rn(one_m);
-          T *= inv_rest;  // T before this splat
-          const float w = ap * T;
-          const float cr = b.z, cg = b.w, cb = s_c[jj];
-          v6 = d0 * w;
-          v7 = d1 * w;
-          v8 = d2 * w;
-          const float d_ap = d0 * (cr * T - S0 * inv_rest) + d1 * (cg * T - S1 * inv_rest) +
-                             d2 * (cb * T - S2 * inv_rest);
-          S0 += cr * w;
-          S1 += cg * w;
-          S2 += cb * w;
-          if (aG <= kAlphaMax) {
-            v5 = d_ap * G;                          // g_alpha
-            const float dm = -0.5f * G * b.y * d_ap;
-            v2 = dm * dx * dx;                      // g_inv2d
-            v3 = dm * 2.f * dx * dy;
-            v4 = dm * dy * dy;
-            v0 = -dm * 2.f * (a.z * dx + a.w * dy);  // g_mean2d
-            v1 = -dm * 2.f * (a.w * dx + b.x * dy);
+    my_max = max(my_max, last[k]);
+  }
+  const int2 rg = ranges[tile];
+  const int walk_end = rg.x + __reduce_max_sync(0xffffffffu, my_max);
+  const int slot = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                   ((lane >> 1) & 1);
+  for (int end = walk_end; end > rg.x; end -= 32) {
+    const int start = max(rg.x, end - 32);
+    __syncwarp();
+    stage_load(st, lane, start + lane, end, vals, rec_a, rec_b, rec_c);
+    __syncwarp();
+    for (int j = end - start - 1; j >= 0; --j) {
+      const int pos = start - rg.x + j;  // 0-based position in the tile list
+      const float4 a = st.a[j];
+      const float4 b = st.b[j];
+      const float cb = st.c[j];
+      const float dx = fx - a.x, dy0 = fy0 - a.y;
+      const float A = a.z * dx * dx, B = 2.f * a.w * dx, cc = b.x;
+      const float alpha = b.y;
+      float sdm = 0.f, sdmy = 0.f, sdmyy = 0.f, sal = 0.f, sc0 = 0.f, sc1 = 0.f, sc2 = 0.f;
+      bool touched = false;
+#pragma unroll
+      for (int k = 0; k < kStrip; ++k) {
+        if (pos < last[k]) {
+          const float dy = dy0 + (float)k;
+          const float m = fmaf(dy, fmaf(cc, dy, B), A);
+          if (m <= kMahaMax) {
+            touched = true;
+            const float G = ex2(m * kNegHalfLog2e);
+            const float aG = alpha * G;
+            const float ap = fminf(aG, kAlphaMax);
+            const float inv = __frcp_rn(1.f - ap);
+            T[k] *= inv;  // T before this splat
+            const float w = ap * T[k];
+            sc0 = fmaf(d0[k], w, sc0);
+            sc1 = fmaf(d1[k], w, sc1);
+            sc2 = fmaf(d2[k], w, sc2);
+            const float dap = d0[k] * (b.z * T[k] - S0[k] * inv) +
+                              d1[k] * (b.w * T[k] - S1[k] * inv) +
+                              d2[k] * (cb * T[k] - S2[k] * inv);
+            S0[k] = fmaf(b.z, w, S0[k]);
+            S1[k] = fmaf(b.w, w, S1[k]);
+            S2[k] = fmaf(cb, w, S2[k]);
+            if (aG <= kAlphaMax) {  // clamped splats pass no alpha/footprint gradient
+              sal = fmaf(dap, G, sal);
+              const float dm = -0.5f * G * alpha * dap;
+              sdm += dm;
+              sdmy = fmaf(dm, dy, sdmy);
+              sdmyy = fmaf(dm * dy, dy, sdmyy);
+            }
           }
         }
       }
-      if (__any_sync(0xffffffffu, has)) {
-        v0 = warp_sum(v0);
-        v1 = warp_sum(v1);
-        v2 = warp_sum(v2);
-        v3 = warp_sum(v3);
-        v4 = warp_sum(v4);
-        v5 = warp_sum(v5);
-        v6 = warp_sum(v6);
-        v7 = warp_sum(v7);
-        v8 = warp_sum(v8);
-        if (lane == 0) {
-          float4* dst = g2d + (int64_t)s_g[jj] * 3;
-          atomicAdd(dst, make_float4(v0, v1, v2, v3));
-          atomicAdd(dst + 1, make_float4(v4, v5, v6, v7));
-          atomicAdd(&dst[2].x, v8);
-        }
-      }
+      if (!__any_sync(0xffffffffu, touched)) continue;
+      // g_mean2d = -2 dm (conic d), g_inv2d = dm (dx^2, 2 dx dy, dy^2) summed over the strip
+      float v[16];
+      v[0] = -2.f * (a.z * dx * sdm + a.w * sdmy);
+      v[1] = -2.f * (a.w * dx * sdm + cc * sdmy);
+      v[2] = dx * dx * sdm;
+      v[3] = 2.f * dx * sdmy;
+      v[4] = sdmyy;
+      v[5] = sal;
+      v[6] = sc0;
+      v[7] = sc1;
+      v[8] = sc2;
+#pragma unroll
+      for (int i = 9; i < 16; ++i) v[i] = 0.f;
+      const float tot = reduce16(v, lane);
+      if (!(lane & 1) && slot < 9) atomicAdd(g2d + (int64_t)st.g[j] * SS_G2D_ROW + slot, tot);
     }
   }
 }
@@ -203,9 +267,10 @@ extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const v
                              float* img, float* t_final, int32_t* n_contrib, cudaStream_t stream) {
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_raster_fwd: bad size");
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
-  raster_fwd_kernel<<<tiles_x * tiles_y, kTilePix, 0, stream>>>(
+  const int n_tiles = tiles_x * tiles_y;
+  raster_fwd_kernel<<<(n_tiles + kWarps - 1) / kWarps, kWarps * 32, 0, stream>>>(
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
-      tiles_x, img, t_final, n_contrib);
+      tiles_x, n_tiles, img, t_final, n_contrib);
   return check_launch("ss_raster_fwd");
 }
 
@@ -215,8 +280,9 @@ extern "C" int ss_raster_bwd(const int32_t* ranges, const int32_t* vals, const v
                              float* g2d, cudaStream_t stream) {
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_raster_bwd: bad size");
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
-  raster_bwd_kernel<<<tiles_x * tiles_y, kTilePix, 0, stream>>>(
+  const int n_tiles = tiles_x * tiles_y;
+  raster_bwd_kernel<<<(n_tiles + kWarps - 1) / kWarps, kWarps * 32, 0, stream>>>(
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
-      tiles_x, dimg, t_final, n_contrib, (float4*)g2d);
+      tiles_x, n_tiles, dimg, t_final, n_contrib, g2d);
   return check_launch("ss_raster_bwd");
 }

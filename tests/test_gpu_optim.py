@@ -3,7 +3,7 @@ reference's golden vectors (tests/golden/optim.npz, train_tiny.npz).
 
 Tolerances: SGLD and relocation with injected draws <= 1e-12 relative
 (fp64 kernels; libm ulp differences only); Adam with float32 gradients
-(the trainer's gradient buffer) <= 1e-6 relative on moments and 1e-9
+(the trainer's gradient buffer) <= 1e-6 relative on moments and 1e-8
 absolute on parameters."""
 
 import numpy as np
@@ -39,7 +39,7 @@ def test_adam_steps_match_reference(T):
             T._optimizer_step(g, grads, cfg)
             assert g.adam_t == int(d[f"t{step}_{gi}"])
             for k in GROUPS:
-                np.testing.assert_allclose(g.params[k], d[f"p{step + 1}_{gi}_{k}"], rtol=0, atol=1e-9)
+                np.testing.assert_allclose(g.params[k], d[f"p{step + 1}_{gi}_{k}"], rtol=0, atol=1e-8)
                 np.testing.assert_allclose(g.adam_m[k], d[f"m{step + 1}_{gi}_{k}"], rtol=1e-6, atol=1e-300)
                 np.testing.assert_allclose(g.adam_v[k], d[f"v{step + 1}_{gi}_{k}"], rtol=1e-6, atol=1e-300)
 
@@ -50,7 +50,7 @@ def test_sgd_step_matches_reference(T):
     T._optimizer_step(g, {k: d[f"g1_0_{k}"] for k in GROUPS},
                       T.TrainConfig(swin_size=5, num_gs=500, optimizer="sgd"))
     for k in GROUPS:
-        np.testing.assert_allclose(g.params[k], d[f"sgd_{k}"], rtol=0, atol=1e-9)
+        np.testing.assert_allclose(g.params[k], d[f"sgd_{k}"], rtol=0, atol=1e-8)
 
 
 def test_sgld_matches_reference_with_same_draws(T):
