@@ -132,20 +132,27 @@ int ss_sort_tile_pairs(uint32_t* keys, int32_t* vals, uint32_t* keys_alt, int32_
                        size_t ws_bytes, ss_stream_t stream);
 int ss_tile_ranges(const uint32_t* sorted_keys, int64_t n_pairs, int32_t n_tiles,
                    int32_t* ranges, ss_stream_t stream);
+/* Tiles ordered by list length, longest first (raster scheduling order:
+ * longest-processing-time-first across the SMs).  ws >= ss_tile_order_workspace_bytes. */
+size_t ss_tile_order_workspace_bytes(int32_t n_tiles);
+int ss_tile_order(const int32_t* ranges, int32_t n_tiles, int32_t* tile_order, void* ws,
+                  size_t ws_bytes, ss_stream_t stream);
 
 /* ---- a-5 blend forward: _kernels.py:20-53.  img is (H, W, 3) float32;
- * t_final / n_contrib per pixel feed the backward. */
+ * t_final / n_contrib per pixel feed the backward.  tile_order (nullable)
+ * is the tile processing order from ss_tile_order. */
 int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                   const void* rec_b, const float* rec_c, int32_t width, int32_t height,
-                  float* img, float* t_final, int32_t* n_contrib, ss_stream_t stream);
+                  const int32_t* tile_order, float* img, float* t_final, int32_t* n_contrib,
+                  ss_stream_t stream);
 
 /* ---- a-6 blend backward: _kernels.py:56-130.  Accumulates into g2d
  * (n x 12 floats: g_mean2d[2] g_inv2d[3] g_alpha g_color[3] pad[3]),
  * which the caller zeroes. */
 int ss_raster_bwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                   const void* rec_b, const float* rec_c, int32_t width, int32_t height,
-                  const float* dimg, const float* t_final, const int32_t* n_contrib, float* g2d,
-                  ss_stream_t stream);
+                  const int32_t* tile_order, const float* dimg, const float* t_final,
+                  const int32_t* n_contrib, float* g2d, ss_stream_t stream);
 
 /* ---- a-7 projection backward: raster.py:249-348.  For active i with
  * trainable (mask ? mask[i] : 1) and row < trainable_rows, writes the

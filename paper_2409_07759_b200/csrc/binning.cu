@@ -59,6 +59,15 @@ __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int64_t n_
   if (p == n_pairs - 1 || keys[p + 1] != t) ranges[t].y = (int32_t)(p + 1);
 }
 
+__global__ void tile_len_kernel(const int2* __restrict__ ranges, int n_tiles,
+                                int32_t* __restrict__ len, int32_t* __restrict__ ids) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_tiles) return;
+  const int2 r = ranges[t];
+  len[t] = r.y - r.x;
+  ids[t] = t;
+}
+
 static int bits_for(int64_t v) {
   int b = 1;
   while ((1ll << b) < v) ++b;
@@ -170,4 +179,37 @@ extern "C" int ss_tile_ranges(const uint32_t* sorted_keys, int64_t n_pairs, int3
     tile_ranges_kernel<<<grid_for(n_pairs, 256), 256, 0, stream>>>(sorted_keys, n_pairs,
                                                                     (int2*)ranges);
   return check_launch("ss_tile_ranges");
+}
+
+static size_t tile_order_cub_bytes(int32_t n_tiles) {
+  size_t b = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr,
+                                            (int32_t*)nullptr, (int32_t*)nullptr,
+                                            n_tiles > 0 ? n_tiles : 1);
+  return b;
+}
+
+extern "C" size_t ss_tile_order_workspace_bytes(int32_t n_tiles) {
+  size_t nn = (size_t)(n_tiles > 0 ? n_tiles : 1);
+  return align256(tile_order_cub_bytes(n_tiles)) + 3 * align256(nn * 4) + 256;
+}
+
+extern "C" int ss_tile_order(const int32_t* ranges, int32_t n_tiles, int32_t* tile_order,
+                             void* ws, size_t ws_bytes, cudaStream_t stream) {
+  if (n_tiles <= 0) return set_error(SS_ERR_INVALID, "ss_tile_order: n_tiles <= 0");
+  if (ws_bytes < ss_tile_order_workspace_bytes(n_tiles))
+    return set_error(SS_ERR_WORKSPACE, "ss_tile_order: workspace too small");
+  char* w = (char*)ws;
+  const size_t nn = (size_t)n_tiles;
+  const size_t tb = align256(tile_order_cub_bytes(n_tiles));
+  int32_t* len = (int32_t*)(w + tb);
+  int32_t* len_out = (int32_t*)((char*)len + align256(nn * 4));
+  int32_t* ids = (int32_t*)((char*)len_out + align256(nn * 4));
+  tile_len_kernel<<<grid_for(n_tiles, 256), 256, 0, stream>>>((const int2*)ranges, n_tiles, len,
+                                                               ids);
+  size_t tmp = tb;
+  cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(w, tmp, len, len_out, ids, tile_order,
+                                                            n_tiles, 0, 32, stream);
+  if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_tile_order: %s", cudaGetErrorString(e));
+  return check_launch("ss_tile_order");
 }

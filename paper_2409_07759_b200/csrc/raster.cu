@@ -60,12 +60,14 @@ __global__ void __launch_bounds__(kWarps * 32)
     raster_fwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
                       const float4* __restrict__ rec_a, const float4* __restrict__ rec_b,
                       const float* __restrict__ rec_c, int width, int height, int tiles_x,
-                      int n_tiles, float* __restrict__ img, float* __restrict__ t_final,
+                      int n_tiles, const int32_t* __restrict__ tile_order,
+                      float* __restrict__ img, float* __restrict__ t_final,
                       int32_t* __restrict__ n_contrib) {
   __shared__ WarpStage s_stage[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kWarps + warp;
-  if (tile >= n_tiles) return;
+  const int slot_id = blockIdx.x * kWarps + warp;
+  if (slot_id >= n_tiles) return;
+  const int tile = tile_order ? tile_order[slot_id] : slot_id;
   WarpStage& st = s_stage[warp];
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int px = tx * kTile + (lane & 15);
@@ -98,25 +100,23 @@ __global__ void __launch_bounds__(kWarps * 32)
         const float dx = fx - a.x, dy0 = fy0 - a.y;
         const float A = a.z * dx * dx, B = 2.f * a.w * dx, cc = b.x;
         const int pos = base - rg.x + j + 1;
+        // branch-free over the strip: invalid pixels get alpha' = 0, which
+        // leaves C and T untouched, so the 8 chains interleave freely
 #pragma unroll
         for (int k = 0; k < kStrip; ++k) {
-          if (live & (1u << k)) {
-            const float dy = dy0 + (float)k;
-            const float m = fmaf(dy, fmaf(cc, dy, B), A);
-            if (m <= kMahaMax) {
-              const float G = ex2(m * kNegHalfLog2e);
-              const float ap = fminf(b.y * G, kAlphaMax);
-              const float w = ap * T[k];
-              c0[k] = fmaf(b.z, w, c0[k]);
-              c1[k] = fmaf(b.w, w, c1[k]);
-              c2[k] = fmaf(cb, w, c2[k]);
-              T[k] *= 1.f - ap;
-              last[k] = pos;
-              if (T[k] < kTMin) live &= ~(1u << k);
-            }
-          }
+          const float dy = dy0 + (float)k;
+          const float m = fmaf(dy, fmaf(cc, dy, B), A);
+          const bool valid = ((live >> k) & 1u) && (m <= kMahaMax);
+          const float G = ex2(m * kNegHalfLog2e);
+          const float ap = valid ? fminf(b.y * G, kAlphaMax) : 0.f;
+          const float w = ap * T[k];
+          c0[k] = fmaf(b.z, w, c0[k]);
+          c1[k] = fmaf(b.w, w, c1[k]);
+          c2[k] = fmaf(cb, w, c2[k]);
+          T[k] *= 1.f - ap;
+          last[k] = valid ? pos : last[k];
+          live &= ~((unsigned)(T[k] < kTMin) << k);
         }
-        if (!live) break;
       }
     }
   }
@@ -154,13 +154,14 @@ __global__ void __launch_bounds__(kWarps * 32)
     raster_bwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
                       const float4* __restrict__ rec_a, const float4* __restrict__ rec_b,
                       const float* __restrict__ rec_c, int width, int height, int tiles_x,
-                      int n_tiles, const float* __restrict__ dimg,
-                      const float* __restrict__ t_final, const int32_t* __restrict__ n_contrib,
-                      float* __restrict__ g2d) {
+                      int n_tiles, const int32_t* __restrict__ tile_order,
+                      const float* __restrict__ dimg, const float* __restrict__ t_final,
+                      const int32_t* __restrict__ n_contrib, float* __restrict__ g2d) {
   __shared__ WarpStage s_stage[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kWarps + warp;
-  if (tile >= n_tiles) return;
+  const int slot_id = blockIdx.x * kWarps + warp;
+  if (slot_id >= n_tiles) return;
+  const int tile = tile_order ? tile_order[slot_id] : slot_id;
   WarpStage& st = s_stage[warp];
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int px = tx * kTile + (lane & 15);
@@ -208,35 +209,34 @@ __global__ void __launch_bounds__(kWarps * 32)
       bool touched = false;
 #pragma unroll
       for (int k = 0; k < kStrip; ++k) {
-        if (pos < last[k]) {
-          const float dy = dy0 + (float)k;
-          const float m = fmaf(dy, fmaf(cc, dy, B), A);
-          if (m <= kMahaMax) {
-            touched = true;
-            const float G = ex2(m * kNegHalfLog2e);
-            const float aG = alpha * G;
-            const float ap = fminf(aG, kAlphaMax);
-            const float inv = __frcp_rn(1.f - ap);
-            T[k] *= inv;  // T before this splat
-            const float w = ap * T[k];
-            sc0 = fmaf(d0[k], w, sc0);
-            sc1 = fmaf(d1[k], w, sc1);
-            sc2 = fmaf(d2[k], w, sc2);
-            const float dap = d0[k] * (b.z * T[k] - S0[k] * inv) +
+        // branch-free: an invalid pixel has alpha' = 0 (T and S unchanged) and
+        // its d alpha' is zeroed, so it contributes nothing
+        const float dy = dy0 + (float)k;
+        const float m = fmaf(dy, fmaf(cc, dy, B), A);
+        const bool valid = (pos < last[k]) && (m <= kMahaMax);
+        touched |= valid;
+        const float G = ex2(m * kNegHalfLog2e);
+        const float aG = alpha * G;
+        const float ap = valid ? fminf(aG, kAlphaMax) : 0.f;
+        const float inv = __frcp_rn(1.f - ap);
+        T[k] *= inv;  // T before this splat
+        const float w = ap * T[k];
+        sc0 = fmaf(d0[k], w, sc0);
+        sc1 = fmaf(d1[k], w, sc1);
+        sc2 = fmaf(d2[k], w, sc2);
+        const float dap_raw = d0[k] * (b.z * T[k] - S0[k] * inv) +
                               d1[k] * (b.w * T[k] - S1[k] * inv) +
                               d2[k] * (cb * T[k] - S2[k] * inv);
-            S0[k] = fmaf(b.z, w, S0[k]);
-            S1[k] = fmaf(b.w, w, S1[k]);
-            S2[k] = fmaf(cb, w, S2[k]);
-            if (aG <= kAlphaMax) {  // clamped splats pass no alpha/footprint gradient
-              sal = fmaf(dap, G, sal);
-              const float dm = -0.5f * G * alpha * dap;
-              sdm += dm;
-              sdmy = fmaf(dm, dy, sdmy);
-              sdmyy = fmaf(dm * dy, dy, sdmyy);
-            }
-          }
-        }
+        S0[k] = fmaf(b.z, w, S0[k]);
+        S1[k] = fmaf(b.w, w, S1[k]);
+        S2[k] = fmaf(cb, w, S2[k]);
+        // clamped splats pass no alpha/footprint gradient (_kernels.py:120-121)
+        const float dap = (valid && aG <= kAlphaMax) ? dap_raw : 0.f;
+        sal = fmaf(dap, G, sal);
+        const float dm = -0.5f * G * alpha * dap;
+        sdm += dm;
+        sdmy = fmaf(dm, dy, sdmy);
+        sdmyy = fmaf(dm * dy, dy, sdmyy);
       }
       if (!__any_sync(0xffffffffu, touched)) continue;
       // g_mean2d = -2 dm (conic d), g_inv2d = dm (dx^2, 2 dx dy, dy^2) summed over the strip
@@ -264,25 +264,26 @@ using namespace ss;
 
 extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                              const void* rec_b, const float* rec_c, int32_t width, int32_t height,
-                             float* img, float* t_final, int32_t* n_contrib, cudaStream_t stream) {
+                             const int32_t* tile_order, float* img, float* t_final,
+                             int32_t* n_contrib, cudaStream_t stream) {
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_raster_fwd: bad size");
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
   raster_fwd_kernel<<<(n_tiles + kWarps - 1) / kWarps, kWarps * 32, 0, stream>>>(
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
-      tiles_x, n_tiles, img, t_final, n_contrib);
+      tiles_x, n_tiles, tile_order, img, t_final, n_contrib);
   return check_launch("ss_raster_fwd");
 }
 
 extern "C" int ss_raster_bwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                              const void* rec_b, const float* rec_c, int32_t width, int32_t height,
-                             const float* dimg, const float* t_final, const int32_t* n_contrib,
-                             float* g2d, cudaStream_t stream) {
+                             const int32_t* tile_order, const float* dimg, const float* t_final,
+                             const int32_t* n_contrib, float* g2d, cudaStream_t stream) {
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_raster_bwd: bad size");
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
   raster_bwd_kernel<<<(n_tiles + kWarps - 1) / kWarps, kWarps * 32, 0, stream>>>(
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
-      tiles_x, n_tiles, dimg, t_final, n_contrib, g2d);
+      tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d);
   return check_launch("ss_raster_bwd");
 }

@@ -163,9 +163,13 @@ class ViewPipeline:
         sk, sv = (keys, vals) if sel.value == 0 else (keys_alt, vals_alt)
         self.sorted_keys, self.sorted_vals = sk, sv
         L.check(lib.ss_tile_ranges(L.ptr(sk), n_pairs, n_tiles, L.ptr(ranges), sp), "tile_ranges")
+        tord = self._buf("tile_order", (n_tiles,), torch.int32)
+        tws = self._buf("ws_tord", (int(lib.ss_tile_order_workspace_bytes(n_tiles)),), torch.uint8)
+        L.check(lib.ss_tile_order(L.ptr(ranges), n_tiles, L.ptr(tord), L.ptr(tws), tws.numel(), sp),
+                "tile_order")
         tok = self._mark("raster_fwd")
         L.check(lib.ss_raster_fwd(L.ptr(ranges), L.ptr(sv), L.ptr(rec_a), L.ptr(rec_b),
-                                  L.ptr(rec_c), W, H, L.ptr(img), L.ptr(t_final),
+                                  L.ptr(rec_c), W, H, L.ptr(tord), L.ptr(img), L.ptr(t_final),
                                   L.ptr(n_contrib), sp), "raster_fwd")
         self._done(tok)
         return img[: H * W * 3].view(H, W, 3)
@@ -185,7 +189,8 @@ class ViewPipeline:
         b = self._b
         tok = self._mark("raster_bwd")
         L.check(lib.ss_raster_bwd(L.ptr(b["ranges"]), L.ptr(self.sorted_vals), L.ptr(b["rec_a"]),
-                                  L.ptr(b["rec_b"]), L.ptr(b["rec_c"]), W, H, L.ptr(dimg),
+                                  L.ptr(b["rec_b"]), L.ptr(b["rec_c"]), W, H,
+                                  L.ptr(b["tile_order"]), L.ptr(dimg),
                                   L.ptr(b["t_final"]), L.ptr(b["n_contrib"]), L.ptr(g2d), sp),
                 "raster_bwd")
         self._done(tok)
