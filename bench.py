@@ -434,6 +434,7 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="after warm-up run N steps between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off); prints no JSON")
+    ap.add_argument("--strip", type=int, default=0, help="raster pixels per lane (2/4/8); 0 = library default")
     ap.add_argument("--init", default="gt", choices=["gt", "random"],
                     help="model state: ground-truth splats (converged proxy) or init_state")
     args = ap.parse_args()
@@ -452,6 +453,10 @@ def main():
     from paper_2409_07759_b200.parallel import init_from_env
 
     dp = init_from_env("nccl")
+    if args.strip:
+        from paper_2409_07759_b200 import _lib
+
+        _lib.check(_lib.lib().ss_set_raster_strip(args.strip), "set_raster_strip")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     world = 1 if dp is None else dp.world_size

@@ -146,6 +146,10 @@ int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                   const int32_t* tile_order, float* img, float* t_final, int32_t* n_contrib,
                   ss_stream_t stream);
 
+/* Tuning knob: pixels per lane in the raster kernels (2, 4 or 8); a warp
+ * covers 16 x (2 strip) pixels, i.e. 8 / strip warps per tile.  Default 4. */
+int ss_set_raster_strip(int32_t strip);
+
 /* ---- a-6 blend backward: _kernels.py:56-130.  Accumulates into g2d
  * (n x 12 floats: g_mean2d[2] g_inv2d[3] g_alpha g_color[3] pad[3]),
  * which the caller zeroes. */

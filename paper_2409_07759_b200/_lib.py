@@ -63,6 +63,7 @@ _SIGNATURES = {
     "ss_tile_order": ([P, I32, P, P, c_size_t, P], c_int),
     "ss_raster_fwd": ([P, P, P, P, P, I32, I32, P, P, P, P, P], c_int),
     "ss_raster_bwd": ([P, P, P, P, P, I32, I32, P, P, P, P, P, P], c_int),
+    "ss_set_raster_strip": ([I32], c_int),
     "ss_project_bwd": ([POINTER(SSStore), P, I32, POINTER(SSCamera), P, P, P, I64, P, P], c_int),
     "ss_loss_workspace_bytes": ([I32, I32], c_size_t),
     "ss_loss_l1_ssim": ([P, P, P, P, I32, I32, c_double, P, P, P, c_size_t, P], c_int),

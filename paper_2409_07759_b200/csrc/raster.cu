@@ -26,7 +26,6 @@
 namespace ss {
 
 constexpr int kWarps = 4;        // tiles per CTA
-constexpr int kStrip = 8;        // pixels per lane
 constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // exp(-m/2) = 2^(m * this)
 
 __device__ __forceinline__ float ex2(float x) {
@@ -56,6 +55,7 @@ __device__ __forceinline__ void stage_load(WarpStage& st, int lane, int idx, int
   }
 }
 
+template <int STRIP>
 __global__ void __launch_bounds__(kWarps * 32)
     raster_fwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
                       const float4* __restrict__ rec_a, const float4* __restrict__ rec_b,
@@ -65,22 +65,24 @@ __global__ void __launch_bounds__(kWarps * 32)
                       int32_t* __restrict__ n_contrib) {
   __shared__ WarpStage s_stage[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot_id = blockIdx.x * kWarps + warp;
+  constexpr int WPT = kTile / (2 * STRIP);  // warps per tile
+  const int gwarp = blockIdx.x * kWarps + warp;
+  const int slot_id = gwarp / WPT, sub = gwarp % WPT;
   if (slot_id >= n_tiles) return;
   const int tile = tile_order ? tile_order[slot_id] : slot_id;
   WarpStage& st = s_stage[warp];
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int px = tx * kTile + (lane & 15);
-  const int py0 = ty * kTile + (lane >> 4) * kStrip;
+  const int py0 = ty * kTile + sub * 2 * STRIP + (lane >> 4) * STRIP;
   const float fx = (float)px, fy0 = (float)py0;
   unsigned live = 0;
 #pragma unroll
-  for (int k = 0; k < kStrip; ++k)
+  for (int k = 0; k < STRIP; ++k)
     if (px < width && py0 + k < height) live |= 1u << k;
-  float T[kStrip], c0[kStrip], c1[kStrip], c2[kStrip];
-  int last[kStrip];
+  float T[STRIP], c0[STRIP], c1[STRIP], c2[STRIP];
+  int last[STRIP];
 #pragma unroll
-  for (int k = 0; k < kStrip; ++k) {
+  for (int k = 0; k < STRIP; ++k) {
     T[k] = 1.f;
     c0[k] = c1[k] = c2[k] = 0.f;
     last[k] = 0;
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(kWarps * 32)
         // branch-free over the strip: invalid pixels get alpha' = 0, which
         // leaves C and T untouched, so the 8 chains interleave freely
 #pragma unroll
-        for (int k = 0; k < kStrip; ++k) {
+        for (int k = 0; k < STRIP; ++k) {
           const float dy = dy0 + (float)k;
           const float m = fmaf(dy, fmaf(cc, dy, B), A);
           const bool valid = ((live >> k) & 1u) && (m <= kMahaMax);
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     }
   }
 #pragma unroll
-  for (int k = 0; k < kStrip; ++k) {
+  for (int k = 0; k < STRIP; ++k) {
     const int py = py0 + k;
     if (px < width && py < height) {
       const int64_t p = (int64_t)py * width + px;
@@ -150,6 +152,7 @@ __device__ __forceinline__ float reduce16(float v[16], int lane) {
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+template <int STRIP>
 __global__ void __launch_bounds__(kWarps * 32)
     raster_bwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
                       const float4* __restrict__ rec_a, const float4* __restrict__ rec_b,
@@ -159,19 +162,21 @@ __global__ void __launch_bounds__(kWarps * 32)
                       const int32_t* __restrict__ n_contrib, float* __restrict__ g2d) {
   __shared__ WarpStage s_stage[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot_id = blockIdx.x * kWarps + warp;
+  constexpr int WPT = kTile / (2 * STRIP);  // warps per tile
+  const int gwarp = blockIdx.x * kWarps + warp;
+  const int slot_id = gwarp / WPT, sub = gwarp % WPT;
   if (slot_id >= n_tiles) return;
   const int tile = tile_order ? tile_order[slot_id] : slot_id;
   WarpStage& st = s_stage[warp];
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int px = tx * kTile + (lane & 15);
-  const int py0 = ty * kTile + (lane >> 4) * kStrip;
+  const int py0 = ty * kTile + sub * 2 * STRIP + (lane >> 4) * STRIP;
   const float fx = (float)px, fy0 = (float)py0;
-  float T[kStrip], d0[kStrip], d1[kStrip], d2[kStrip], S0[kStrip], S1[kStrip], S2[kStrip];
-  int last[kStrip];
+  float T[STRIP], d0[STRIP], d1[STRIP], d2[STRIP], S0[STRIP], S1[STRIP], S2[STRIP];
+  int last[STRIP];
   int my_max = 0;
 #pragma unroll
-  for (int k = 0; k < kStrip; ++k) {
+  for (int k = 0; k < STRIP; ++k) {
     const int py = py0 + k;
     S0[k] = S1[k] = S2[k] = 0.f;
     if (px < width && py < height) {
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(kWarps * 32)
       float sdm = 0.f, sdmy = 0.f, sdmyy = 0.f, sal = 0.f, sc0 = 0.f, sc1 = 0.f, sc2 = 0.f;
       bool touched = false;
 #pragma unroll
-      for (int k = 0; k < kStrip; ++k) {
+      for (int k = 0; k < STRIP; ++k) {
         // branch-free: an invalid pixel has alpha' = 0 (T and S unchanged) and
         // its d alpha' is zeroed, so it contributes nothing
         const float dy = dy0 + (float)k;
@@ -258,9 +263,18 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
 }
 
+static int g_strip = 4;
+
 }  // namespace ss
 
 using namespace ss;
+
+extern "C" int ss_set_raster_strip(int32_t strip) {
+  if (strip != 2 && strip != 4 && strip != 8)
+    return set_error(SS_ERR_INVALID, "ss_set_raster_strip: strip must be 2, 4 or 8");
+  g_strip = strip;
+  return SS_OK;
+}
 
 extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                              const void* rec_b, const float* rec_c, int32_t width, int32_t height,
@@ -269,9 +283,16 @@ extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const v
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_raster_fwd: bad size");
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
-  raster_fwd_kernel<<<(n_tiles + kWarps - 1) / kWarps, kWarps * 32, 0, stream>>>(
-      (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
-      tiles_x, n_tiles, tile_order, img, t_final, n_contrib);
+  const int wpt = kTile / (2 * g_strip);
+  const int blocks = (n_tiles * wpt + kWarps - 1) / kWarps;
+#define SS_FWD(S)                                                                             \
+  raster_fwd_kernel<S><<<blocks, kWarps * 32, 0, stream>>>(                                   \
+      (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
+      height, tiles_x, n_tiles, tile_order, img, t_final, n_contrib)
+  if (g_strip == 8) SS_FWD(8);
+  else if (g_strip == 4) SS_FWD(4);
+  else SS_FWD(2);
+#undef SS_FWD
   return check_launch("ss_raster_fwd");
 }
 
@@ -282,8 +303,15 @@ extern "C" int ss_raster_bwd(const int32_t* ranges, const int32_t* vals, const v
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_raster_bwd: bad size");
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
-  raster_bwd_kernel<<<(n_tiles + kWarps - 1) / kWarps, kWarps * 32, 0, stream>>>(
-      (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
-      tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d);
+  const int wpt = kTile / (2 * g_strip);
+  const int blocks = (n_tiles * wpt + kWarps - 1) / kWarps;
+#define SS_BWD(S)                                                                             \
+  raster_bwd_kernel<S><<<blocks, kWarps * 32, 0, stream>>>(                                   \
+      (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
+      height, tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d)
+  if (g_strip == 8) SS_BWD(8);
+  else if (g_strip == 4) SS_BWD(4);
+  else SS_BWD(2);
+#undef SS_BWD
   return check_launch("ss_raster_bwd");
 }
