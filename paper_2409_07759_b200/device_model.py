@@ -193,7 +193,9 @@ class DeviceModel:
         frame, view = draws[rank]
         frames = [f for f, _ in draws]
         live = lambda ls, f: ls.start <= f < ls.expire  # noqa: E731
-        stepped = [any(live(g.lifespan, f) for f in frames) for g in state.slices]
+        from .train import stepped_generations
+
+        stepped = stepped_generations(state.slices, frames)
         self._gen_table(stepped)
         n_opt_here = sl * sum(live(g.lifespan, frame) for g in state.slices)
         n_mat_here = sl * sum(live(m.lifespan, frame) for m in state.matured)

@@ -307,6 +307,41 @@ def make_golden_render(ref):
     print(f"golden_render: frame {frame}, {len(gens_json)} generations")
 
 
+def make_codec(ref):
+    """encode_records / pack_slice bytes for both profiles and a whole container
+    (reference codec.py:215-232, 298-320, 365-406)."""
+    C = sys.modules["ref_splatstream.codec"]
+    rng = np.random.default_rng(31)
+    out = {}
+    n = 257
+    arr = random_arrays(ref, rng, n, opacity_lo=0.0, opacity_hi=1.0)
+    arr.quats[:5] = [[1, 0, 0, 0], [0, 1, 0, 0], [0.5, 0.5, 0.5, 0.5], [0.7071, 0, 0.7071, 0],
+                     [-0.3, 0.1, 0.9, -0.2]]
+    out.update(means=arr.means, quats=arr.quats, scales=arr.scales, opacities=arr.opacities,
+               colors=arr.colors)
+    for pid in (0, 1):
+        prof = C.PROFILES[pid]
+        out[f"records_p{pid}"] = np.frombuffer(C.encode_records(arr, prof), dtype=np.uint8)
+        ls = ref.core.Lifespan(7, 7, 12)
+        out[f"slice_p{pid}"] = np.frombuffer(C.pack_slice(arr, ls, prof, swin_size=5),
+                                             dtype=np.uint8)
+        dec = C.decode_records(C.encode_records(arr, prof), prof)
+        out[f"decoded_p{pid}"] = np.concatenate([dec.means, dec.quats, dec.scales,
+                                                 dec.opacities[:, None], dec.colors], 1)
+    tmp = Path(tempfile.mkdtemp(prefix="golden_codec_"))
+    man = C.Manifest(num_gs=20, swin_size=2, fps=30.0, total_frames=3, profile_id=1,
+                     scene_bounds=(-1, -1, -1, 1, 1, 1), camera_count=2)
+    part = arr.take(np.arange(10))
+    with C.ContainerWriter(tmp / "c.swin", man) as w:
+        for i, birth in enumerate([0, 0, 1, 2, 3]):
+            w.write_slice(C.pack_slice(part, ref.core.Lifespan(birth, birth, birth + 2),
+                                       C.PROFILES[1], swin_size=2,
+                                       slice_index=(i if i < 2 else None)))
+    out["container"] = np.frombuffer((tmp / "c.swin").read_bytes(), dtype=np.uint8)
+    np.savez_compressed(OUT / "codec.npz", **out)
+    print("codec: ok")
+
+
 def main():
     ref = load_reference()
     import ref_splatstream.synth  # noqa: F401
@@ -315,6 +350,8 @@ def main():
     make_optim(ref)
     make_train_tiny(ref)
     make_golden_render(ref)
+    import ref_splatstream.codec  # noqa: F401
+    make_codec(ref)
 
 
 if __name__ == "__main__":
