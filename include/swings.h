@@ -103,8 +103,9 @@ int ss_compact_active(const int32_t* row_start, const int32_t* row_expire, int64
                       size_t ws_bytes, ss_stream_t stream);
 
 /* ---- a-3 EWA projection / cull / conic / bbox: raster.py:76-173.
- * For active index i (row = rows ? rows[i] : i): rec_a = (u, v, inv0, inv1),
- * rec_b = (inv2, alpha, r, g), rec_c = b (float32, rounded once from fp64);
+ * For active index i (row = rows ? rows[i] : i): rec_a = (u, v, k inv0, k inv1),
+ * rec_b = (k inv2, log2 alpha, r, g), rec_c = b (float32, rounded once from fp64;
+ * k = -log2(e)/2 so alpha exp(-m/2) = 2^(k m + log2 alpha));
  * depth_key = fp64 z bits (UINT64_MAX when culled); bbox = (x0,x1,y0,y1)
  * pixels, half open; n_tiles = 16x16 tiles the bbox touches (0 when culled). */
 int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_t n, const ss_camera* cam,

@@ -145,8 +145,12 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
   }
   n_tiles[i] = nt;
   depth_key[i] = (uint64_t)__double_as_longlong(p.z);  // z > 0.01: bits are monotone
-  rec_a[i] = make_float4((float)p.ux, (float)p.uy, (float)i0, (float)i1);
-  rec_b[i] = make_float4((float)i2, (float)g.opacity, (float)g.color[0], (float)g.color[1]);
+  // rasterizer record (raster.cu): conic pre-scaled by kappa = -log2(e)/2 so
+  // alpha G = 2^(kappa m + log2 alpha); alpha floored at 2^-100
+  const double kappa = -0.72134752044448170368;
+  const double l2a = fmax(log2(g.opacity), -100.0);
+  rec_a[i] = make_float4((float)p.ux, (float)p.uy, (float)(kappa * i0), (float)(kappa * i1));
+  rec_b[i] = make_float4((float)(kappa * i2), (float)l2a, (float)g.color[0], (float)g.color[1]);
   rec_c[i] = (float)g.color[2];
 }
 

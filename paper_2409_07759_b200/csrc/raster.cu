@@ -1,36 +1,54 @@
 // a-5 blend forward (_kernels.py:20-53) and a-6 blend backward
 // (_kernels.py:56-130) as 16x16-tile rasterizers.
 //
-// Work mapping: one warp per tile (4 tiles per 128-thread CTA, warps are
-// independent).  Lane l owns the 8-pixel column strip x = l % 16,
-// y = 8 (l / 16) + 0..7 of the tile, so per list entry a lane evaluates 8
-// pixels that share dx: the Mahalanobis term is A + dy (B + c dy) with
-// A = a dx^2, B = 2 b dx computed once per entry (2 FMAs per pixel).  The
+// Work mapping: a warp covers 16 x (2 STRIP) pixels of a tile (8 / STRIP
+// warps per tile, 4 warps per CTA, warps independent).  Lane l owns the
+// STRIP-pixel column strip x = l % 16, y = y0 + STRIP (l / 16) + k.  The
 // tile's list (already in the reference's global (z, src) order, see
 // binning.cu) is staged 32 records at a time through a warp-private shared
-// buffer; each record is 36 B (rec_a float4, rec_b float4, rec_c float).
+// buffer; a record is 36 B: rec_a = (u, v, kappa i0, kappa i1), rec_b =
+// (kappa i2, log2 alpha, r, g), rec_c = b with kappa = -log2(e) / 2, so that
 //
-// Per pixel the reference rules are kept: maha > 64 skips, alpha' =
-// min(alpha G, 0.999), accumulation stops once T < 1e-4 (the crossing splat
-// included), no background.  The bbox test of _kernels.py:35-36 is implied
-// by maha <= 64 (the 8-sigma bbox encloses the maha = 64 ellipse).
+//     alpha G = alpha exp(-m/2) = 2^(kappa m + log2 alpha) = 2^(q0 + k (lin + k quad))
+//
+// per strip pixel k with q0, lin, quad computed once per (lane, entry): two
+// FMAs with immediate k per pixel, no separate multiply by alpha.  On
+// Blackwell 3-register FFMA/FMUL issue at half rate, so the per-pixel bodies
+// are written to minimise them.
+//
+// Per pixel the reference rules are kept: maha > 64 skips (kappa m + log2 a
+// >= 64 kappa + log2 a), alpha' = min(alpha G, 0.999), accumulation stops once
+// T < 1e-4 (the crossing splat included), no background.  The bbox test of
+// _kernels.py:35-36 is implied by maha <= 64 (the 8-sigma bbox encloses the
+// maha = 64 ellipse).  Bodies are branch-free: an invalid pixel gets
+// alpha' = 0, which leaves C and T unchanged.
 //
 // Backward: back to front from each pixel's last contributor, T recovered
-// by division by (1 - alpha'), suffix colour S accumulated as in
-// _kernels.py:100-130.  Per entry a lane folds its 8 pixels into 7 partial
-// sums (sum dm, sum dm dy, sum dm dy^2, sum dap G, colour x3) from which the
-// 9 gradient components follow; one transposed warp reduction and one
-// 9-lane float atomic per (tile, entry).
+// by multiplication with 1 / (1 - alpha').  The reference's suffix colour S
+// (_kernels.py:100-130) only enters through sum_ch dC_ch S_ch, so a pixel
+// carries the scalar Q = dC . S (Q += w dC . c) and d alpha' = T dC.c - Q/(1-a').
+// With t = alpha G d alpha' (zero when clamped), g_alpha = sum t / alpha and
+// dm = -t/2, and the strip sums sum t, sum t k, sum t k^2 give every
+// footprint gradient; one transposed warp reduction and one 9-lane float
+// atomic per (warp, entry).
 #include "ss_common.cuh"
 
 namespace ss {
 
-constexpr int kWarps = 4;        // tiles per CTA
-constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // exp(-m/2) = 2^(m * this)
+constexpr int kWarps = 4;  // warps per CTA
+constexpr float kKappa = -0.72134752044448170368f;  // -log2(e) / 2
+constexpr float kInvKappa = -1.38629436111989061883f;  // 1 / kappa = -2 ln 2
+constexpr float kMahaKappa = kMahaMax * kKappa;       // 64 kappa
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
@@ -55,6 +73,27 @@ __device__ __forceinline__ void stage_load(WarpStage& st, int lane, int idx, int
   }
 }
 
+// Per (lane, entry) coefficients of kappa m + log2 alpha over the strip.
+struct StripQuad {
+  float q0, lin, quad, thr, dx, dy0;
+};
+
+__device__ __forceinline__ StripQuad strip_quad(const float4& a, const float4& b, float fx,
+                                                float fy0) {
+  StripQuad s;
+  s.dx = fx - a.x;
+  s.dy0 = fy0 - a.y;
+  // kappa m(dy) = A + dy (B + C dy), A = ka dx^2, B = 2 kb dx, C = kc
+  const float A = a.z * s.dx * s.dx;
+  const float B = 2.f * a.w * s.dx;
+  const float C = b.x;
+  s.q0 = fmaf(s.dy0, fmaf(C, s.dy0, B), A) + b.y;
+  s.lin = fmaf(2.f * C, s.dy0, B);
+  s.quad = C;
+  s.thr = kMahaKappa + b.y;
+  return s;
+}
+
 template <int STRIP>
 __global__ void __launch_bounds__(kWarps * 32)
     raster_fwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
@@ -64,8 +103,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                       float* __restrict__ img, float* __restrict__ t_final,
                       int32_t* __restrict__ n_contrib) {
   __shared__ WarpStage s_stage[kWarps];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int WPT = kTile / (2 * STRIP);  // warps per tile
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gwarp = blockIdx.x * kWarps + warp;
   const int slot_id = gwarp / WPT, sub = gwarp % WPT;
   if (slot_id >= n_tiles) return;
@@ -75,50 +114,43 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int px = tx * kTile + (lane & 15);
   const int py0 = ty * kTile + sub * 2 * STRIP + (lane >> 4) * STRIP;
   const float fx = (float)px, fy0 = (float)py0;
-  unsigned live = 0;
-#pragma unroll
-  for (int k = 0; k < STRIP; ++k)
-    if (px < width && py0 + k < height) live |= 1u << k;
   float T[STRIP], c0[STRIP], c1[STRIP], c2[STRIP];
   int last[STRIP];
 #pragma unroll
   for (int k = 0; k < STRIP; ++k) {
-    T[k] = 1.f;
+    // pixels outside the image start "saturated" (T = 0) and never contribute
+    T[k] = (px < width && py0 + k < height) ? 1.f : 0.f;
     c0[k] = c1[k] = c2[k] = 0.f;
     last[k] = 0;
   }
   const int2 rg = ranges[tile];
   for (int base = rg.x; base < rg.y; base += 32) {
+    bool live = false;
+#pragma unroll
+    for (int k = 0; k < STRIP; ++k) live |= T[k] >= kTMin;
     if (!__any_sync(0xffffffffu, live)) break;
     __syncwarp();
     stage_load(st, lane, base + lane, rg.y, vals, rec_a, rec_b, rec_c);
     __syncwarp();
-    if (live) {
-      const int cnt = min(32, rg.y - base);
-      for (int j = 0; j < cnt; ++j) {
-        const float4 a = st.a[j];
-        const float4 b = st.b[j];
-        const float cb = st.c[j];
-        const float dx = fx - a.x, dy0 = fy0 - a.y;
-        const float A = a.z * dx * dx, B = 2.f * a.w * dx, cc = b.x;
-        const int pos = base - rg.x + j + 1;
-        // branch-free over the strip: invalid pixels get alpha' = 0, which
-        // leaves C and T untouched, so the 8 chains interleave freely
+    if (!live) continue;
+    const int cnt = min(32, rg.y - base);
+    for (int j = 0; j < cnt; ++j) {
+      const float4 a = st.a[j];
+      const float4 b = st.b[j];
+      const float cb = st.c[j];
+      const StripQuad s = strip_quad(a, b, fx, fy0);
+      const int pos = base - rg.x + j + 1;
 #pragma unroll
-        for (int k = 0; k < STRIP; ++k) {
-          const float dy = dy0 + (float)k;
-          const float m = fmaf(dy, fmaf(cc, dy, B), A);
-          const bool valid = ((live >> k) & 1u) && (m <= kMahaMax);
-          const float G = ex2(m * kNegHalfLog2e);
-          const float ap = valid ? fminf(b.y * G, kAlphaMax) : 0.f;
-          const float w = ap * T[k];
-          c0[k] = fmaf(b.z, w, c0[k]);
-          c1[k] = fmaf(b.w, w, c1[k]);
-          c2[k] = fmaf(cb, w, c2[k]);
-          T[k] *= 1.f - ap;
-          last[k] = valid ? pos : last[k];
-          live &= ~((unsigned)(T[k] < kTMin) << k);
-        }
+      for (int k = 0; k < STRIP; ++k) {
+        const float e = fmaf((float)(k * k), s.quad, fmaf((float)k, s.lin, s.q0));
+        const bool valid = (T[k] >= kTMin) && (e >= s.thr);
+        const float ap = valid ? fminf(ex2(e), kAlphaMax) : 0.f;
+        const float w = ap * T[k];
+        c0[k] = fmaf(b.z, w, c0[k]);
+        c1[k] = fmaf(b.w, w, c1[k]);
+        c2[k] = fmaf(cb, w, c2[k]);
+        T[k] = fmaf(-ap, T[k], T[k]);
+        last[k] = valid ? pos : last[k];
       }
     }
   }
@@ -161,8 +193,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                       const float* __restrict__ dimg, const float* __restrict__ t_final,
                       const int32_t* __restrict__ n_contrib, float* __restrict__ g2d) {
   __shared__ WarpStage s_stage[kWarps];
+  constexpr int WPT = kTile / (2 * STRIP);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int WPT = kTile / (2 * STRIP);  // warps per tile
   const int gwarp = blockIdx.x * kWarps + warp;
   const int slot_id = gwarp / WPT, sub = gwarp % WPT;
   if (slot_id >= n_tiles) return;
@@ -172,13 +204,13 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int px = tx * kTile + (lane & 15);
   const int py0 = ty * kTile + sub * 2 * STRIP + (lane >> 4) * STRIP;
   const float fx = (float)px, fy0 = (float)py0;
-  float T[STRIP], d0[STRIP], d1[STRIP], d2[STRIP], S0[STRIP], S1[STRIP], S2[STRIP];
+  float T[STRIP], d0[STRIP], d1[STRIP], d2[STRIP], Q[STRIP];
   int last[STRIP];
   int my_max = 0;
 #pragma unroll
   for (int k = 0; k < STRIP; ++k) {
     const int py = py0 + k;
-    S0[k] = S1[k] = S2[k] = 0.f;
+    Q[k] = 0.f;
     if (px < width && py < height) {
       const int64_t p = (int64_t)py * width + px;
       T[k] = t_final[p];
@@ -207,51 +239,45 @@ __global__ void __launch_bounds__(kWarps * 32)
       const float4 a = st.a[j];
       const float4 b = st.b[j];
       const float cb = st.c[j];
-      const float dx = fx - a.x, dy0 = fy0 - a.y;
-      const float A = a.z * dx * dx, B = 2.f * a.w * dx, cc = b.x;
-      const float alpha = b.y;
-      float sdm = 0.f, sdmy = 0.f, sdmyy = 0.f, sal = 0.f, sc0 = 0.f, sc1 = 0.f, sc2 = 0.f;
+      const StripQuad s = strip_quad(a, b, fx, fy0);
+      float sc0 = 0.f, sc1 = 0.f, sc2 = 0.f, st0 = 0.f, st1 = 0.f, st2 = 0.f;
       bool touched = false;
 #pragma unroll
       for (int k = 0; k < STRIP; ++k) {
-        // branch-free: an invalid pixel has alpha' = 0 (T and S unchanged) and
-        // its d alpha' is zeroed, so it contributes nothing
-        const float dy = dy0 + (float)k;
-        const float m = fmaf(dy, fmaf(cc, dy, B), A);
-        const bool valid = (pos < last[k]) && (m <= kMahaMax);
+        const float e = fmaf((float)(k * k), s.quad, fmaf((float)k, s.lin, s.q0));
+        const bool valid = (pos < last[k]) && (e >= s.thr);
         touched |= valid;
-        const float G = ex2(m * kNegHalfLog2e);
-        const float aG = alpha * G;
+        const float aG = ex2(e);
         const float ap = valid ? fminf(aG, kAlphaMax) : 0.f;
-        const float inv = __frcp_rn(1.f - ap);
+        const float inv = rcp(1.f - ap);
         T[k] *= inv;  // T before this splat
         const float w = ap * T[k];
         sc0 = fmaf(d0[k], w, sc0);
         sc1 = fmaf(d1[k], w, sc1);
         sc2 = fmaf(d2[k], w, sc2);
-        const float dap_raw = d0[k] * (b.z * T[k] - S0[k] * inv) +
-                              d1[k] * (b.w * T[k] - S1[k] * inv) +
-                              d2[k] * (cb * T[k] - S2[k] * inv);
-        S0[k] = fmaf(b.z, w, S0[k]);
-        S1[k] = fmaf(b.w, w, S1[k]);
-        S2[k] = fmaf(cb, w, S2[k]);
+        const float dc = fmaf(d2[k], cb, fmaf(d1[k], b.w, d0[k] * b.z));
+        const float dap = fmaf(T[k], dc, -Q[k] * inv);
+        Q[k] = fmaf(w, dc, Q[k]);
         // clamped splats pass no alpha/footprint gradient (_kernels.py:120-121)
-        const float dap = (valid && aG <= kAlphaMax) ? dap_raw : 0.f;
-        sal = fmaf(dap, G, sal);
-        const float dm = -0.5f * G * alpha * dap;
-        sdm += dm;
-        sdmy = fmaf(dm, dy, sdmy);
-        sdmyy = fmaf(dm * dy, dy, sdmyy);
+        const float t = (valid && aG <= kAlphaMax) ? aG * dap : 0.f;
+        st0 += t;
+        st1 = fmaf((float)k, t, st1);
+        st2 = fmaf((float)(k * k), t, st2);
       }
       if (!__any_sync(0xffffffffu, touched)) continue;
-      // g_mean2d = -2 dm (conic d), g_inv2d = dm (dx^2, 2 dx dy, dy^2) summed over the strip
+      // strip sums -> 9 gradient components; dm = -t/2, G d alpha' = t / alpha
+      const float i0 = a.z * kInvKappa, i1 = a.w * kInvKappa, i2 = b.x * kInvKappa;
+      const float dx = s.dx, dy0 = s.dy0;
+      const float sdm = -0.5f * st0;
+      const float sdmy = -0.5f * fmaf(dy0, st0, st1);
+      const float sdmyy = -0.5f * fmaf(dy0, fmaf(dy0, st0, 2.f * st1), st2);
       float v[16];
-      v[0] = -2.f * (a.z * dx * sdm + a.w * sdmy);
-      v[1] = -2.f * (a.w * dx * sdm + cc * sdmy);
+      v[0] = -2.f * (i0 * dx * sdm + i1 * sdmy);
+      v[1] = -2.f * (i1 * dx * sdm + i2 * sdmy);
       v[2] = dx * dx * sdm;
       v[3] = 2.f * dx * sdmy;
       v[4] = sdmyy;
-      v[5] = sal;
+      v[5] = st0 * ex2(-b.y);
       v[6] = sc0;
       v[7] = sc1;
       v[8] = sc2;
