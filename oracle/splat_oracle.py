@@ -314,11 +314,13 @@ def render_arrays_backward(cam, means, quats, scales, opacities, colors, grad_im
 # a-4: tile binning restated (build design; reproduces the reference order)
 # --------------------------------------------------------------------------
 
-def tile_bins(cache, width, height, tile=TILE):
+def tile_bins(cache, width, height, tile=TILE, exact=True):
     """SURVEY.md §8 a-4.  For each kept splat i (index into the kept subset)
     with depth rank r_i under the reference's global (z, src) order
     (raster.py:153), emit one key ``tile_id << 21 | r_i`` per 16x16 tile
-    overlapping its half-open pixel bbox [x0,x1)x[y0,y1) (raster.py:144-150);
+    overlapping its half-open pixel bbox [x0,x1)x[y0,y1) (raster.py:144-150)
+    -- with ``exact``, only tiles the maha <= 64 ellipse reaches
+    (tile_keep_mask; dropped tiles hold no pixel the reference blends) --
     sort keys ascending; a tile's range is the run of its tile id.
 
     Returns dict(keys (K,) uint64 sorted, vals (K,) int64 kept-subset index,
@@ -344,6 +346,10 @@ def tile_bins(cache, width, height, tile=TILE):
     w = np.repeat(tx1 - tx0, counts)
     tx = np.repeat(tx0, counts) + local % np.maximum(w, 1)
     ty = np.repeat(ty0, counts) + local // np.maximum(w, 1)
+    if exact and total:
+        keep = tile_keep_mask(cache, owner, tx, ty, tile)
+        owner, tx, ty = owner[keep], tx[keep], ty[keep]
+        total = int(keep.sum())
     tile_id = ty * tiles_x + tx
     keys = (tile_id.astype(np.uint64) << np.uint64(RANK_BITS)) | rank[owner].astype(np.uint64)
     srt = np.argsort(keys, kind="stable")
@@ -613,3 +619,44 @@ def relocate(params_list, m_list, v_list, threshold, uniforms):
             m_list[tg][k][tr] = 0.0
             v_list[tg][k][tr] = 0.0
     return len(dead)
+
+
+# --------------------------------------------------------------------------
+# exact ellipse-vs-tile culling (build refinement of a-4; no pixel changes)
+# --------------------------------------------------------------------------
+
+CULL_MARGIN = 64.0 * (1.0 + 1e-9)
+
+
+def tile_min_maha(i0, i1, i2, u, v, X0, X1, Y0, Y1):
+    """Minimum over the continuous rectangle [X0, X1] x [Y0, Y1] (pixel-centre
+    coordinates) of m = i0 dx^2 + 2 i1 dx dy + i2 dy^2, dx = x - u, dy = y - v.
+    Vectorised restatement of project.cu tile_min_maha (same operation order).
+    A tile whose minimum exceeds CULL_MARGIN holds no pixel the reference's
+    loop would blend (maha > 64 skip, _kernels.py:39-41)."""
+    ax, bx = X0 - u, X1 - u
+    ay, by = Y0 - v, Y1 - v
+    inside = (ax <= 0.0) & (bx >= 0.0) & (ay <= 0.0) & (by >= 0.0)
+
+    def q(dx, dy):
+        return (i0 * dx) * dx + ((2.0 * i1) * dx) * dy + (i2 * dy) * dy
+
+    best = np.full(np.shape(u), np.inf)
+    for ex in (ax, bx):          # vertical edges: dx fixed, minimise over dy
+        dy = np.clip(-(i1 * ex) / i2, ay, by)
+        best = np.minimum(best, q(ex, dy))
+    for ey in (ay, by):          # horizontal edges: dy fixed, minimise over dx
+        dx = np.clip(-(i1 * ey) / i0, ax, bx)
+        best = np.minimum(best, q(dx, ey))
+    return np.where(inside, 0.0, best)
+
+
+def tile_keep_mask(cache, owner, tx, ty, tile=TILE):
+    x0, x1, y0, y1 = cache["bbox"]
+    i0, i1, i2 = cache["inv2d"][owner].T
+    u, v = cache["mean2d"][owner].T
+    X0 = np.maximum(tx * tile, x0[owner]).astype(np.float64)
+    X1 = np.minimum(tx * tile + tile - 1, x1[owner] - 1).astype(np.float64)
+    Y0 = np.maximum(ty * tile, y0[owner]).astype(np.float64)
+    Y1 = np.minimum(ty * tile + tile - 1, y1[owner] - 1).astype(np.float64)
+    return tile_min_maha(i0, i1, i2, u, v, X0, X1, Y0, Y1) <= CULL_MARGIN

@@ -27,11 +27,14 @@ __global__ void gather_counts_kernel(const int32_t* __restrict__ order,
   if (k == n) out[k] = 0;
 }
 
-// One warp per splat in rank order; lanes stride over the splat's tiles.
+// One warp per splat in rank order; lanes stride over the splat's bbox tiles,
+// keep those the ellipse reaches (tile_keeps, same test as the count in
+// project.cu) and compact them with a ballot prefix.
 __global__ void emit_pairs_kernel(const int32_t* __restrict__ order,
                                   const int32_t* __restrict__ offsets,
-                                  const int4* __restrict__ bbox, int32_t n, int32_t tiles_x,
-                                  uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+                                  const int4* __restrict__ bbox, const double* __restrict__ geom,
+                                  int32_t n, int32_t tiles_x, uint32_t* __restrict__ keys,
+                                  int32_t* __restrict__ vals) {
   const int lane = threadIdx.x & 31;
   int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (k >= n) return;
@@ -41,12 +44,24 @@ __global__ void emit_pairs_kernel(const int32_t* __restrict__ order,
   const int32_t i = order[k];
   const int4 bb = bbox[i];
   const int tx0 = bb.x / kTile, tx1 = (bb.y - 1) / kTile + 1;
-  const int ty0 = bb.z / kTile;
+  const int ty0 = bb.z / kTile, ty1 = (bb.w - 1) / kTile + 1;
   const int w = tx1 - tx0;
-  for (int j = lane; j < cnt; j += 32) {
+  const int total = w * (ty1 - ty0);
+  double gl[5];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) gl[c] = geom[(int64_t)i * 5 + c];
+  int written = 0;
+  for (int j0 = 0; j0 < total; j0 += 32) {
+    const int j = j0 + lane;
     const int ty = ty0 + j / w, tx = tx0 + j % w;
-    keys[off + j] = (uint32_t)(ty * tiles_x + tx);
-    vals[off + j] = i;
+    const bool keep = j < total && tile_keeps(gl, tx, ty, bb);
+    const unsigned ball = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int at = off + written + __popc(ball & ((1u << lane) - 1));
+      keys[at] = (uint32_t)(ty * tiles_x + tx);
+      vals[at] = i;
+    }
+    written += __popc(ball);
   }
 }
 
@@ -141,12 +156,13 @@ extern "C" int ss_tile_offsets(const int32_t* order, const int32_t* n_tiles, int
 }
 
 extern "C" int ss_emit_tile_pairs(const int32_t* order, const int32_t* offsets,
-                                  const int32_t* bbox, int32_t n, int32_t tiles_x, uint32_t* keys,
-                                  int32_t* vals, cudaStream_t stream) {
+                                  const int32_t* bbox, const double* geom, int32_t n,
+                                  int32_t tiles_x, uint32_t* keys, int32_t* vals,
+                                  cudaStream_t stream) {
   if (n < 0 || tiles_x <= 0) return set_error(SS_ERR_INVALID, "ss_emit_tile_pairs: bad sizes");
   if (n == 0) return SS_OK;
   emit_pairs_kernel<<<grid_for((int64_t)n * 32, 256), 256, 0, stream>>>(
-      order, offsets, (const int4*)bbox, n, tiles_x, keys, vals);
+      order, offsets, (const int4*)bbox, geom, n, tiles_x, keys, vals);
   return check_launch("ss_emit_tile_pairs");
 }
 

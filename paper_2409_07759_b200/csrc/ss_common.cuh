@@ -83,6 +83,36 @@ __device__ __forceinline__ void quat_to_rot(const double q[4], double r[3][3]) {
   r[2][2] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(y, y))));
 }
 
+// Exact ellipse-vs-tile test (a-4 refinement): minimum over the continuous
+// rectangle [X0, X1] x [Y0, Y1] of pixel centres of m = i0 dx^2 + 2 i1 dx dy +
+// i2 dy^2.  Same operation order as oracle/splat_oracle.py tile_min_maha, so
+// keep/drop decisions (and therefore tile keys) are bit-identical to it.
+constexpr double kCullMargin = 64.0 * (1.0 + 1e-9);
+
+__device__ __forceinline__ double quad_form(double i0, double i1, double i2, double dx, double dy) {
+  return dadd(dadd(dmul(dmul(i0, dx), dx), dmul(dmul(dmul(2.0, i1), dx), dy)),
+              dmul(dmul(i2, dy), dy));
+}
+
+__device__ __forceinline__ double clampd(double x, double lo, double hi) {
+  return fmin(fmax(x, lo), hi);
+}
+
+__device__ __forceinline__ bool tile_keeps(const double* geom, int tx, int ty, int4 bb) {
+  // geom = (u, v, i0, i1, i2) in fp64; bb = pixel bbox (x0, x1, y0, y1) half open
+  const double u = geom[0], v = geom[1], i0 = geom[2], i1 = geom[3], i2 = geom[4];
+  const double ax = (double)max(tx * SS_TILE, bb.x) - u;
+  const double bx = (double)min(tx * SS_TILE + SS_TILE - 1, bb.y - 1) - u;
+  const double ay = (double)max(ty * SS_TILE, bb.z) - v;
+  const double by = (double)min(ty * SS_TILE + SS_TILE - 1, bb.w - 1) - v;
+  if (ax <= 0.0 && bx >= 0.0 && ay <= 0.0 && by >= 0.0) return true;
+  double best = quad_form(i0, i1, i2, ax, clampd(ddiv(-dmul(i1, ax), i2), ay, by));
+  best = fmin(best, quad_form(i0, i1, i2, bx, clampd(ddiv(-dmul(i1, bx), i2), ay, by)));
+  best = fmin(best, quad_form(i0, i1, i2, clampd(ddiv(-dmul(i1, ay), i0), ax, bx), ay));
+  best = fmin(best, quad_form(i0, i1, i2, clampd(ddiv(-dmul(i1, by), i0), ax, bx), by));
+  return best <= kCullMargin;
+}
+
 // Philox4x32-10 counter-based generator (Salmon et al., SC'11).
 struct Philox4 {
   uint32_t v[4];

@@ -180,6 +180,24 @@ class DeviceModel:
         # synchronizes once (tile-pair count readback) after this point
         self.gen_dev.copy_(self.gen_host, non_blocking=True)
 
+    def compact(self, frame: int):
+        """Active row ids of `frame` (a-2): optimizable rows of generations in
+        state.slices order, then matured rows in archive order.  Returns
+        (rows device tensor, n_active, n_active_optimizable)."""
+        state, sl = self.state, self.sl
+        if self.dirty:
+            self.sync_lifespans()
+        live = lambda ls: ls.start <= frame < ls.expire  # noqa: E731
+        n_opt = sl * sum(live(g.lifespan) for g in state.slices)
+        n_mat = sl * sum(live(m.lifespan) for m in state.matured)
+        lib = L.lib()
+        L.check(lib.ss_compact_active(L.ptr(self.row_start), L.ptr(self.row_expire), self.num_gs,
+                                      len(state.matured) * sl, L.ptr(self.blk_map), sl, frame,
+                                      L.ptr(self.active_rows), L.ptr(self.counts),
+                                      L.ptr(self.ws_compact), self.ws_compact.numel(),
+                                      L.stream_ptr()), "compact_active")
+        return self.active_rows, n_opt + n_mat, n_opt
+
     # ------------------------------------------------------------------ step
     def train_step(self, draws, rank, dataset, it):
         """One training view (train.py:375-417).  `draws` are the (frame, view)
@@ -188,8 +206,6 @@ class DeviceModel:
         state, cfg, sl = self.state, self.cfg, self.sl
         lib = L.lib()
         sp = L.stream_ptr()
-        if self.dirty:
-            self.sync_lifespans()
         frame, view = draws[rank]
         frames = [f for f, _ in draws]
         live = lambda ls, f: ls.start <= f < ls.expire  # noqa: E731
@@ -197,14 +213,7 @@ class DeviceModel:
 
         stepped = stepped_generations(state.slices, frames)
         self._gen_table(stepped)
-        n_opt_here = sl * sum(live(g.lifespan, frame) for g in state.slices)
-        n_mat_here = sl * sum(live(m.lifespan, frame) for m in state.matured)
-        n = n_opt_here + n_mat_here
-        L.check(lib.ss_compact_active(L.ptr(self.row_start), L.ptr(self.row_expire), self.num_gs,
-                                      len(state.matured) * sl, L.ptr(self.blk_map), sl, frame,
-                                      L.ptr(self.active_rows), L.ptr(self.counts),
-                                      L.ptr(self.ws_compact), self.ws_compact.numel(), sp),
-                "compact_active")
+        _, n, n_opt_here = self.compact(frame)
         self.grads.zero_()
         cam = dataset.cameras[view]
         gt = dataset.device_frame(frame, view)

@@ -63,6 +63,8 @@ def test_tile_bins_reproduce_reference_order():
     rank = np.empty(len(order), np.int64)
     rank[order] = np.arange(len(order))
     x0, x1, y0, y1 = cache["bbox"]
+    loose = O.tile_bins(cache, cam.width, cam.height, exact=False)
+    m2, inv = cache["mean2d"], cache["inv2d"]
     for t in range(bins["tiles_x"] * bins["tiles_y"]):
         s, e = bins["ranges"][t]
         lst = bins["vals"][s:e]
@@ -70,8 +72,18 @@ def test_tile_bins_reproduce_reference_order():
         tx, ty = t % bins["tiles_x"], t // bins["tiles_x"]
         hit = ((x0 < (tx + 1) * 16) & (x1 > tx * 16) & (y0 < (ty + 1) * 16) & (y1 > ty * 16)
                & (x1 > x0) & (y1 > y0))
-        assert set(np.nonzero(hit)[0]) == set(lst.tolist())
+        ls, le = loose["ranges"][t]
+        assert set(np.nonzero(hit)[0]) == set(loose["vals"][ls:le].tolist())
+        assert set(lst.tolist()) <= set(np.nonzero(hit)[0])
+        # every dropped splat has maha > 64 at every pixel of the tile
+        dropped = sorted(set(np.nonzero(hit)[0]) - set(lst.tolist()))
+        ys, xs = np.mgrid[ty * 16:min(ty * 16 + 16, cam.height), tx * 16:min(tx * 16 + 16, cam.width)]
+        for sidx in dropped:
+            dx, dy = xs - m2[sidx, 0], ys - m2[sidx, 1]
+            mm = inv[sidx, 0] * dx * dx + 2 * inv[sidx, 1] * dx * dy + inv[sidx, 2] * dy * dy
+            assert mm.min() > 64.0
     assert bins["K"] == len(bins["keys"]) and np.all(np.diff(bins["keys"].astype(np.float64)) >= 0)
+    assert bins["K"] < loose["K"]
 
 
 def test_golden_render_frontend_fixture():
