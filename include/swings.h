@@ -206,6 +206,16 @@ int ss_relocate(double* opt, double* adam_m, double* adam_v, int64_t n_rows,
                 const double* uniforms, uint64_t seed, uint64_t counter, int32_t* out_counts,
                 void* ws, size_t ws_bytes, ss_stream_t stream);
 
+/* ---- a-13 / §8(f)-1 export records: codec.py:195-266.  rows are n direct-
+ * space Gaussian rows (f64); profile 0 writes 56-byte, profile 1 30-byte
+ * little-endian records, byte-identical to encode_records.  *bad (device
+ * int, caller zeroes) is set when a row holds a non-finite value (the
+ * reference raises CodecError).  ss_decode_records is decode_records. */
+int ss_encode_records(const double* rows, int64_t n, int32_t profile, uint8_t* out,
+                      int32_t* bad, ss_stream_t stream);
+int ss_decode_records(const uint8_t* data, int64_t n, int32_t profile, double* rows,
+                      ss_stream_t stream);
+
 /* Direct-space snapshot of optimizable rows (train.py:155-161 + 474):
  * dst[i] = (mean, quat, exp(log_scale), sigmoid(logit), color) of src[i]. */
 int ss_to_direct(const double* src, double* dst, int64_t n, ss_stream_t stream);

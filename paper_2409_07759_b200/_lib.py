@@ -74,6 +74,8 @@ _SIGNATURES = {
     "ss_relocate": ([P, P, P, I64, I32, P, c_double, P, c_uint64, c_uint64, P, P, c_size_t, P],
                     c_int),
     "ss_to_direct": ([P, P, I64, P], c_int),
+    "ss_encode_records": ([P, I64, I32, P, P, P], c_int),
+    "ss_decode_records": ([P, I64, I32, P, P], c_int),
 }
 
 _LIB = None

@@ -156,6 +156,9 @@ class DeviceModel:
                 "to_direct")
         return block, GaussianArrays.from_rows(dst.cpu().numpy())
 
+    def block_rows(self, block: int):
+        return self.mat[block * self.sl:(block + 1) * self.sl]
+
     def release_block(self, block: int):
         if block >= 0:
             self.free_blocks.append(block)
