@@ -51,6 +51,7 @@ CONFIGS = {
             dynerf=True),
 }
 METRIC = "window training views/sec (1352x1014)"
+METRIC5 = "render-only streaming playback frames/sec (1920x1080)"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 
 
@@ -391,6 +392,122 @@ def cpu_state(c):
     return means, quats, scales, opac, cols, opt
 
 
+def build_player(n_total=1_000_000, swin=20, views=20, W=1920, H=1080, seed=7):
+    """Config 5: a 1M-splat slot buffer (swin slots of n/swin decoded records)
+    from the DyNeRF-shaped recipe, arc cameras at 1920x1080, focal 2100,
+    70-degree arc (test_acceptance.py:385)."""
+    from paper_2409_07759_b200 import player, synth
+    from paper_2409_07759_b200.codec import DecodedSlice, SliceHeader
+    from paper_2409_07759_b200.core import GaussianArrays, Lifespan
+
+    cams = synth.arc_cameras(views, W, H, radius=3.0, focal=2100.0, arc_degrees=70.0)
+    k = (300.0 / n_total) ** (1.0 / 3.0)
+    scene = synth.make_scene(seed, 300, cams, n_total, scale_range=(0.045 * k, 0.1 * k))
+    g0 = scene.gaussians_at(0)
+    rng = np.random.default_rng(0)
+    idx = np.concatenate([np.arange(len(g0)), rng.integers(0, len(g0), n_total - len(g0))])
+    arr = g0.take(idx)
+    sl = n_total // swin
+    slices = []
+    for s_ in range(swin):
+        part = arr.take(np.arange(s_ * sl, (s_ + 1) * sl))
+        ls = Lifespan(0, 0, 1 << 30)
+        slices.append(DecodedSlice(SliceHeader(0, s_, sl), part, ls, np.ones(sl, bool)))
+    buf = player.PlayerBuffer(slices, swin)
+    buf.to_device()
+    return buf, cams, arr, sl
+
+
+def run_render_only(args, dp):
+    """--config 5: frames/s of the render-only playback path (compaction over
+    the slot buffer in (birth, slot) order -> projection -> binning -> raster
+    forward) at 1920x1080, 1M splats; e2e adds per frame one slot update
+    from wire bytes (H2D, GPU decode) and the frame read back to the host."""
+    import torch
+
+    from paper_2409_07759_b200 import codec
+    from paper_2409_07759_b200.core import StreamParams
+
+    world = 1 if dp is None else dp.world_size
+    rank = 0 if dp is None else dp.rank
+    buf, cams, arr, sl = build_player()
+    W, H = cams[0].width, cams[0].height
+
+    def frames(n, start=0):
+        for i in range(n):
+            buf.render_device(cams[(start + i * world + rank) % len(cams)], 0)
+
+    frames(args.warmup)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clocks:
+        if dp is not None:
+            dp.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        frames(args.steps)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dp is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dp.dist.all_reduce(t, op=dp.dist.ReduceOp.MAX)
+        ms = float(t.item())
+    out = {"metric": METRIC5, "value": world * args.steps / (ms / 1e3), "unit": "frames/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (DyNeRF-shaped recipe, 1M splats in 20 slots)",
+           "config": {"workload": "render-only streaming playback: 1M lifespan Gaussians, "
+                                  "1920x1080 novel views", "width": W, "height": H,
+                      "splats": len(arr), "slots": 20, "parallelism": f"replicas{world}",
+                      "l2": "per-frame working set > 126 MB L2 (tile pairs); no explicit flush"},
+           "clocks": clocks.summary()}
+    # e2e: one slot update from wire bytes per frame + frame read back
+    prof = codec.PROFILES[1]
+    params = StreamParams(swin_size=20, num_gs=len(arr), fps=30.0, bytes_per_gaussian=30,
+                          total_frames=1 << 20)
+    blobs = []
+    from paper_2409_07759_b200.core import Lifespan
+    for s_ in range(4):
+        part = arr.take(np.arange(s_ * sl, (s_ + 1) * sl))
+        blobs.append(codec.pack_slice(part, Lifespan(s_, s_, s_ + 20), prof, 20))
+    h2d = d2h = 0
+    pinned = torch.empty((H, W, 3), dtype=torch.float32).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record()
+    for i in range(args.steps):
+        blob = blobs[i % len(blobs)]
+        buf.apply_bytes(blob, prof, params)
+        h2d += len(blob)
+        img = buf.render_device(cams[(i * world + rank) % len(cams)], 19)
+        pinned.copy_(img)
+        d2h += img.numel() * 4
+    e1.record()
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1)
+    out["e2e"] = {"value": world * args.steps / (ms_e2e / 1e3), "unit": "frames/s",
+                  "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+                  "api": "PlayerBuffer.apply_bytes (GPU decode) + render_device + frame D2H"}
+    pipe = buf.to_device().pipe
+    pipe.enable_timing(True)
+    ku = []
+    for i in range(10):
+        buf.render_device(cams[i % len(cams)], 0)
+        ku.append(pipe.k_used())
+    kms = pipe.kernel_ms()
+    pipe.enable_timing(False)
+    t_f = kms.get("raster_fwd", 0.0) / 10 / 1e3
+    P = W * H
+    b = 40.0 * float(np.mean(ku)) + 20.0 * P
+    peak, kind = load_peaks()
+    out["roofline"] = {"bound": "hbm", "achieved": b / t_f / 1e9, "peak": peak, "unit": "GB/s",
+                       "frac": b / t_f / 1e9 / peak, "traffic": None, "kernel": "raster_fwd",
+                       "peak_source": kind, "bytes_per_view": b, "K_used": float(np.mean(ku)),
+                       "ms_per_view": {"raster_fwd": kms.get("raster_fwd", 0.0) / 10}}
+    return out
+
+
 def run_reference(args, c):
     from oracle import splat_oracle as O
 
@@ -422,12 +539,68 @@ def run_reference(args, c):
     }
 
 
+def run_reference_render(args):
+    """Config 5 on the host: the oracle's reference forward (global-order
+    blend, fp64, all threads) over crop cameras of a 1920x1080 view of the 1M
+    slot buffer, extrapolated by P / P_crop."""
+    from oracle import splat_oracle as O
+    from paper_2409_07759_b200.synth import make_scene
+
+    O.build_oracle()
+    threads = O.default_threads()
+    n = 1_000_000
+    k = (300.0 / n) ** (1.0 / 3.0)
+    scene = make_scene(7, 300, [], n, scale_range=(0.045 * k, 0.1 * k))
+    g0 = scene.gaussians_at(0)
+    rng = np.random.default_rng(0)
+    idx = np.concatenate([np.arange(len(g0)), rng.integers(0, len(g0), n - len(g0))])
+    arr = g0.take(idx)
+    W, H, f = 1920, 1080, 2100.0
+    half = np.radians(70.0) / 2
+    ang = -half
+    center = np.array([3 * np.sin(ang), 0.25 * np.sin(2.1 * ang), -3 * np.cos(ang)])
+    fwd = -center / np.linalg.norm(center)
+    right = np.cross([0.0, 1.0, 0.0], fwd)
+    right /= np.linalg.norm(right)
+    R = np.stack([right, np.cross(fwd, right), fwd])
+    crop = 96
+    times = []
+    for _ in range(max(args.steps, 1)):
+        t_pix = 0.0
+        t0 = time.perf_counter()
+        cache = O.project_arrays(_Cam(W, H, f, f, W / 2, H / 2, R, -R @ center), arr.means,
+                                 arr.quats, arr.scales, arr.opacities, arr.colors)
+        t_gauss = time.perf_counter() - t0
+        for xc, yc in [(W // 4, H // 4), (3 * W // 4, H // 4), (W // 4, 3 * H // 4),
+                       (3 * W // 4, 3 * H // 4)]:
+            cc = _Cam(crop, crop, f, f, W / 2 - (xc - crop // 2), H / 2 - (yc - crop // 2), R,
+                      -R @ center)
+            c2 = O.project_arrays(cc, arr.means, arr.quats, arr.scales, arr.opacities, arr.colors)
+            t1 = time.perf_counter()
+            if c2 is not None:
+                O.blend_forward(c2, crop, crop, nthreads=threads)
+            t_pix += time.perf_counter() - t1
+        times.append(t_pix / 4 * (W * H) / (crop * crop) + t_gauss)
+    tv = float(np.mean(times))
+    v = 1.0 / tv
+    return {"metric": METRIC5, "value": v, "unit": "frames/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tv * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "render-only streaming playback: 1M lifespan Gaussians, "
+                                   "1920x1080 novel views", "threads": threads},
+            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
+                             "sample": f"crop-extrapolated: 4 crops of {crop}^2 px"},
+            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -439,8 +612,23 @@ def main():
                     help="model state: ground-truth splats (converged proxy) or init_state")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    c = CONFIGS[args.config]
+    c = CONFIGS.get(args.config)
     rank = int(os.environ.get("RANK", "0"))
+    if args.config == 5:
+        if args.impl == "reference":
+            if rank == 0:
+                print(json.dumps(run_reference_render(args)), flush=True)
+            return
+        import torch
+
+        from paper_2409_07759_b200.parallel import init_from_env
+
+        dp = init_from_env("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        out = run_render_only(args, dp)
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        return
 
     if args.impl == "reference":
         if rank != 0:
