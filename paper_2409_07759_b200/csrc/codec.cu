@@ -8,8 +8,6 @@
 // One thread per record; every rounding follows numpy's (round-to-nearest-
 // even conversions, np.rint = rint, left-to-right quaternion norms), so the
 // bytes equal the reference's encode_records on the same float64 input.
-#include <cuda_fp16.h>
-
 #include "ss_common.cuh"
 
 namespace ss {
@@ -27,14 +25,49 @@ __device__ __forceinline__ float get_f32(const uint8_t* p) {
                          ((uint32_t)p[3] << 24));
 }
 
+// float64 -> binary16, round to nearest even, directly from the double (as
+// numpy's astype('<f2')).  Integer implementation: the hardware F2F.F16.F64
+// conversion did not reproduce numpy's bytes on sm_100a.
+__device__ __forceinline__ unsigned short f64_to_f16_rn(double d) {
+  const uint64_t x = (uint64_t)__double_as_longlong(d);
+  const unsigned short sign = (unsigned short)((x >> 48) & 0x8000u);
+  const int exp = (int)((x >> 52) & 0x7ff);
+  uint64_t mant = x & 0xFFFFFFFFFFFFFull;
+  if (exp == 0x7ff) return sign | 0x7c00u | (mant ? 0x200u : 0u);
+  const int e = exp - 1023 + 15;
+  if (e >= 31) return sign | 0x7c00u;
+  if (e <= 0) {
+    if (e < -10) return sign;
+    mant |= 1ull << 52;
+    const int shift = 43 - e;
+    uint64_t m = mant >> shift;
+    const uint64_t rem = mant & ((1ull << shift) - 1), half = 1ull << (shift - 1);
+    if (rem > half || (rem == half && (m & 1))) ++m;
+    return sign | (unsigned short)m;
+  }
+  uint32_t h = ((uint32_t)e << 10) | (uint32_t)(mant >> 42);
+  const uint64_t rem = mant & ((1ull << 42) - 1), half = 1ull << 41;
+  if (rem > half || (rem == half && (h & 1))) ++h;
+  return sign | (unsigned short)h;
+}
+
 __device__ __forceinline__ void put_f16(uint8_t* p, double v) {
-  const unsigned short h = __half_as_ushort(__double2half(v));
+  const unsigned short h = f64_to_f16_rn(v);
   p[0] = h & 0xff;
   p[1] = h >> 8;
 }
 
+// binary16 -> float64 (exact)
 __device__ __forceinline__ double get_f16(const uint8_t* p) {
-  return (double)__half2float(__ushort_as_half((unsigned short)(p[0] | (p[1] << 8))));
+  const unsigned h = (unsigned)(p[0] | (p[1] << 8));
+  const int e = (h >> 10) & 0x1f;
+  const double m = (double)(h & 0x3ff);
+  double v;
+  if (e == 0) v = ldexp(m, -24);
+  else if (e == 31) v = (h & 0x3ff) ? __longlong_as_double(0x7ff8000000000000ll)
+                                   : __longlong_as_double(0x7ff0000000000000ll);
+  else v = ldexp(1024.0 + m, e - 25);
+  return (h & 0x8000) ? -v : v;
 }
 
 // codec.py:183-186 left-to-right sum of squares
