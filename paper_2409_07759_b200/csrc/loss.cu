@@ -10,21 +10,37 @@
 //   pass 2: separable blur of the three partial maps, combine into
 //           dL/dx = (1-w) sign(x-y)/N - w (B(ds_dmu) + 2x B(ds_dmxx) + y B(ds_dmxy))/N.
 //   pass 3: one block reduces the per-block sums in a fixed order.
+//
+// The blurs are register-blocked: a thread produces 8 consecutive outputs of
+// a column (vertical pass) or 4 of a row (horizontal pass) from a sliding
+// window held in registers, so each shared-memory value is loaded once per
+// thread instead of once per tap; the 11 taps are compile-time immediates
+// (full-rate FFMA with an immediate operand).
 #include "ss_common.cuh"
 
 namespace ss {
 
-constexpr int kLT = 32;             // output tile edge
-constexpr int kHalo = 5;            // 11 taps
+constexpr int kLT = 32;               // output tile edge
+constexpr int kHalo = 5;              // 11 taps
 constexpr int kLR = kLT + 2 * kHalo;  // 42: loaded region edge
-constexpr int kLP = kLR + 1;        // padded row pitch
+constexpr int kLP = kLR + 1;          // padded row pitch
 constexpr int kLossThreads = 256;
+constexpr int kVR = 8;                // vertical pass: outputs per thread
+constexpr int kHC = 4;                // horizontal pass: outputs per thread
 
-__constant__ float c_win[11];
+// loss.py:20-26 normalized 11-tap Gaussian, sigma 1.5 (fp64, rounded to fp32)
+__device__ __forceinline__ constexpr float win(int t) {
+  return t == 0 || t == 10 ? 0.001028380123898387f
+       : t == 1 || t == 9  ? 0.0075987582094967365f
+       : t == 2 || t == 8  ? 0.036000773310661316f
+       : t == 3 || t == 7  ? 0.10936068743467331f
+       : t == 4 || t == 6  ? 0.21300554275512695f
+                           : 0.26601171493530273f;
+}
 
 __device__ __forceinline__ float gt_value(const uint8_t* gt_u8, const float* lut,
                                           const float* gt_f32, int64_t idx) {
-  return gt_u8 ? lut[gt_u8[idx]] : gt_f32[idx];
+  return gt_u8 ? __ldg(lut + gt_u8[idx]) : gt_f32[idx];
 }
 
 struct LossArgs {
@@ -36,6 +52,60 @@ struct LossArgs {
   float* maps;        // 3 quantities x 3 channels x H x W
   double* partials;   // 2 per block
 };
+
+// Vertical blur of NQ quantities: out[q][r][c] = sum_t w_t src_q(r + t, c) for
+// r in [0, 32), c in [0, 42), from a (42 x kLP) source; quantities are
+// derived from the loaded sources by `load` (e.g. x, y, x*x, x*y, y*y).
+template <int NQ, typename Load>
+__device__ __forceinline__ void vblur(float (*out)[kLT][kLP], Load load) {
+  for (int task = threadIdx.x; task < kLR * (kLT / kVR); task += kLossThreads) {
+    const int c = task % kLR, r0 = (task / kLR) * kVR;
+    float acc[NQ][kVR];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int i = 0; i < kVR; ++i) acc[q][i] = 0.f;
+#pragma unroll
+    for (int s = 0; s < kVR + 10; ++s) {
+      float v[NQ];
+      load(r0 + s, c, v);
+#pragma unroll
+      for (int i = 0; i < kVR; ++i) {
+        const int t = s - i;
+        if (t >= 0 && t <= 10) {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) acc[q][i] = fmaf(win(t), v[q], acc[q][i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int i = 0; i < kVR; ++i) out[q][r0 + i][c] = acc[q][i];
+  }
+}
+
+// Horizontal blur: res[q][i] = sum_t w_t v[q][r][c0 + i + t], i in [0, kHC)
+template <int NQ>
+__device__ __forceinline__ void hblur(const float (*v)[kLT][kLP], int r, int c0,
+                                      float res[NQ][kHC]) {
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int i = 0; i < kHC; ++i) res[q][i] = 0.f;
+#pragma unroll
+  for (int s = 0; s < kHC + 10; ++s) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const float x = v[q][r][c0 + s];
+#pragma unroll
+      for (int i = 0; i < kHC; ++i) {
+        const int t = s - i;
+        if (t >= 0 && t <= 10) res[q][i] = fmaf(win(t), x, res[q][i]);
+      }
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
   __shared__ float s_x[kLR][kLP];
@@ -61,61 +131,47 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
       s_y[r][q] = yv;
     }
     __syncthreads();
-    // vertical pass (axis 0, loss.py:31)
-    for (int idx = threadIdx.x; idx < kLT * kLR; idx += kLossThreads) {
-      const int r = idx / kLR, q = idx % kLR;
-      float mx = 0.f, my = 0.f, mxx = 0.f, mxy = 0.f, myy = 0.f;
-#pragma unroll
-      for (int t = 0; t < 11; ++t) {
-        const float w = c_win[t];
-        const float xv = s_x[r + t][q], yv = s_y[r + t][q];
-        mx += w * xv;
-        my += w * yv;
-        mxx += w * (xv * xv);
-        mxy += w * (xv * yv);
-        myy += w * (yv * yv);
-      }
-      s_v[0][r][q] = mx;
-      s_v[1][r][q] = my;
-      s_v[2][r][q] = mxx;
-      s_v[3][r][q] = mxy;
-      s_v[4][r][q] = myy;
-    }
+    // vertical pass (axis 0, loss.py:31) of x, y, xx, xy, yy
+    vblur<5>(s_v, [&](int r, int c, float* v) {
+      const float xv = s_x[r][c], yv = s_y[r][c];
+      v[0] = xv;
+      v[1] = yv;
+      v[2] = xv * xv;
+      v[3] = xv * yv;
+      v[4] = yv * yv;
+    });
     __syncthreads();
     // horizontal pass (axis 1, loss.py:32) + SSIM terms (loss.py:39-59)
-    for (int idx = threadIdx.x; idx < kLT * kLT; idx += kLossThreads) {
-      const int r = idx / kLT, c = idx % kLT;
-      const int gy = y0 + r, gx = x0 + c;
-      if (gy >= H || gx >= W) continue;
-      float mu_x = 0.f, mu_y = 0.f, mxx = 0.f, mxy = 0.f, myy = 0.f;
+    {
+      const int r = threadIdx.x / (kLT / kHC), c0 = (threadIdx.x % (kLT / kHC)) * kHC;
+      float m[5][kHC];
+      hblur<5>(s_v, r, c0, m);
+      const int gy = y0 + r;
 #pragma unroll
-      for (int t = 0; t < 11; ++t) {
-        const float w = c_win[t];
-        mu_x += w * s_v[0][r][c + t];
-        mu_y += w * s_v[1][r][c + t];
-        mxx += w * s_v[2][r][c + t];
-        mxy += w * s_v[3][r][c + t];
-        myy += w * s_v[4][r][c + t];
+      for (int i = 0; i < kHC; ++i) {
+        const int gx = x0 + c0 + i;
+        if (gy >= H || gx >= W) continue;
+        const float mu_x = m[0][i], mu_y = m[1][i], mxx = m[2][i], mxy = m[3][i], myy = m[4][i];
+        const float C1 = 1e-4f, C2 = 9e-4f;
+        const float sig_x = mxx - mu_x * mu_x;
+        const float sig_y = myy - mu_y * mu_y;
+        const float sig_xy = mxy - mu_x * mu_y;
+        const float a1 = 2.f * mu_x * mu_y + C1;
+        const float a2 = 2.f * sig_xy + C2;
+        const float b1 = mu_x * mu_x + mu_y * mu_y + C1;
+        const float b2 = sig_x + sig_y + C2;
+        const float denom = b1 * b2;
+        const float s = (a1 * a2) / denom;
+        const float ds_dmu = (2.f * mu_y * (a2 - a1) - 2.f * mu_x * s * (b2 - b1)) / denom;
+        const float ds_dmxx = -s / b2;
+        const float ds_dmxy = 2.f * a1 / denom;
+        const int64_t pix = (int64_t)gy * W + gx;
+        a.maps[(0 * 3 + ch) * plane + pix] = ds_dmu;
+        a.maps[(1 * 3 + ch) * plane + pix] = ds_dmxx;
+        a.maps[(2 * 3 + ch) * plane + pix] = ds_dmxy;
+        ss += (double)s;
+        l1 += (double)fabsf(s_x[r + kHalo][c0 + i + kHalo] - s_y[r + kHalo][c0 + i + kHalo]);
       }
-      const float C1 = 1e-4f, C2 = 9e-4f;
-      const float sig_x = mxx - mu_x * mu_x;
-      const float sig_y = myy - mu_y * mu_y;
-      const float sig_xy = mxy - mu_x * mu_y;
-      const float a1 = 2.f * mu_x * mu_y + C1;
-      const float a2 = 2.f * sig_xy + C2;
-      const float b1 = mu_x * mu_x + mu_y * mu_y + C1;
-      const float b2 = sig_x + sig_y + C2;
-      const float denom = b1 * b2;
-      const float s = (a1 * a2) / denom;
-      const float ds_dmu = (2.f * mu_y * (a2 - a1) - 2.f * mu_x * s * (b2 - b1)) / denom;
-      const float ds_dmxx = -s / b2;
-      const float ds_dmxy = 2.f * a1 / denom;
-      const int64_t pix = (int64_t)gy * W + gx;
-      a.maps[(0 * 3 + ch) * plane + pix] = ds_dmu;
-      a.maps[(1 * 3 + ch) * plane + pix] = ds_dmxx;
-      a.maps[(2 * 3 + ch) * plane + pix] = ds_dmxy;
-      ss += (double)s;
-      l1 += (double)fabsf(s_x[r + kHalo][c + kHalo] - s_y[r + kHalo][c + kHalo]);
     }
   }
   // block reduction of the two sums (fixed order -> deterministic)
@@ -160,37 +216,24 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, floa
       for (int k = 0; k < 3; ++k) s_m[k][r][q] = in ? a.maps[(k * 3 + ch) * plane + pix] : 0.f;
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < kLT * kLR; idx += kLossThreads) {
-      const int r = idx / kLR, q = idx % kLR;
-      float v0 = 0.f, v1 = 0.f, v2 = 0.f;
-#pragma unroll
-      for (int t = 0; t < 11; ++t) {
-        const float w = c_win[t];
-        v0 += w * s_m[0][r + t][q];
-        v1 += w * s_m[1][r + t][q];
-        v2 += w * s_m[2][r + t][q];
-      }
-      s_v[0][r][q] = v0;
-      s_v[1][r][q] = v1;
-      s_v[2][r][q] = v2;
-    }
+    vblur<3>(s_v, [&](int r, int c, float* v) {
+      v[0] = s_m[0][r][c];
+      v[1] = s_m[1][r][c];
+      v[2] = s_m[2][r][c];
+    });
     __syncthreads();
-    for (int idx = threadIdx.x; idx < kLT * kLT; idx += kLossThreads) {
-      const int r = idx / kLT, c = idx % kLT;
-      const int gy = y0 + r, gx = x0 + c;
-      if (gy >= H || gx >= W) continue;
-      float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+    const int r = threadIdx.x / (kLT / kHC), c0 = (threadIdx.x % (kLT / kHC)) * kHC;
+    float bl[3][kHC];
+    hblur<3>(s_v, r, c0, bl);
+    const int gy = y0 + r;
 #pragma unroll
-      for (int t = 0; t < 11; ++t) {
-        const float w = c_win[t];
-        b0 += w * s_v[0][r][c + t];
-        b1 += w * s_v[1][r][c + t];
-        b2 += w * s_v[2][r][c + t];
-      }
+    for (int i = 0; i < kHC; ++i) {
+      const int gx = x0 + c0 + i;
+      if (gy >= H || gx >= W) continue;
       const int64_t e = ((int64_t)gy * W + gx) * 3 + ch;
       const float x = a.pred[e];
       const float y = gt_value(a.gt_u8, a.lut, a.gt_f32, e);
-      const float grad = (b0 + 2.f * x * b1 + y * b2) * inv_n;
+      const float grad = (bl[0][i] + 2.f * x * bl[1][i] + y * bl[2][i]) * inv_n;
       const float d = x - y;
       const float sgn = (d > 0.f) ? 1.f : ((d < 0.f) ? -1.f : 0.f);
       dimg[e] = (1.f - w_ssim) * sgn * inv_n - w_ssim * grad;
@@ -227,25 +270,6 @@ __global__ void loss_reduce_kernel(const double* __restrict__ partials, int n_bl
   }
 }
 
-static bool g_win_ready = false;
-
-static int ensure_window() {
-  if (g_win_ready) return SS_OK;
-  // loss.py:20-26  normalized 11-tap Gaussian, sigma 1.5 (computed in fp64)
-  double w[11], sum = 0.0;
-  for (int i = 0; i < 11; ++i) {
-    double x = i - 5.0;
-    w[i] = exp(-(x * x) / (2.0 * 1.5 * 1.5));
-    sum += w[i];
-  }
-  float wf[11];
-  for (int i = 0; i < 11; ++i) wf[i] = (float)(w[i] / sum);
-  if (cudaMemcpyToSymbol(c_win, wf, sizeof(wf)) != cudaSuccess)
-    return set_error(SS_ERR_CUDA, "ss_loss: cannot upload blur window");
-  g_win_ready = true;
-  return SS_OK;
-}
-
 }  // namespace ss
 
 using namespace ss;
@@ -265,8 +289,6 @@ extern "C" int ss_loss_l1_ssim(const float* pred, const uint8_t* gt_u8, const fl
   if (gt_u8 && !lut) return set_error(SS_ERR_INVALID, "ss_loss: u8 ground truth needs a LUT");
   if (ws_bytes < ss_loss_workspace_bytes(width, height))
     return set_error(SS_ERR_WORKSPACE, "ss_loss: workspace too small");
-  int rc = ensure_window();
-  if (rc) return rc;
   dim3 grid((width + kLT - 1) / kLT, (height + kLT - 1) / kLT);
   const size_t plane = (size_t)width * height;
   LossArgs a{pred, gt_u8, lut, gt_f32, width, height, (float*)ws,

@@ -29,7 +29,7 @@
 // carries the scalar Q = dC . S (Q += w dC . c) and d alpha' = T dC.c - Q/(1-a').
 // With t = alpha G d alpha' (zero when clamped), g_alpha = sum t / alpha and
 // dm = -t/2, and the strip sums sum t, sum t k, sum t k^2 give every
-// footprint gradient; one transposed warp reduction and one 9-lane float
+// footprint gradient; one 12-shuffle transposed warp reduction and one 9-lane float
 // atomic per (warp, entry).
 #include "ss_common.cuh"
 
@@ -168,20 +168,36 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
 }
 
-// Transposed warp reduction of 16 slots: afterwards lane L holds the warp
-// total of slot 8 b4 + 4 b3 + 2 b2 + b1 (b_i = bit i of L); lanes L, L^1 agree.
-__device__ __forceinline__ float reduce16(float v[16], int lane) {
+// Transposed warp reduction of 9 values in 12 shuffles: each round halves
+// (unevenly) the slots a lane keeps -- 9 -> 5 (xor 16) -> 3 (xor 8) -> 2 (xor 4)
+// -> 1 (xor 2) -> +xor 1.  Afterwards lane L (bits b4..b0) holds the warp total
+// of value 5 b4 + 3 b3 + 2 b2 + b1 when red9_slot marks it valid (L and L^1 agree).
+__device__ __forceinline__ float red_round(float lo, float hi, bool up, int off) {
+  const float send = up ? lo : hi;
+  const float keep = up ? hi : lo;
+  return keep + __shfl_xor_sync(0xffffffffu, send, off);
+}
+
+__device__ __forceinline__ float reduce9(const float v[9], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+  float w[5];
 #pragma unroll
-  for (int half = 8, off = 16; half >= 1; half >>= 1, off >>= 1) {
-    const bool up = lane & off;
+  for (int i = 0; i < 5; ++i) w[i] = red_round(v[i], i + 5 < 9 ? v[i + 5] : 0.f, b4, 16);
+  float x[3];
 #pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const float send = up ? v[i] : v[i + half];
-      const float keep = up ? v[i + half] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-  }
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+  for (int i = 0; i < 3; ++i) x[i] = red_round(w[i], i + 3 < 5 ? w[i + 3] : 0.f, b3, 8);
+  float y[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) y[i] = red_round(x[i], i + 2 < 3 ? x[i + 2] : 0.f, b2, 4);
+  const float z = red_round(y[0], y[1], b1, 2);
+  return z + __shfl_xor_sync(0xffffffffu, z, 1);
+}
+
+__device__ __forceinline__ int red9_slot(int lane, bool& valid) {
+  const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
+  const int p = 3 * b3 + 2 * b2 + b1;
+  valid = !(lane & 1) && !(b2 && (b1 || b3)) && (b4 == 0 ? p < 5 : p < 4);
+  return 5 * b4 + p;
 }
 
 template <int STRIP>
@@ -227,8 +243,8 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
   const int2 rg = ranges[tile];
   const int walk_end = rg.x + __reduce_max_sync(0xffffffffu, my_max);
-  const int slot = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
-                   ((lane >> 1) & 1);
+  bool slot_ok;
+  const int slot = red9_slot(lane, slot_ok);
   for (int end = walk_end; end > rg.x; end -= 32) {
     const int start = max(rg.x, end - 32);
     __syncwarp();
@@ -271,7 +287,7 @@ __global__ void __launch_bounds__(kWarps * 32)
       const float sdm = -0.5f * st0;
       const float sdmy = -0.5f * fmaf(dy0, st0, st1);
       const float sdmyy = -0.5f * fmaf(dy0, fmaf(dy0, st0, 2.f * st1), st2);
-      float v[16];
+      float v[9];
       v[0] = -2.f * (i0 * dx * sdm + i1 * sdmy);
       v[1] = -2.f * (i1 * dx * sdm + i2 * sdmy);
       v[2] = dx * dx * sdm;
@@ -281,10 +297,8 @@ __global__ void __launch_bounds__(kWarps * 32)
       v[6] = sc0;
       v[7] = sc1;
       v[8] = sc2;
-#pragma unroll
-      for (int i = 9; i < 16; ++i) v[i] = 0.f;
-      const float tot = reduce16(v, lane);
-      if (!(lane & 1) && slot < 9) atomicAdd(g2d + (int64_t)st.g[j] * SS_G2D_ROW + slot, tot);
+      const float tot = reduce9(v, lane);
+      if (slot_ok) atomicAdd(g2d + (int64_t)st.g[j] * SS_G2D_ROW + slot, tot);
     }
   }
 }
