@@ -628,12 +628,14 @@ def relocate(params_list, m_list, v_list, threshold, uniforms):
 CULL_MARGIN = 64.0 * (1.0 + 1e-9)
 
 
-def tile_min_maha(i0, i1, i2, u, v, X0, X1, Y0, Y1):
+def tile_min_maha(i0, i1, i2, u, v, X0, X1, Y0, Y1, r0=None, r2=None):
     """Minimum over the continuous rectangle [X0, X1] x [Y0, Y1] (pixel-centre
     coordinates) of m = i0 dx^2 + 2 i1 dx dy + i2 dy^2, dx = x - u, dy = y - v.
     Vectorised restatement of project.cu tile_min_maha (same operation order).
     A tile whose minimum exceeds CULL_MARGIN holds no pixel the reference's
     loop would blend (maha > 64 skip, _kernels.py:39-41)."""
+    r0 = 1.0 / i0 if r0 is None else r0
+    r2 = 1.0 / i2 if r2 is None else r2
     ax, bx = X0 - u, X1 - u
     ay, by = Y0 - v, Y1 - v
     inside = (ax <= 0.0) & (bx >= 0.0) & (ay <= 0.0) & (by >= 0.0)
@@ -643,10 +645,10 @@ def tile_min_maha(i0, i1, i2, u, v, X0, X1, Y0, Y1):
 
     best = np.full(np.shape(u), np.inf)
     for ex in (ax, bx):          # vertical edges: dx fixed, minimise over dy
-        dy = np.clip(-(i1 * ex) / i2, ay, by)
+        dy = np.clip(-(i1 * ex) * r2, ay, by)
         best = np.minimum(best, q(ex, dy))
     for ey in (ay, by):          # horizontal edges: dy fixed, minimise over dx
-        dx = np.clip(-(i1 * ey) / i0, ax, bx)
+        dx = np.clip(-(i1 * ey) * r0, ax, bx)
         best = np.minimum(best, q(dx, ey))
     return np.where(inside, 0.0, best)
 

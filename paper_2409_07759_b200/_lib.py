@@ -52,12 +52,12 @@ _SIGNATURES = {
     "ss_device_sm_count": ([], c_int),
     "ss_compact_workspace_bytes": ([I64], c_size_t),
     "ss_compact_active": ([P, P, I64, I64, P, I32, I32, P, P, P, c_size_t, P], c_int),
-    "ss_project_fwd": ([POINTER(SSStore), P, I32, POINTER(SSCamera), P, P, P, P, P, P, P, P],
+    "ss_project_fwd": ([POINTER(SSStore), P, I32, POINTER(SSCamera), P, P, P, P, P, P, P, P, P],
                        c_int),
     "ss_binning_workspace_bytes": ([I32, I64, I32], c_size_t),
     "ss_depth_order": ([P, I32, P, P, c_size_t, P], c_int),
     "ss_tile_offsets": ([P, P, I32, P, P, c_size_t, P], c_int),
-    "ss_emit_tile_pairs": ([P, P, P, P, I32, I32, P, P, P], c_int),
+    "ss_emit_tile_pairs": ([P, P, P, P, P, I32, I32, P, P, P], c_int),
     "ss_sort_tile_pairs": ([P, P, P, P, I64, I32, POINTER(I32), P, c_size_t, P], c_int),
     "ss_tile_ranges": ([P, I64, I32, P, P], c_int),
     "ss_tile_order_workspace_bytes": ([I32], c_size_t),

@@ -33,7 +33,8 @@ __global__ void gather_counts_kernel(const int32_t* __restrict__ order,
 __global__ void emit_pairs_kernel(const int32_t* __restrict__ order,
                                   const int32_t* __restrict__ offsets,
                                   const int4* __restrict__ bbox, const double* __restrict__ geom,
-                                  int32_t n, int32_t tiles_x, uint32_t* __restrict__ keys,
+                                  const uint64_t* __restrict__ tile_mask, int32_t n,
+                                  int32_t tiles_x, uint32_t* __restrict__ keys,
                                   int32_t* __restrict__ vals) {
   const int lane = threadIdx.x & 31;
   int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -47,14 +48,18 @@ __global__ void emit_pairs_kernel(const int32_t* __restrict__ order,
   const int ty0 = bb.z / kTile, ty1 = (bb.w - 1) / kTile + 1;
   const int w = tx1 - tx0;
   const int total = w * (ty1 - ty0);
-  double gl[5];
+  const uint64_t mask = tile_mask[i];
+  double gl[kGeom];
+  if (total > 64) {
 #pragma unroll
-  for (int c = 0; c < 5; ++c) gl[c] = geom[(int64_t)i * 5 + c];
+    for (int c = 0; c < kGeom; ++c) gl[c] = geom[(int64_t)i * kGeom + c];
+  }
   int written = 0;
   for (int j0 = 0; j0 < total; j0 += 32) {
     const int j = j0 + lane;
     const int ty = ty0 + j / w, tx = tx0 + j % w;
-    const bool keep = j < total && tile_keeps(gl, tx, ty, bb);
+    const bool keep = j < total && (j < 64 ? ((mask >> j) & 1ull) != 0
+                                           : tile_keeps(gl, tx, ty, bb));
     const unsigned ball = __ballot_sync(0xffffffffu, keep);
     if (keep) {
       const int at = off + written + __popc(ball & ((1u << lane) - 1));
@@ -156,13 +161,13 @@ extern "C" int ss_tile_offsets(const int32_t* order, const int32_t* n_tiles, int
 }
 
 extern "C" int ss_emit_tile_pairs(const int32_t* order, const int32_t* offsets,
-                                  const int32_t* bbox, const double* geom, int32_t n,
-                                  int32_t tiles_x, uint32_t* keys, int32_t* vals,
-                                  cudaStream_t stream) {
+                                  const int32_t* bbox, const double* geom,
+                                  const uint64_t* tile_mask, int32_t n, int32_t tiles_x,
+                                  uint32_t* keys, int32_t* vals, cudaStream_t stream) {
   if (n < 0 || tiles_x <= 0) return set_error(SS_ERR_INVALID, "ss_emit_tile_pairs: bad sizes");
   if (n == 0) return SS_OK;
   emit_pairs_kernel<<<grid_for((int64_t)n * 32, 256), 256, 0, stream>>>(
-      order, offsets, (const int4*)bbox, geom, n, tiles_x, keys, vals);
+      order, offsets, (const int4*)bbox, geom, tile_mask, n, tiles_x, keys, vals);
   return check_launch("ss_emit_tile_pairs");
 }
 

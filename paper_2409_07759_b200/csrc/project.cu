@@ -108,7 +108,8 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
                                    CamK cam, float4* __restrict__ rec_a,
                                    float4* __restrict__ rec_b, float* __restrict__ rec_c,
                                    uint64_t* __restrict__ depth_key, int4* __restrict__ bbox,
-                                   int32_t* __restrict__ n_tiles, double* __restrict__ geom) {
+                                   int32_t* __restrict__ n_tiles, double* __restrict__ geom,
+                                   uint64_t* __restrict__ tile_mask) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int32_t row = rows ? rows[i] : i;
@@ -137,22 +138,28 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
   const int y0 = (int)fmax(ceil(dsub(p.uy, r8)), 0.0);
   const int y1 = (int)fmin(dadd(floor(dadd(p.uy, r8)), 1.0), (double)cam.height);
   bbox[i] = make_int4(x0, x1, y0, y1);
-  double* gm = geom + (int64_t)i * 5;
-  gm[0] = p.ux;
-  gm[1] = p.uy;
-  gm[2] = i0;
-  gm[3] = i1;
-  gm[4] = i2;
+  double gl[kGeom] = {p.ux, p.uy, i0, i1, i2, ddiv(1.0, i0), ddiv(1.0, i2)};
+  double* gm = geom + (int64_t)i * kGeom;
+#pragma unroll
+  for (int c = 0; c < kGeom; ++c) gm[c] = gl[c];
   int nt = 0;
+  uint64_t mask = 0;
   if (x1 > x0 && y1 > y0) {
-    // tiles of the 8-sigma bbox that the maha <= 64 ellipse actually reaches
+    // tiles of the 8-sigma bbox that the maha <= 64 ellipse actually reaches;
+    // the first 64 (row-major in the bbox tile rectangle) are also recorded as
+    // a bit mask so the emit pass does not repeat the test
     const int4 bb = make_int4(x0, x1, y0, y1);
-    const double gl[5] = {p.ux, p.uy, i0, i1, i2};
     const int tx0 = x0 / kTile, tx1 = (x1 - 1) / kTile + 1;
     const int ty0 = y0 / kTile, ty1 = (y1 - 1) / kTile + 1;
+    int j = 0;
     for (int ty = ty0; ty < ty1; ++ty)
-      for (int tx = tx0; tx < tx1; ++tx) nt += tile_keeps(gl, tx, ty, bb);
+      for (int tx = tx0; tx < tx1; ++tx, ++j) {
+        const bool keep = tile_keeps(gl, tx, ty, bb);
+        nt += keep;
+        if (keep && j < 64) mask |= 1ull << j;
+      }
   }
+  tile_mask[i] = mask;
   n_tiles[i] = nt;
   depth_key[i] = (uint64_t)__double_as_longlong(p.z);  // z > 0.01: bits are monotone
   // rasterizer record (raster.cu): conic pre-scaled by kappa = -log2(e)/2 so
@@ -296,7 +303,7 @@ using namespace ss;
 extern "C" int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_t n,
                               const ss_camera* cam, void* rec_a, void* rec_b, float* rec_c,
                               uint64_t* depth_key, int32_t* bbox, int32_t* n_tiles,
-                              double* geom, cudaStream_t stream) {
+                              double* geom, uint64_t* tile_mask, cudaStream_t stream) {
   if (!store || !cam || n < 0) return set_error(SS_ERR_INVALID, "ss_project_fwd: bad arguments");
   if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0) || !(cam->fy > 0))
     return set_error(SS_ERR_INVALID, "ss_project_fwd: bad camera");
@@ -304,7 +311,7 @@ extern "C" int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_
   StoreView sv{store->opt, store->n_opt, store->mat};
   project_fwd_kernel<<<grid_for(n, 128), 128, 0, stream>>>(
       sv, rows, n, to_camk(cam), (float4*)rec_a, (float4*)rec_b, rec_c, depth_key, (int4*)bbox,
-      n_tiles, geom);
+      n_tiles, geom, tile_mask);
   return check_launch("ss_project_fwd");
 }
 

@@ -98,20 +98,23 @@ __device__ __forceinline__ double clampd(double x, double lo, double hi) {
   return fmin(fmax(x, lo), hi);
 }
 
+// geom = (u, v, i0, i1, i2, 1/i0, 1/i2) in fp64; bb = pixel bbox (x0, x1, y0, y1)
 __device__ __forceinline__ bool tile_keeps(const double* geom, int tx, int ty, int4 bb) {
-  // geom = (u, v, i0, i1, i2) in fp64; bb = pixel bbox (x0, x1, y0, y1) half open
   const double u = geom[0], v = geom[1], i0 = geom[2], i1 = geom[3], i2 = geom[4];
+  const double r0 = geom[5], r2 = geom[6];
   const double ax = (double)max(tx * SS_TILE, bb.x) - u;
   const double bx = (double)min(tx * SS_TILE + SS_TILE - 1, bb.y - 1) - u;
   const double ay = (double)max(ty * SS_TILE, bb.z) - v;
   const double by = (double)min(ty * SS_TILE + SS_TILE - 1, bb.w - 1) - v;
   if (ax <= 0.0 && bx >= 0.0 && ay <= 0.0 && by >= 0.0) return true;
-  double best = quad_form(i0, i1, i2, ax, clampd(ddiv(-dmul(i1, ax), i2), ay, by));
-  best = fmin(best, quad_form(i0, i1, i2, bx, clampd(ddiv(-dmul(i1, bx), i2), ay, by)));
-  best = fmin(best, quad_form(i0, i1, i2, clampd(ddiv(-dmul(i1, ay), i0), ax, bx), ay));
-  best = fmin(best, quad_form(i0, i1, i2, clampd(ddiv(-dmul(i1, by), i0), ax, bx), by));
+  double best = quad_form(i0, i1, i2, ax, clampd(dmul(-dmul(i1, ax), r2), ay, by));
+  best = fmin(best, quad_form(i0, i1, i2, bx, clampd(dmul(-dmul(i1, bx), r2), ay, by)));
+  best = fmin(best, quad_form(i0, i1, i2, clampd(dmul(-dmul(i1, ay), r0), ax, bx), ay));
+  best = fmin(best, quad_form(i0, i1, i2, clampd(dmul(-dmul(i1, by), r0), ax, bx), by));
   return best <= kCullMargin;
 }
+
+constexpr int kGeom = 7;  // doubles per splat in the binning geometry record
 
 // Philox4x32-10 counter-based generator (Salmon et al., SC'11).
 struct Philox4 {

@@ -121,7 +121,8 @@ class ViewPipeline:
         dkey = self._buf("depth_key", (nn,), torch.int64)
         bbox = self._buf("bbox", (nn, 4), torch.int32)
         ntl = self._buf("n_tiles", (nn,), torch.int32)
-        geom = self._buf("geom", (nn, 5), torch.float64)
+        geom = self._buf("geom", (nn, 7), torch.float64)
+        tmask = self._buf("tile_mask", (nn,), torch.int64)
         order = self._buf("order", (nn,), torch.int32)
         offsets = self._buf("offsets", (nn + 1,), torch.int32)
         ranges = self._buf("ranges", (n_tiles, 2), torch.int32)
@@ -140,7 +141,7 @@ class ViewPipeline:
         rp = L.ptr(rows)
         L.check(lib.ss_project_fwd(ctypes.byref(self.store_struct), rp, n, ctypes.byref(self.cam_struct),
                                    L.ptr(rec_a), L.ptr(rec_b), L.ptr(rec_c), L.ptr(dkey), L.ptr(bbox),
-                                   L.ptr(ntl), L.ptr(geom), sp), "project_fwd")
+                                   L.ptr(ntl), L.ptr(geom), L.ptr(tmask), sp), "project_fwd")
         L.check(lib.ss_depth_order(L.ptr(dkey), n, L.ptr(order), L.ptr(ws), ws.numel(), sp),
                 "depth_order")
         L.check(lib.ss_tile_offsets(L.ptr(order), L.ptr(ntl), n, L.ptr(offsets), L.ptr(ws),
@@ -154,8 +155,9 @@ class ViewPipeline:
         vals_alt = self._buf("vals_alt", (pc,), torch.int32)
         ws_bytes = int(lib.ss_binning_workspace_bytes(nn, pc, n_tiles))
         ws = self._buf("ws_bin", (ws_bytes,), torch.uint8)
-        L.check(lib.ss_emit_tile_pairs(L.ptr(order), L.ptr(offsets), L.ptr(bbox), L.ptr(geom), n,
-                                       tiles_x, L.ptr(keys), L.ptr(vals), sp), "emit_tile_pairs")
+        L.check(lib.ss_emit_tile_pairs(L.ptr(order), L.ptr(offsets), L.ptr(bbox), L.ptr(geom),
+                                       L.ptr(tmask), n, tiles_x, L.ptr(keys), L.ptr(vals), sp),
+                "emit_tile_pairs")
         sel = ctypes.c_int32(0)
         L.check(lib.ss_sort_tile_pairs(L.ptr(keys), L.ptr(vals), L.ptr(keys_alt), L.ptr(vals_alt),
                                        n_pairs, n_tiles, ctypes.byref(sel), L.ptr(ws), ws.numel(),

@@ -38,7 +38,8 @@ def test_error_reporting_without_gpu():
     """Argument validation happens before any device work."""
     from paper_2409_07759_b200 import _lib
     lib = _lib.lib()
-    rc = lib.ss_project_fwd(None, None, -1, None, None, None, None, None, None, None, None, None)
+    rc = lib.ss_project_fwd(None, None, -1, None, None, None, None, None, None, None, None, None,
+                            None)
     assert rc == _lib.SS_ERR_INVALID
     assert b"bad arguments" in lib.ss_last_error()
     assert lib.ss_version() >= 1
