@@ -94,6 +94,14 @@ __device__ __forceinline__ StripQuad strip_quad(const float4& a, const float4& b
   return s;
 }
 
+// kappa m + log2 alpha at strip pixel k: q0 + k lin + k^2 quad (k = 0, 1
+// special-cased: no multiply-by-immediate-zero FMAs)
+__device__ __forceinline__ float strip_exp(const StripQuad& s, int k) {
+  if (k == 0) return s.q0;
+  if (k == 1) return (s.q0 + s.lin) + s.quad;
+  return fmaf((float)(k * k), s.quad, fmaf((float)k, s.lin, s.q0));
+}
+
 template <int STRIP>
 __global__ void __launch_bounds__(kWarps * 32)
     raster_fwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
@@ -132,7 +140,6 @@ __global__ void __launch_bounds__(kWarps * 32)
     __syncwarp();
     stage_load(st, lane, base + lane, rg.y, vals, rec_a, rec_b, rec_c);
     __syncwarp();
-    if (!live) continue;
     const int cnt = min(32, rg.y - base);
     for (int j = 0; j < cnt; ++j) {
       const float4 a = st.a[j];
@@ -140,17 +147,29 @@ __global__ void __launch_bounds__(kWarps * 32)
       const float cb = st.c[j];
       const StripQuad s = strip_quad(a, b, fx, fy0);
       const int pos = base - rg.x + j + 1;
+      // exponents and validity of the whole strip first: a warp skips the
+      // entry when none of its pixels is live and inside the maha <= 64 ellipse
+      float e[STRIP];
+      bool valid[STRIP];
+      bool any = false;
 #pragma unroll
       for (int k = 0; k < STRIP; ++k) {
-        const float e = fmaf((float)(k * k), s.quad, fmaf((float)k, s.lin, s.q0));
-        const bool valid = (T[k] >= kTMin) && (e >= s.thr);
-        const float ap = valid ? fminf(ex2(e), kAlphaMax) : 0.f;
+        e[k] = strip_exp(s, k);
+        valid[k] = (T[k] >= kTMin) && (e[k] >= s.thr);
+        any |= valid[k];
+      }
+      if (!__any_sync(0xffffffffu, any)) continue;
+      // branch-free over the strip: invalid pixels get alpha' = 0, which
+      // leaves C and T untouched, so the chains interleave freely
+#pragma unroll
+      for (int k = 0; k < STRIP; ++k) {
+        const float ap = valid[k] ? fminf(ex2(e[k]), kAlphaMax) : 0.f;
         const float w = ap * T[k];
         c0[k] = fmaf(b.z, w, c0[k]);
         c1[k] = fmaf(b.w, w, c1[k]);
         c2[k] = fmaf(cb, w, c2[k]);
         T[k] = fmaf(-ap, T[k], T[k]);
-        last[k] = valid ? pos : last[k];
+        last[k] = valid[k] ? pos : last[k];
       }
     }
   }
@@ -256,31 +275,48 @@ __global__ void __launch_bounds__(kWarps * 32)
       const float4 b = st.b[j];
       const float cb = st.c[j];
       const StripQuad s = strip_quad(a, b, fx, fy0);
-      float sc0 = 0.f, sc1 = 0.f, sc2 = 0.f, st0 = 0.f, st1 = 0.f, st2 = 0.f;
-      bool touched = false;
+      float e[STRIP];
+      bool valid[STRIP];
+      bool any = false;
 #pragma unroll
       for (int k = 0; k < STRIP; ++k) {
-        const float e = fmaf((float)(k * k), s.quad, fmaf((float)k, s.lin, s.q0));
-        const bool valid = (pos < last[k]) && (e >= s.thr);
-        touched |= valid;
-        const float aG = ex2(e);
-        const float ap = valid ? fminf(aG, kAlphaMax) : 0.f;
+        e[k] = strip_exp(s, k);
+        valid[k] = (pos < last[k]) && (e[k] >= s.thr);
+        any |= valid[k];
+      }
+      if (!__any_sync(0xffffffffu, any)) continue;
+      float sc0, sc1, sc2, st0, st1, st2;
+#pragma unroll
+      for (int k = 0; k < STRIP; ++k) {
+        // branch-free: an invalid pixel has alpha' = 0 (T and Q unchanged) and
+        // a zero gradient weight g
+        const float aG = ex2(e[k]);
+        const float ap = valid[k] ? fminf(aG, kAlphaMax) : 0.f;
+        // clamped splats pass no alpha/footprint gradient (_kernels.py:120-121)
+        const float g = (valid[k] && aG <= kAlphaMax) ? aG : 0.f;
         const float inv = rcp(1.f - ap);
         T[k] *= inv;  // T before this splat
         const float w = ap * T[k];
-        sc0 = fmaf(d0[k], w, sc0);
-        sc1 = fmaf(d1[k], w, sc1);
-        sc2 = fmaf(d2[k], w, sc2);
         const float dc = fmaf(d2[k], cb, fmaf(d1[k], b.w, d0[k] * b.z));
         const float dap = fmaf(T[k], dc, -Q[k] * inv);
         Q[k] = fmaf(w, dc, Q[k]);
-        // clamped splats pass no alpha/footprint gradient (_kernels.py:120-121)
-        const float t = (valid && aG <= kAlphaMax) ? aG * dap : 0.f;
-        st0 += t;
-        st1 = fmaf((float)k, t, st1);
-        st2 = fmaf((float)(k * k), t, st2);
+        const float t = g * dap;
+        if (k == 0) {
+          sc0 = d0[k] * w;
+          sc1 = d1[k] * w;
+          sc2 = d2[k] * w;
+          st0 = t;
+          st1 = 0.f;
+          st2 = 0.f;
+        } else {
+          sc0 = fmaf(d0[k], w, sc0);
+          sc1 = fmaf(d1[k], w, sc1);
+          sc2 = fmaf(d2[k], w, sc2);
+          st0 += t;
+          st1 = k == 1 ? st1 + t : fmaf((float)k, t, st1);
+          st2 = k == 1 ? st2 + t : fmaf((float)(k * k), t, st2);
+        }
       }
-      if (!__any_sync(0xffffffffu, touched)) continue;
       // strip sums -> 9 gradient components; dm = -t/2, G d alpha' = t / alpha
       const float i0 = a.z * kInvKappa, i1 = a.w * kInvKappa, i2 = b.x * kInvKappa;
       const float dx = s.dx, dy0 = s.dy0;
