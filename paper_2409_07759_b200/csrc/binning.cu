@@ -27,19 +27,18 @@ __global__ void gather_counts_kernel(const int32_t* __restrict__ order,
   if (k == n) out[k] = 0;
 }
 
-// One warp per splat in rank order; lanes stride over the splat's bbox tiles,
-// keep those the ellipse reaches (tile_keeps, same test as the count in
-// project.cu) and compact them with a ballot prefix.
+// One thread per splat in rank order: walk the kept-tile bits of its bbox
+// tile rectangle (tile_mask for the first 64 tiles, the fp64 test beyond) and
+// write its run [offsets[k], offsets[k+1]) of (tile id, splat) pairs.
 __global__ void emit_pairs_kernel(const int32_t* __restrict__ order,
                                   const int32_t* __restrict__ offsets,
                                   const int4* __restrict__ bbox, const double* __restrict__ geom,
                                   const uint64_t* __restrict__ tile_mask, int32_t n,
                                   int32_t tiles_x, uint32_t* __restrict__ keys,
                                   int32_t* __restrict__ vals) {
-  const int lane = threadIdx.x & 31;
-  int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const int32_t off = offsets[k];
+  int32_t off = offsets[k];
   const int32_t cnt = offsets[k + 1] - off;
   if (cnt == 0) return;
   const int32_t i = order[k];
@@ -48,25 +47,26 @@ __global__ void emit_pairs_kernel(const int32_t* __restrict__ order,
   const int ty0 = bb.z / kTile, ty1 = (bb.w - 1) / kTile + 1;
   const int w = tx1 - tx0;
   const int total = w * (ty1 - ty0);
-  const uint64_t mask = tile_mask[i];
-  double gl[kGeom];
+  uint64_t mask = tile_mask[i];
+  while (mask) {
+    const int j = __ffsll((long long)mask) - 1;
+    mask &= mask - 1;
+    keys[off] = (uint32_t)((ty0 + j / w) * tiles_x + tx0 + j % w);
+    vals[off] = i;
+    ++off;
+  }
   if (total > 64) {
+    double gl[kGeom];
 #pragma unroll
     for (int c = 0; c < kGeom; ++c) gl[c] = geom[(int64_t)i * kGeom + c];
-  }
-  int written = 0;
-  for (int j0 = 0; j0 < total; j0 += 32) {
-    const int j = j0 + lane;
-    const int ty = ty0 + j / w, tx = tx0 + j % w;
-    const bool keep = j < total && (j < 64 ? ((mask >> j) & 1ull) != 0
-                                           : tile_keeps(gl, tx, ty, bb));
-    const unsigned ball = __ballot_sync(0xffffffffu, keep);
-    if (keep) {
-      const int at = off + written + __popc(ball & ((1u << lane) - 1));
-      keys[at] = (uint32_t)(ty * tiles_x + tx);
-      vals[at] = i;
+    for (int j = 64; j < total; ++j) {
+      const int ty = ty0 + j / w, tx = tx0 + j % w;
+      if (tile_keeps(gl, tx, ty, bb)) {
+        keys[off] = (uint32_t)(ty * tiles_x + tx);
+        vals[off] = i;
+        ++off;
+      }
     }
-    written += __popc(ball);
   }
 }
 
@@ -166,7 +166,7 @@ extern "C" int ss_emit_tile_pairs(const int32_t* order, const int32_t* offsets,
                                   uint32_t* keys, int32_t* vals, cudaStream_t stream) {
   if (n < 0 || tiles_x <= 0) return set_error(SS_ERR_INVALID, "ss_emit_tile_pairs: bad sizes");
   if (n == 0) return SS_OK;
-  emit_pairs_kernel<<<grid_for((int64_t)n * 32, 256), 256, 0, stream>>>(
+  emit_pairs_kernel<<<grid_for(n, 128), 128, 0, stream>>>(
       order, offsets, (const int4*)bbox, geom, tile_mask, n, tiles_x, keys, vals);
   return check_launch("ss_emit_tile_pairs");
 }
@@ -202,6 +202,44 @@ extern "C" int ss_tile_ranges(const uint32_t* sorted_keys, int64_t n_pairs, int3
   return check_launch("ss_tile_ranges");
 }
 
+// Longest-first tile order in one CTA: bitonic sort of (maxlen - len) << 13 | tile
+// over up to 8192 tiles in shared memory (ties by tile id).
+constexpr int kOrderMax = 8192;
+
+__global__ void __launch_bounds__(1024) tile_order_bitonic_kernel(const int2* __restrict__ ranges,
+                                                                  int n_tiles,
+                                                                  int32_t* __restrict__ out) {
+  __shared__ uint32_t key[kOrderMax];
+  int n2 = 1;
+  while (n2 < n_tiles) n2 <<= 1;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    if (i < n_tiles) {
+      const int2 r = ranges[i];
+      const uint32_t len = (uint32_t)min(r.y - r.x, (1 << 18) - 1);
+      key[i] = (((1u << 18) - 1 - len) << 13) | (uint32_t)i;
+    } else {
+      key[i] = 0xffffffffu;
+    }
+  }
+  __syncthreads();
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const uint32_t a = key[lo], b = key[hi];
+        if ((a > b) == asc) {
+          key[lo] = b;
+          key[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) out[i] = (int32_t)(key[i] & 0x1fffu);
+}
+
 static size_t tile_order_cub_bytes(int32_t n_tiles) {
   size_t b = 0;
   cub::DeviceRadixSort::SortPairsDescending(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr,
@@ -218,6 +256,10 @@ extern "C" size_t ss_tile_order_workspace_bytes(int32_t n_tiles) {
 extern "C" int ss_tile_order(const int32_t* ranges, int32_t n_tiles, int32_t* tile_order,
                              void* ws, size_t ws_bytes, cudaStream_t stream) {
   if (n_tiles <= 0) return set_error(SS_ERR_INVALID, "ss_tile_order: n_tiles <= 0");
+  if (n_tiles <= kOrderMax) {
+    tile_order_bitonic_kernel<<<1, 1024, 0, stream>>>((const int2*)ranges, n_tiles, tile_order);
+    return check_launch("ss_tile_order");
+  }
   if (ws_bytes < ss_tile_order_workspace_bytes(n_tiles))
     return set_error(SS_ERR_WORKSPACE, "ss_tile_order: workspace too small");
   char* w = (char*)ws;

@@ -81,10 +81,15 @@ __global__ void adam_sgld_kernel(double* __restrict__ opt, const float* __restri
   double* p = opt + r * SS_ROW;
   const float* gf = grads + r * SS_GRAD_ROW;
   double g[SS_ROW], pv[SS_ROW];
+  // rows are 112 B (params, moments) / 56 B (gradients): 16 B / 8 B vector loads
 #pragma unroll
-  for (int k = 0; k < SS_ROW; ++k) {
-    pv[k] = p[k];
-    g[k] = (double)gf[k];
+  for (int k = 0; k < SS_ROW / 2; ++k) {
+    const double2 d = reinterpret_cast<const double2*>(p)[k];
+    pv[2 * k] = d.x;
+    pv[2 * k + 1] = d.y;
+    const float2 f = reinterpret_cast<const float2*>(gf)[k];
+    g[2 * k] = (double)f.x;
+    g[2 * k + 1] = (double)f.y;
   }
   // loss.py:110-111 regularizer gradients (train.py:397-398)
   const double alpha = sigmoid(pv[10]);
@@ -100,17 +105,22 @@ __global__ void adam_sgld_kernel(double* __restrict__ opt, const float* __restri
 #pragma unroll
     for (int k = 0; k < SS_ROW; ++k) pv[k] = dsub(pv[k], dmul(h.lr[group[k]], g[k]));
   } else {
-    double* mr = m + r * SS_ROW;
-    double* vr = v + r * SS_ROW;
+    double2* mr = reinterpret_cast<double2*>(m + r * SS_ROW);
+    double2* vr = reinterpret_cast<double2*>(v + r * SS_ROW);
 #pragma unroll
-    for (int k = 0; k < SS_ROW; ++k) {
-      double mk = mr[k], vk = vr[k];
-      mk = __dadd_rn(__dmul_rn(mk, h.b1), __dmul_rn(1.0 - h.b1, g[k]));
-      vk = __dadd_rn(__dmul_rn(vk, h.b2), __dmul_rn(__dmul_rn(1.0 - h.b2, g[k]), g[k]));
-      mr[k] = mk;
-      vr[k] = vk;
-      const double step = ddiv(ddiv(mk, gs.bc1), dadd(sqrt(ddiv(vk, gs.bc2)), h.eps));
-      pv[k] = dsub(pv[k], dmul(h.lr[group[k]], step));
+    for (int k2 = 0; k2 < SS_ROW / 2; ++k2) {
+      double2 mm = mr[k2], vv = vr[k2];
+      double mk[2] = {mm.x, mm.y}, vk[2] = {vv.x, vv.y};
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int k = 2 * k2 + h2;
+        mk[h2] = __dadd_rn(__dmul_rn(mk[h2], h.b1), __dmul_rn(1.0 - h.b1, g[k]));
+        vk[h2] = __dadd_rn(__dmul_rn(vk[h2], h.b2), __dmul_rn(__dmul_rn(1.0 - h.b2, g[k]), g[k]));
+        const double step = ddiv(ddiv(mk[h2], gs.bc1), dadd(sqrt(ddiv(vk[h2], gs.bc2)), h.eps));
+        pv[k] = dsub(pv[k], dmul(h.lr[group[k]], step));
+      }
+      mr[k2] = make_double2(mk[0], mk[1]);
+      vr[k2] = make_double2(vk[0], vk[1]);
     }
   }
   // train.py:341-344 projections
@@ -136,7 +146,8 @@ __global__ void adam_sgld_kernel(double* __restrict__ opt, const float* __restri
     sgld_row(pv, h, e);
   }
 #pragma unroll
-  for (int k = 0; k < SS_ROW; ++k) p[k] = pv[k];
+  for (int k = 0; k < SS_ROW / 2; ++k)
+    reinterpret_cast<double2*>(p)[k] = make_double2(pv[2 * k], pv[2 * k + 1]);
 }
 
 __global__ void sgld_kernel(double* __restrict__ opt, int64_t n_rows, int32_t rows_per_gen,
