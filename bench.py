@@ -55,6 +55,19 @@ METRIC5 = "render-only streaming playback frames/sec (1920x1080)"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 
 
+def load_traffic(kernels):
+    """Per-launch DRAM bytes (read + write) of the given kernels from the latest
+    committed ncu --set full capture (profiles/*_traffic.json), or None."""
+    files = sorted((ROOT / "profiles").glob("r*_traffic.json"))
+    if not files:
+        return None
+    d = json.loads(files[-1].read_text())
+    try:
+        return sum(d[k]["dram_bytes_read"] + d[k]["dram_bytes_write"] for k in kernels)
+    except KeyError:
+        return None
+
+
 def load_peaks():
     if PEAKS.exists():
         d = json.loads(PEAKS.read_text())
@@ -696,7 +709,10 @@ def main():
     peak, peak_kind = load_peaks()
     achieved = b_raster / t_raster / 1e9 if t_raster > 0 else 0.0
     out["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                       "frac": achieved / peak, "traffic": None,
+                       "frac": achieved / peak,
+                       "traffic": load_traffic(["raster_fwd", "raster_bwd"]),
+                       "traffic_source": "ncu --set full dram__bytes_read+write per launch "
+                                         "(profiles/r*_traffic.json, config 3)",
                        "kernel": "raster_fwd + raster_bwd", "peak_source": peak_kind,
                        "bytes_per_view": b_raster, "K_used": k_used, "K": k_pairs,
                        "active_splats": n_act, "pixels": P,
