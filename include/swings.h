@@ -217,6 +217,57 @@ int ss_encode_records(const double* rows, int64_t n, int32_t profile, uint8_t* o
 int ss_decode_records(const uint8_t* data, int64_t n, int32_t profile, double* rows,
                       ss_stream_t stream);
 
+/* ---- native per-view driver (csrc/view.cu).  All pointers device memory,
+ * caller-owned; capacities: per-splat buffers >= n, pairs >= pair_cap,
+ * ranges / tile_order >= tiles, per-pixel >= W*H, ws >= ws_needed. */
+typedef struct {
+  const int32_t* rows;  /* active row ids (NULL = 0..n-1)                */
+  int32_t n;            /* active splats                                 */
+  int32_t pad0;
+  void* rec_a;          /* float4 x n                                    */
+  void* rec_b;          /* float4 x n                                    */
+  float* rec_c;
+  uint64_t* depth_key;
+  int32_t* bbox;        /* int4 x n                                      */
+  int32_t* n_tiles;
+  double* geom;         /* 7 x n                                         */
+  uint64_t* tile_mask;
+  int32_t* order;
+  int32_t* offsets;     /* n + 1                                         */
+  uint32_t* keys;
+  int32_t* vals;
+  uint32_t* keys_alt;
+  int32_t* vals_alt;
+  int64_t pair_cap;
+  int32_t* ranges;      /* int2 x tiles                                  */
+  int32_t* tile_order;
+  float* img;           /* H x W x 3                                     */
+  float* t_final;
+  int32_t* n_contrib;
+  void* ws;
+  size_t ws_bytes;
+  size_t ws_needed;     /* out: workspace the call needed (on SS_ERR_WORKSPACE) */
+  int64_t n_pairs;      /* out: K                                        */
+  int32_t sorted_sel;   /* out: 1 when the sorted pairs are in *_alt      */
+  int32_t pad1;
+  void* events[4];      /* optional cudaEvent_t: raster fwd start/end, bwd start/end */
+} ss_view;
+
+/* Projection -> depth order -> tile offsets -> [one stream sync for K] ->
+ * emit -> pair sort -> ranges -> tile order -> raster forward.  Returns
+ * SS_ERR_CAPACITY (K in v->n_pairs) when K > pair_cap, SS_ERR_WORKSPACE
+ * (size in v->ws_needed) when ws is too small; call again after growing. */
+int ss_render_fwd(const ss_store* store, const ss_camera* cam, ss_view* v, ss_stream_t stream);
+/* Raster backward -> projection backward for the view ss_render_fwd left in v;
+ * g2d (n x 12 floats) is zeroed here; grads are accumulated (caller zeroes). */
+int ss_render_bwd(const ss_store* store, const ss_camera* cam, const ss_view* v,
+                  const float* dimg, float* g2d, const uint8_t* trainable_mask,
+                  int64_t trainable_rows, float* grads, ss_stream_t stream);
+/* CUDA event helpers for the optional raster timing in ss_view. */
+int ss_event_create(void** ev);
+int ss_event_destroy(void* ev);
+int ss_event_elapsed_ms(void* start, void* end, float* ms);
+
 /* Direct-space snapshot of optimizable rows (train.py:155-161 + 474):
  * dst[i] = (mean, quat, exp(log_scale), sigmoid(logit), color) of src[i]. */
 int ss_to_direct(const double* src, double* dst, int64_t n, ss_stream_t stream);

@@ -46,6 +46,16 @@ P = c_void_p
 I32 = c_int32
 I64 = c_int64
 
+
+class SSView(Structure):
+    _fields_ = [("rows", P), ("n", c_int32), ("pad0", c_int32), ("rec_a", P), ("rec_b", P),
+                ("rec_c", P), ("depth_key", P), ("bbox", P), ("n_tiles", P), ("geom", P),
+                ("tile_mask", P), ("order", P), ("offsets", P), ("keys", P), ("vals", P),
+                ("keys_alt", P), ("vals_alt", P), ("pair_cap", c_int64), ("ranges", P),
+                ("tile_order", P), ("img", P), ("t_final", P), ("n_contrib", P), ("ws", P),
+                ("ws_bytes", c_size_t), ("ws_needed", c_size_t), ("n_pairs", c_int64),
+                ("sorted_sel", c_int32), ("pad1", c_int32), ("events", P * 4)]
+
 _SIGNATURES = {
     "ss_last_error": ([], ctypes.c_char_p),
     "ss_version": ([], c_int),
@@ -74,6 +84,12 @@ _SIGNATURES = {
     "ss_relocate": ([P, P, P, I64, I32, P, c_double, P, c_uint64, c_uint64, P, P, c_size_t, P],
                     c_int),
     "ss_to_direct": ([P, P, I64, P], c_int),
+    "ss_render_fwd": ([POINTER(SSStore), POINTER(SSCamera), POINTER(SSView), P], c_int),
+    "ss_render_bwd": ([POINTER(SSStore), POINTER(SSCamera), POINTER(SSView), P, P, P, I64, P, P],
+                      c_int),
+    "ss_event_create": ([POINTER(P)], c_int),
+    "ss_event_destroy": ([P], c_int),
+    "ss_event_elapsed_ms": ([P, P, POINTER(ctypes.c_float)], c_int),
     "ss_encode_records": ([P, I64, I32, P, P, P], c_int),
     "ss_decode_records": ([P, I64, I32, P, P], c_int),
 }

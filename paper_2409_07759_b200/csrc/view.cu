@@ -1,0 +1,106 @@
+// Native per-view driver: the whole forward (projection -> binning -> raster
+// forward) and backward (raster backward -> projection backward) of one view
+// as single C-ABI calls, so the host issues two calls per view instead of ~25
+// (the Python-side launch overhead left the GPU idle ~16 % of a step).
+//
+// The forward synchronizes the stream once, to read the number of
+// (splat, tile) pairs K that sizes the pair sort; if K exceeds the caller's
+// pair capacity it returns SS_ERR_CAPACITY with K in v->n_pairs and the
+// caller grows the buffers and calls again.
+#include "ss_common.cuh"
+
+using namespace ss;
+
+static void record(void* ev, cudaStream_t stream) {
+  if (ev) cudaEventRecord((cudaEvent_t)ev, stream);
+}
+
+extern "C" int ss_event_create(void** ev) {
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return check_launch("ss_event_create");
+  *ev = (void*)e;
+  return SS_OK;
+}
+
+extern "C" int ss_event_destroy(void* ev) {
+  cudaEventDestroy((cudaEvent_t)ev);
+  return SS_OK;
+}
+
+extern "C" int ss_event_elapsed_ms(void* start, void* end, float* ms) {
+  if (cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)end) != cudaSuccess)
+    return check_launch("ss_event_elapsed_ms");
+  return SS_OK;
+}
+
+extern "C" int ss_render_fwd(const ss_store* store, const ss_camera* cam, ss_view* v,
+                             cudaStream_t stream) {
+  if (!store || !cam || !v || v->n < 0) return set_error(SS_ERR_INVALID, "ss_render_fwd: bad args");
+  const int W = cam->width, H = cam->height;
+  if (W <= 0 || H <= 0) return set_error(SS_ERR_INVALID, "ss_render_fwd: bad camera");
+  const int tiles_x = (W + kTile - 1) / kTile, tiles_y = (H + kTile - 1) / kTile;
+  const int n_tiles = tiles_x * tiles_y;
+  const int n = v->n;
+  v->n_pairs = 0;
+  v->sorted_sel = 0;
+  int rc;
+  if (n == 0) {
+    cudaMemsetAsync(v->img, 0, sizeof(float) * 3 * (size_t)W * H, stream);
+    cudaMemsetAsync(v->n_contrib, 0, sizeof(int32_t) * (size_t)W * H, stream);
+    cudaMemsetAsync(v->ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, stream);
+    return check_launch("ss_render_fwd");
+  }
+  size_t need_ws = ss_binning_workspace_bytes(n, v->pair_cap > 0 ? v->pair_cap : 1, n_tiles);
+  const size_t need_order = ss_tile_order_workspace_bytes(n_tiles);
+  if (need_order > need_ws) need_ws = need_order;
+  if (v->ws_bytes < need_ws) {
+    v->ws_needed = need_ws;
+    return set_error(SS_ERR_WORKSPACE, "ss_render_fwd: workspace %zu < %zu", v->ws_bytes, need_ws);
+  }
+  if ((rc = ss_project_fwd(store, v->rows, n, cam, v->rec_a, v->rec_b, v->rec_c, v->depth_key,
+                           v->bbox, v->n_tiles, v->geom, v->tile_mask, stream)))
+    return rc;
+  if ((rc = ss_depth_order(v->depth_key, n, v->order, v->ws, v->ws_bytes, stream))) return rc;
+  if ((rc = ss_tile_offsets(v->order, v->n_tiles, n, v->offsets, v->ws, v->ws_bytes, stream)))
+    return rc;
+  int32_t k_host = 0;
+  if (cudaMemcpyAsync(&k_host, v->offsets + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(stream) != cudaSuccess)
+    return check_launch("ss_render_fwd: pair count");
+  v->n_pairs = k_host;
+  if (k_host > v->pair_cap) return set_error(SS_ERR_CAPACITY, "ss_render_fwd: %d pairs > capacity", k_host);
+  if ((rc = ss_emit_tile_pairs(v->order, v->offsets, v->bbox, v->geom, v->tile_mask, n, tiles_x,
+                               v->keys, v->vals, stream)))
+    return rc;
+  int32_t sel = 0;
+  if ((rc = ss_sort_tile_pairs(v->keys, v->vals, v->keys_alt, v->vals_alt, k_host, n_tiles, &sel,
+                               v->ws, v->ws_bytes, stream)))
+    return rc;
+  v->sorted_sel = sel;
+  const uint32_t* sk = sel ? v->keys_alt : v->keys;
+  const int32_t* sv = sel ? v->vals_alt : v->vals;
+  if ((rc = ss_tile_ranges(sk, k_host, n_tiles, v->ranges, stream))) return rc;
+  if ((rc = ss_tile_order(v->ranges, n_tiles, v->tile_order, v->ws, v->ws_bytes, stream))) return rc;
+  record(v->events[0], stream);
+  rc = ss_raster_fwd(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,
+                     v->t_final, v->n_contrib, stream);
+  record(v->events[1], stream);
+  return rc;
+}
+
+extern "C" int ss_render_bwd(const ss_store* store, const ss_camera* cam, const ss_view* v,
+                             const float* dimg, float* g2d, const uint8_t* trainable_mask,
+                             int64_t trainable_rows, float* grads, cudaStream_t stream) {
+  if (!store || !cam || !v) return set_error(SS_ERR_INVALID, "ss_render_bwd: bad args");
+  if (v->n == 0 || v->n_pairs == 0) return SS_OK;
+  cudaMemsetAsync(g2d, 0, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
+  const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
+  record(v->events[2], stream);
+  int rc = ss_raster_bwd(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, cam->width, cam->height,
+                         v->tile_order, dimg, v->t_final, v->n_contrib, g2d, stream);
+  record(v->events[3], stream);
+  if (rc) return rc;
+  return ss_project_bwd(store, v->rows, v->n, cam, g2d, v->depth_key, trainable_mask,
+                        trainable_rows, grads, stream);
+}

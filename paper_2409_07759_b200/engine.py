@@ -73,27 +73,25 @@ class ViewPipeline:
         L.lib()
 
     def enable_timing(self, on: bool = True):
+        """Record CUDA events around the raster kernels (inside the native
+        driver, on the launch stream) for kernel_ms()."""
+        if not on and self.events:
+            for evs in self.events.get("_pending", []):
+                for e in evs:
+                    L.lib().ss_event_destroy(e)
         self.events = {} if on else None
 
-    def _mark(self, name):
-        if self.events is None:
-            return None
-        ev = torch.cuda.Event(enable_timing=True)
-        ev.record()
-        return (name, ev)
-
-    def _done(self, tok):
-        if tok is None:
-            return
-        name, start = tok
-        end = torch.cuda.Event(enable_timing=True)
-        end.record()
-        self.events.setdefault(name, []).append((start, end))
-
     def kernel_ms(self) -> dict:
-        """Total milliseconds per timed stage (synchronizes)."""
+        """Total milliseconds of raster_fwd / raster_bwd over the timed views
+        (synchronizes)."""
         torch.cuda.synchronize()
-        return {k: sum(a.elapsed_time(b) for a, b in v) for k, v in (self.events or {}).items()}
+        out = {"raster_fwd": 0.0, "raster_bwd": 0.0}
+        ms = ctypes.c_float()
+        for evs in (self.events or {}).get("_pending", []):
+            for name, (a, b) in (("raster_fwd", (0, 1)), ("raster_bwd", (2, 3))):
+                if L.lib().ss_event_elapsed_ms(evs[a], evs[b], ctypes.byref(ms)) == L.SS_OK:
+                    out[name] += ms.value
+        return out
 
     def _buf(self, name, shape, dtype):
         t = _grow(self._b.get(name), shape, dtype, self.dev)
@@ -103,106 +101,99 @@ class ViewPipeline:
     # ------------------------------------------------------------------ fwd
     def forward(self, store: Store, rows: torch.Tensor | None, n: int, cam, stream=None):
         """Project, bin and rasterize n active splats (row ids `rows`, or
-        0..n-1 into `store` when rows is None).  Returns the (H, W, 3) float32
-        image (a view into an internal buffer)."""
+        0..n-1 into `store` when rows is None) with one native call
+        (ss_render_fwd).  Returns the (H, W, 3) float32 image (a view into an
+        internal buffer)."""
         lib = L.lib()
         sp = L.stream_ptr(stream)
         W, H = int(cam.width), int(cam.height)
         tiles_x, tiles_y = (W + TILE - 1) // TILE, (H + TILE - 1) // TILE
         n_tiles = tiles_x * tiles_y
-        self.n, self.width, self.height = n, W, H
-        self.n_tiles = n_tiles
+        self.n, self.width, self.height, self.n_tiles = n, W, H, n_tiles
         self.cam_struct = L.camera_struct(cam)
         self.store, self.store_struct, self.rows = store, store.struct(), rows
         nn = max(n, 1)
-        rec_a = self._buf("rec_a", (nn, 4), torch.float32)
-        rec_b = self._buf("rec_b", (nn, 4), torch.float32)
-        rec_c = self._buf("rec_c", (nn,), torch.float32)
-        dkey = self._buf("depth_key", (nn,), torch.int64)
-        bbox = self._buf("bbox", (nn, 4), torch.int32)
-        ntl = self._buf("n_tiles", (nn,), torch.int32)
-        geom = self._buf("geom", (nn, 7), torch.float64)
-        tmask = self._buf("tile_mask", (nn,), torch.int64)
-        order = self._buf("order", (nn,), torch.int32)
-        offsets = self._buf("offsets", (nn + 1,), torch.int32)
-        ranges = self._buf("ranges", (n_tiles, 2), torch.int32)
-        img = self._buf("img", (H * W * 3,), torch.float32)
-        t_final = self._buf("t_final", (H * W,), torch.float32)
-        n_contrib = self._buf("n_contrib", (H * W,), torch.int32)
-        ws_bytes = int(lib.ss_binning_workspace_bytes(nn, 1, n_tiles))
-        ws = self._buf("ws_bin", (ws_bytes,), torch.uint8)
-        if n == 0:
-            img[: H * W * 3].zero_()
-            t_final[: H * W].fill_(1.0)
-            n_contrib[: H * W].zero_()
-            ranges.zero_()
-            self.n_pairs = 0
-            return img[: H * W * 3].view(H, W, 3)
-        rp = L.ptr(rows)
-        L.check(lib.ss_project_fwd(ctypes.byref(self.store_struct), rp, n, ctypes.byref(self.cam_struct),
-                                   L.ptr(rec_a), L.ptr(rec_b), L.ptr(rec_c), L.ptr(dkey), L.ptr(bbox),
-                                   L.ptr(ntl), L.ptr(geom), L.ptr(tmask), sp), "project_fwd")
-        L.check(lib.ss_depth_order(L.ptr(dkey), n, L.ptr(order), L.ptr(ws), ws.numel(), sp),
-                "depth_order")
-        L.check(lib.ss_tile_offsets(L.ptr(order), L.ptr(ntl), n, L.ptr(offsets), L.ptr(ws),
-                                    ws.numel(), sp), "tile_offsets")
-        n_pairs = int(offsets[n].item())  # the one host sync of a view
-        self.n_pairs = n_pairs
-        pc = max(n_pairs, 1)
-        keys = self._buf("keys", (pc,), torch.int32)
-        vals = self._buf("vals", (pc,), torch.int32)
-        keys_alt = self._buf("keys_alt", (pc,), torch.int32)
-        vals_alt = self._buf("vals_alt", (pc,), torch.int32)
-        ws_bytes = int(lib.ss_binning_workspace_bytes(nn, pc, n_tiles))
-        ws = self._buf("ws_bin", (ws_bytes,), torch.uint8)
-        L.check(lib.ss_emit_tile_pairs(L.ptr(order), L.ptr(offsets), L.ptr(bbox), L.ptr(geom),
-                                       L.ptr(tmask), n, tiles_x, L.ptr(keys), L.ptr(vals), sp),
-                "emit_tile_pairs")
-        sel = ctypes.c_int32(0)
-        L.check(lib.ss_sort_tile_pairs(L.ptr(keys), L.ptr(vals), L.ptr(keys_alt), L.ptr(vals_alt),
-                                       n_pairs, n_tiles, ctypes.byref(sel), L.ptr(ws), ws.numel(),
-                                       sp), "sort_tile_pairs")
-        self.sel = sel.value
-        sk, sv = (keys, vals) if sel.value == 0 else (keys_alt, vals_alt)
-        self.sorted_keys, self.sorted_vals = sk, sv
-        L.check(lib.ss_tile_ranges(L.ptr(sk), n_pairs, n_tiles, L.ptr(ranges), sp), "tile_ranges")
-        tord = self._buf("tile_order", (n_tiles,), torch.int32)
-        tws = self._buf("ws_tord", (int(lib.ss_tile_order_workspace_bytes(n_tiles)),), torch.uint8)
-        L.check(lib.ss_tile_order(L.ptr(ranges), n_tiles, L.ptr(tord), L.ptr(tws), tws.numel(), sp),
-                "tile_order")
-        tok = self._mark("raster_fwd")
-        L.check(lib.ss_raster_fwd(L.ptr(ranges), L.ptr(sv), L.ptr(rec_a), L.ptr(rec_b),
-                                  L.ptr(rec_c), W, H, L.ptr(tord), L.ptr(img), L.ptr(t_final),
-                                  L.ptr(n_contrib), sp), "raster_fwd")
-        self._done(tok)
-        return img[: H * W * 3].view(H, W, 3)
+        b = {}
+        for name, shape, dt in (("rec_a", (nn, 4), torch.float32), ("rec_b", (nn, 4), torch.float32),
+                                ("rec_c", (nn,), torch.float32), ("depth_key", (nn,), torch.int64),
+                                ("bbox", (nn, 4), torch.int32), ("n_tiles", (nn,), torch.int32),
+                                ("geom", (nn, 7), torch.float64), ("tile_mask", (nn,), torch.int64),
+                                ("order", (nn,), torch.int32), ("offsets", (nn + 1,), torch.int32),
+                                ("ranges", (n_tiles, 2), torch.int32),
+                                ("tile_order", (n_tiles,), torch.int32),
+                                ("img", (H * W * 3,), torch.float32),
+                                ("t_final", (H * W,), torch.float32),
+                                ("n_contrib", (H * W,), torch.int32)):
+            b[name] = self._buf(name, shape, dt)
+        if "keys" not in self._b:
+            cap = max(1 << 16, 16 * nn)
+            for name in ("keys", "vals", "keys_alt", "vals_alt"):
+                self._b[name] = torch.empty(cap, dtype=torch.int32, device=self.dev)
+            self._b["ws_bin"] = torch.empty(1 << 20, dtype=torch.uint8, device=self.dev)
+        v = L.SSView()
+        for _ in range(4):
+            v.rows = L.ptr(rows)
+            v.n = n
+            for name in ("rec_a", "rec_b", "rec_c", "depth_key", "bbox", "n_tiles", "geom",
+                         "tile_mask", "order", "offsets", "ranges", "tile_order", "img", "t_final",
+                         "n_contrib"):
+                setattr(v, name, L.ptr(b[name]))
+            for name in ("keys", "vals", "keys_alt", "vals_alt"):
+                setattr(v, name, L.ptr(self._b[name]))
+            v.pair_cap = self._b["keys"].numel()
+            v.ws = L.ptr(self._b["ws_bin"])
+            v.ws_bytes = self._b["ws_bin"].numel()
+            if self.events is not None:
+                evs = self._new_events()
+                for i in range(4):
+                    v.events[i] = evs[i]
+            rc = lib.ss_render_fwd(ctypes.byref(self.store_struct), ctypes.byref(self.cam_struct),
+                                   ctypes.byref(v), sp)
+            if rc == L.SS_ERR_CAPACITY:
+                cap = int(v.n_pairs * 1.25) + 1024
+                for name in ("keys", "vals", "keys_alt", "vals_alt"):
+                    self._b[name] = torch.empty(cap, dtype=torch.int32, device=self.dev)
+                continue
+            if rc == L.SS_ERR_WORKSPACE:
+                self._b["ws_bin"] = torch.empty(int(v.ws_needed * 1.25), dtype=torch.uint8,
+                                                device=self.dev)
+                continue
+            L.check(rc, "render_fwd")
+            break
+        else:
+            raise L.SwingsError("render_fwd: could not size buffers")
+        self.view = v
+        self.n_pairs = int(v.n_pairs)
+        self.sel = int(v.sorted_sel)
+        sk, sv = (("keys", "vals") if self.sel == 0 else ("keys_alt", "vals_alt"))
+        self.sorted_keys, self.sorted_vals = self._b[sk], self._b[sv]
+        return b["img"][: H * W * 3].view(H, W, 3)
+
+    def _new_events(self):
+        evs = []
+        for _ in range(4):
+            e = ctypes.c_void_p()
+            L.check(L.lib().ss_event_create(ctypes.byref(e)), "event_create")
+            evs.append(e.value)
+        self.events.setdefault("_pending", []).append(evs)
+        return evs
 
     # ------------------------------------------------------------------ bwd
     def backward(self, dimg: torch.Tensor, grads: torch.Tensor, trainable_mask=None,
                  trainable_rows: int | None = None, stream=None):
         """Accumulate optimization-space gradients of sum(dimg * image) into
-        `grads` (rows x 14 float32, indexed by row id; caller zeroes)."""
-        lib = L.lib()
-        sp = L.stream_ptr(stream)
-        n, W, H = self.n, self.width, self.height
+        `grads` (rows x 14 float32, indexed by row id; caller zeroes) with one
+        native call (ss_render_bwd)."""
+        n = self.n
         if n == 0 or self.n_pairs == 0:
             return
         g2d = self._buf("g2d", (n, L.SS_G2D_ROW), torch.float32)
-        g2d[:n].zero_()
-        b = self._b
-        tok = self._mark("raster_bwd")
-        L.check(lib.ss_raster_bwd(L.ptr(b["ranges"]), L.ptr(self.sorted_vals), L.ptr(b["rec_a"]),
-                                  L.ptr(b["rec_b"]), L.ptr(b["rec_c"]), W, H,
-                                  L.ptr(b["tile_order"]), L.ptr(dimg),
-                                  L.ptr(b["t_final"]), L.ptr(b["n_contrib"]), L.ptr(g2d), sp),
-                "raster_bwd")
-        self._done(tok)
         if trainable_rows is None:
             trainable_rows = self.store.n_opt + self.store.n_mat
-        L.check(lib.ss_project_bwd(ctypes.byref(self.store_struct), L.ptr(self.rows), n,
-                                   ctypes.byref(self.cam_struct), L.ptr(g2d), L.ptr(b["depth_key"]),
-                                   L.ptr(trainable_mask), int(trainable_rows), L.ptr(grads), sp),
-                "project_bwd")
+        L.check(L.lib().ss_render_bwd(ctypes.byref(self.store_struct), ctypes.byref(self.cam_struct),
+                                      ctypes.byref(self.view), L.ptr(dimg), L.ptr(g2d),
+                                      L.ptr(trainable_mask), int(trainable_rows), L.ptr(grads),
+                                      L.stream_ptr(stream)), "render_bwd")
 
     def k_used(self) -> int:
         """SURVEY.md §8 K_used of the last view: per tile, the longest list

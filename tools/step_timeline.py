@@ -1,0 +1,58 @@
+"""Per-step GPU timeline of the config-3 training step (torch.profiler, CUPTI):
+kernel time by name, GPU busy time vs the step's wall span, i.e. the idle gaps
+that launch overhead and the per-view host sync leave.
+
+    python tools/step_timeline.py [--steps 5] [--config 3]
+"""
+
+import argparse
+import collections
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--config", type=int, default=3)
+    a = ap.parse_args()
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    import bench
+    from paper_2409_07759_b200 import train
+
+    c, scene, ds, state, window = bench.build_workload(a.config, None, "gt")
+    train.train_swin(window[0], window[1], state, ds, iterations=5)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+        train.train_swin(window[0], window[1], state, ds, iterations=a.steps)
+        torch.cuda.synchronize()
+    evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    spans = sorted((e.time_range.start, e.time_range.end, e.name) for e in evs)
+    t0, t1 = spans[0][0], max(s[1] for s in spans)
+    busy = 0
+    cur_s, cur_e = spans[0][0], spans[0][1]
+    for s, e, _ in spans[1:]:
+        if s > cur_e:
+            busy += cur_e - cur_s
+            cur_s, cur_e = s, e
+        else:
+            cur_e = max(cur_e, e)
+    busy += cur_e - cur_s
+    by = collections.Counter()
+    for s, e, n in spans:
+        by[n.split("(")[0][:60]] += e - s
+    out = {"steps": a.steps, "span_us_per_step": (t1 - t0) / a.steps,
+           "gpu_busy_us_per_step": busy / a.steps,
+           "idle_us_per_step": (t1 - t0 - busy) / a.steps,
+           "kernels_us_per_step": {k: v / a.steps for k, v in by.most_common(25)}}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
