@@ -151,6 +151,21 @@ int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                   const int32_t* tile_order, float* img, float* t_final, int32_t* n_contrib,
                   ss_stream_t stream);
 
+/* Deterministic variant of ss_raster_bwd: no float atomics.  Each warp writes
+ * its reduced 9 values per entry to partial (ss_raster_partial_floats(K)
+ * floats), indexed by the entry's emit position (order / offsets / bbox /
+ * tile_mask / geom from the forward), and every splat's partials are summed
+ * in a fixed order into g2d (all of g2d's n rows are written).  rank: n
+ * int32 scratch.  Bit-identical results run to run. */
+int64_t ss_raster_partial_floats(int64_t n_pairs);
+int ss_raster_bwd_deterministic(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                                const void* rec_b, const float* rec_c, int32_t width,
+                                int32_t height, const int32_t* tile_order, const float* dimg,
+                                const float* t_final, const int32_t* n_contrib,
+                                const int32_t* order, const int32_t* offsets, const int32_t* bbox,
+                                const uint64_t* tile_mask, const double* geom, int32_t n,
+                                int32_t* rank, float* partial, float* g2d, ss_stream_t stream);
+
 /* Tuning knob: pixels per lane in the raster kernels (2, 4 or 8); a warp
  * covers 16 x (2 strip) pixels, i.e. 8 / strip warps per tile.  Default 4. */
 int ss_set_raster_strip(int32_t strip);
@@ -251,6 +266,8 @@ typedef struct {
   int32_t sorted_sel;   /* out: 1 when the sorted pairs are in *_alt      */
   int32_t pad1;
   void* events[4];      /* optional cudaEvent_t: raster fwd start/end, bwd start/end */
+  float* partial;       /* deterministic backward: ss_raster_partial_floats(K) floats, */
+  int32_t* rank;        /*   and n int32; partial == NULL selects the atomic backward */
 } ss_view;
 
 /* Projection -> depth order -> tile offsets -> [one stream sync for K] ->

@@ -54,7 +54,8 @@ class SSView(Structure):
                 ("keys_alt", P), ("vals_alt", P), ("pair_cap", c_int64), ("ranges", P),
                 ("tile_order", P), ("img", P), ("t_final", P), ("n_contrib", P), ("ws", P),
                 ("ws_bytes", c_size_t), ("ws_needed", c_size_t), ("n_pairs", c_int64),
-                ("sorted_sel", c_int32), ("pad1", c_int32), ("events", P * 4)]
+                ("sorted_sel", c_int32), ("pad1", c_int32), ("events", P * 4),
+                ("partial", P), ("rank", P)]
 
 _SIGNATURES = {
     "ss_last_error": ([], ctypes.c_char_p),
@@ -75,6 +76,9 @@ _SIGNATURES = {
     "ss_raster_fwd": ([P, P, P, P, P, I32, I32, P, P, P, P, P], c_int),
     "ss_raster_bwd": ([P, P, P, P, P, I32, I32, P, P, P, P, P, P], c_int),
     "ss_set_raster_strip": ([I32], c_int),
+    "ss_raster_partial_floats": ([I64], c_int64),
+    "ss_raster_bwd_deterministic": ([P, P, P, P, P, I32, I32, P, P, P, P, P, P, P, P, P, I32, P, P,
+                                     P, P], c_int),
     "ss_project_bwd": ([POINTER(SSStore), P, I32, POINTER(SSCamera), P, P, P, I64, P, P], c_int),
     "ss_loss_workspace_bytes": ([I32, I32], c_size_t),
     "ss_loss_l1_ssim": ([P, P, P, P, I32, I32, c_double, P, P, P, c_size_t, P], c_int),

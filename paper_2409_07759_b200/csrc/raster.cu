@@ -219,14 +219,49 @@ __device__ __forceinline__ int red9_slot(int lane, bool& valid) {
   return 5 * b4 + p;
 }
 
-template <int STRIP>
+// Deterministic mode (DET): instead of float atomics into g2d, a warp writes
+// its 9 reduced values for an entry to partial[(e * WPT + sub) * 9 + c], where
+// e is the entry's position in emit order (rank-ordered runs per splat, see
+// binning.cu) -- recovered from the splat's rank, its kept-tile mask and a
+// popcount -- and g2d_reduce_kernel sums each splat's run in a fixed order.
+struct DetArgs {
+  float* partial;
+  const int32_t* rank;
+  const int32_t* offsets;
+  const int4* bbox;
+  const uint64_t* tile_mask;
+  const double* geom;
+};
+
+__device__ __forceinline__ int64_t emit_position(const DetArgs& d, int g, int tx, int ty) {
+  const int4 bb = d.bbox[g];
+  const int tx0 = bb.x / kTile, tx1 = (bb.y - 1) / kTile + 1, ty0 = bb.z / kTile;
+  const int w = tx1 - tx0;
+  const int local = (ty - ty0) * w + (tx - tx0);
+  const uint64_t mask = d.tile_mask[g];
+  int j;
+  if (local < 64) {
+    j = __popcll(mask & ((1ull << local) - 1ull));
+  } else {
+    j = __popcll(mask);
+    double gl[kGeom];
+#pragma unroll
+    for (int c = 0; c < kGeom; ++c) gl[c] = d.geom[(int64_t)g * kGeom + c];
+    for (int q = 64; q < local; ++q) j += tile_keeps(gl, tx0 + q % w, ty0 + q / w, bb);
+  }
+  return (int64_t)d.offsets[d.rank[g]] + j;
+}
+
+template <int STRIP, bool DET>
 __global__ void __launch_bounds__(kWarps * 32)
     raster_bwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
                       const float4* __restrict__ rec_a, const float4* __restrict__ rec_b,
                       const float* __restrict__ rec_c, int width, int height, int tiles_x,
                       int n_tiles, const int32_t* __restrict__ tile_order,
                       const float* __restrict__ dimg, const float* __restrict__ t_final,
-                      const int32_t* __restrict__ n_contrib, float* __restrict__ g2d) {
+                      const int32_t* __restrict__ n_contrib, float* __restrict__ g2d,
+                      DetArgs det) {
+  __shared__ int64_t s_epos[kWarps][32];
   __shared__ WarpStage s_stage[kWarps];
   constexpr int WPT = kTile / (2 * STRIP);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -264,10 +299,20 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int walk_end = rg.x + __reduce_max_sync(0xffffffffu, my_max);
   bool slot_ok;
   const int slot = red9_slot(lane, slot_ok);
+  if (DET) {
+    // entries this warp never visits contribute zero partials
+    for (int idx = walk_end + lane; idx < rg.y; idx += 32) {
+      const int64_t e = emit_position(det, vals[idx], tx, ty);
+      float* dst = det.partial + (e * WPT + sub) * 9;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) dst[c] = 0.f;
+    }
+  }
   for (int end = walk_end; end > rg.x; end -= 32) {
     const int start = max(rg.x, end - 32);
     __syncwarp();
     stage_load(st, lane, start + lane, end, vals, rec_a, rec_b, rec_c);
+    if (DET && start + lane < end) s_epos[warp][lane] = emit_position(det, st.g[lane], tx, ty);
     __syncwarp();
     for (int j = end - start - 1; j >= 0; --j) {
       const int pos = start - rg.x + j;  // 0-based position in the tile list
@@ -284,7 +329,10 @@ __global__ void __launch_bounds__(kWarps * 32)
         valid[k] = (pos < last[k]) && (e[k] >= s.thr);
         any |= valid[k];
       }
-      if (!__any_sync(0xffffffffu, any)) continue;
+      if (!__any_sync(0xffffffffu, any)) {
+        if (DET && slot_ok) det.partial[(s_epos[warp][j] * WPT + sub) * 9 + slot] = 0.f;
+        continue;
+      }
       float sc0, sc1, sc2, st0, st1, st2;
 #pragma unroll
       for (int k = 0; k < STRIP; ++k) {
@@ -334,9 +382,37 @@ __global__ void __launch_bounds__(kWarps * 32)
       v[7] = sc1;
       v[8] = sc2;
       const float tot = reduce9(v, lane);
-      if (slot_ok) atomicAdd(g2d + (int64_t)st.g[j] * SS_G2D_ROW + slot, tot);
+      if (slot_ok) {
+        if (DET) det.partial[(s_epos[warp][j] * WPT + sub) * 9 + slot] = tot;
+        else atomicAdd(g2d + (int64_t)st.g[j] * SS_G2D_ROW + slot, tot);
+      }
     }
   }
+}
+
+__global__ void rank_kernel(const int32_t* __restrict__ order, int n, int32_t* __restrict__ rank) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) rank[order[k]] = k;
+}
+
+// Fixed-order sum of each splat's partials (emit order, then warp sub-tile).
+__global__ void g2d_reduce_kernel(const float* __restrict__ partial,
+                                  const int32_t* __restrict__ order,
+                                  const int32_t* __restrict__ offsets, int n, int wpt,
+                                  float* __restrict__ g2d) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  float acc[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) acc[c] = 0.f;
+  const int64_t e0 = offsets[k], e1 = offsets[k + 1];
+  for (int64_t e = e0 * wpt; e < e1 * wpt; ++e) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) acc[c] += partial[e * 9 + c];
+  }
+  float* dst = g2d + (int64_t)order[k] * SS_G2D_ROW;
+#pragma unroll
+  for (int c = 0; c < 9; ++c) dst[c] = acc[c];
 }
 
 static int g_strip = 4;
@@ -372,22 +448,59 @@ extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const v
   return check_launch("ss_raster_fwd");
 }
 
-extern "C" int ss_raster_bwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+static int raster_bwd_launch(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                              const void* rec_b, const float* rec_c, int32_t width, int32_t height,
                              const int32_t* tile_order, const float* dimg, const float* t_final,
-                             const int32_t* n_contrib, float* g2d, cudaStream_t stream) {
+                             const int32_t* n_contrib, float* g2d, const DetArgs* det,
+                             cudaStream_t stream) {
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_raster_bwd: bad size");
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
   const int wpt = kTile / (2 * g_strip);
   const int blocks = (n_tiles * wpt + kWarps - 1) / kWarps;
-#define SS_BWD(S)                                                                             \
-  raster_bwd_kernel<S><<<blocks, kWarps * 32, 0, stream>>>(                                   \
+  DetArgs d = det ? *det : DetArgs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+#define SS_BWD(S, D)                                                                          \
+  raster_bwd_kernel<S, D><<<blocks, kWarps * 32, 0, stream>>>(                                \
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
-      height, tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d)
-  if (g_strip == 8) SS_BWD(8);
-  else if (g_strip == 4) SS_BWD(4);
-  else SS_BWD(2);
+      height, tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d)
+  if (det) {
+    if (g_strip == 8) SS_BWD(8, true);
+    else if (g_strip == 4) SS_BWD(4, true);
+    else SS_BWD(2, true);
+  } else {
+    if (g_strip == 8) SS_BWD(8, false);
+    else if (g_strip == 4) SS_BWD(4, false);
+    else SS_BWD(2, false);
+  }
 #undef SS_BWD
   return check_launch("ss_raster_bwd");
+}
+
+extern "C" int ss_raster_bwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                             const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                             const int32_t* tile_order, const float* dimg, const float* t_final,
+                             const int32_t* n_contrib, float* g2d, cudaStream_t stream) {
+  return raster_bwd_launch(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, dimg,
+                           t_final, n_contrib, g2d, nullptr, stream);
+}
+
+extern "C" int64_t ss_raster_partial_floats(int64_t n_pairs) {
+  return n_pairs * (kTile / (2 * g_strip)) * 9;
+}
+
+extern "C" int ss_raster_bwd_deterministic(
+    const int32_t* ranges, const int32_t* vals, const void* rec_a, const void* rec_b,
+    const float* rec_c, int32_t width, int32_t height, const int32_t* tile_order,
+    const float* dimg, const float* t_final, const int32_t* n_contrib, const int32_t* order,
+    const int32_t* offsets, const int32_t* bbox, const uint64_t* tile_mask, const double* geom,
+    int32_t n, int32_t* rank, float* partial, float* g2d, cudaStream_t stream) {
+  if (n <= 0) return SS_OK;
+  rank_kernel<<<grid_for(n, 256), 256, 0, stream>>>(order, n, rank);
+  DetArgs d{partial, rank, offsets, (const int4*)bbox, tile_mask, geom};
+  int rc = raster_bwd_launch(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, dimg,
+                             t_final, n_contrib, g2d, &d, stream);
+  if (rc) return rc;
+  g2d_reduce_kernel<<<grid_for(n, 128), 128, 0, stream>>>(partial, order, offsets, n,
+                                                           kTile / (2 * g_strip), g2d);
+  return check_launch("ss_raster_bwd_deterministic");
 }

@@ -97,8 +97,15 @@ extern "C" int ss_render_bwd(const ss_store* store, const ss_camera* cam, const 
   cudaMemsetAsync(g2d, 0, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
   const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
   record(v->events[2], stream);
-  int rc = ss_raster_bwd(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, cam->width, cam->height,
-                         v->tile_order, dimg, v->t_final, v->n_contrib, g2d, stream);
+  int rc;
+  if (v->partial)
+    rc = ss_raster_bwd_deterministic(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, cam->width,
+                                     cam->height, v->tile_order, dimg, v->t_final, v->n_contrib,
+                                     v->order, v->offsets, v->bbox, v->tile_mask, v->geom, v->n,
+                                     v->rank, v->partial, g2d, stream);
+  else
+    rc = ss_raster_bwd(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, cam->width, cam->height,
+                       v->tile_order, dimg, v->t_final, v->n_contrib, g2d, stream);
   record(v->events[3], stream);
   if (rc) return rc;
   return ss_project_bwd(store, v->rows, v->n, cam, g2d, v->depth_key, trainable_mask,

@@ -220,6 +220,7 @@ class DeviceModel:
         self.grads.zero_()
         cam = dataset.cameras[view]
         gt = dataset.device_frame(frame, view)
+        self.pipe.deterministic = state.deterministic
         img = self.pipe.forward(self.store, self.active_rows, n, cam)
         dimg, sums = self.lossbuf.run(img, cam.height, cam.width, gt_u8=gt, lut=self.lut,
                                       ssim_weight=cfg.ssim_weight)

@@ -70,6 +70,7 @@ class ViewPipeline:
         self.n_pairs = 0
         self.sel = 0
         self.events = None  # name -> [(start, end)] CUDA events when timing
+        self.deterministic = False  # fixed-order gradient sums (no float atomics)
         L.lib()
 
     def enable_timing(self, on: bool = True):
@@ -188,6 +189,13 @@ class ViewPipeline:
         if n == 0 or self.n_pairs == 0:
             return
         g2d = self._buf("g2d", (n, L.SS_G2D_ROW), torch.float32)
+        if self.deterministic:
+            nf = int(L.lib().ss_raster_partial_floats(self.n_pairs))
+            part = self._buf("partial", (max(nf, 1),), torch.float32)
+            rank = self._buf("rank", (max(n, 1),), torch.int32)
+            self.view.partial, self.view.rank = L.ptr(part), L.ptr(rank)
+        else:
+            self.view.partial, self.view.rank = None, None
         if trainable_rows is None:
             trainable_rows = self.store.n_opt + self.store.n_mat
         L.check(L.lib().ss_render_bwd(ctypes.byref(self.store_struct), ctypes.byref(self.cam_struct),

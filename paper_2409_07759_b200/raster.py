@@ -79,6 +79,13 @@ def pipeline() -> ViewPipeline:
     return _PIPE
 
 
+def set_deterministic(flag: bool = True) -> None:
+    """Fixed-order gradient accumulation in render_arrays_backward (no float
+    atomics; bit-identical run to run, like the reference's single-threaded
+    loops, SPEC.md:153)."""
+    pipeline().deterministic = bool(flag)
+
+
 def _upload(arrays: GaussianArrays) -> Store:
     rows = torch.from_numpy(arrays.rows()).to(device())
     return Store(opt=None, mat=rows)

@@ -225,3 +225,81 @@ def test_active_filter_and_consistency_error(ss):
     assert np.array_equal(full.pixels, pre.pixels)
     with pytest.raises(R.ConsistencyError):
         R.render_backward(cam, pairs[:4], 0, np.zeros((32, 32, 3)), expected_active=[0, 1])
+
+
+def test_huge_and_tiny_splats_tile_keys_and_image(ss):
+    """Splats whose 8-sigma bbox spans > 64 tiles (the emit path past the
+    64-bit keep mask), sub-pixel splats, splats straddling tile borders."""
+    P, R = ss
+    rng = np.random.default_rng(11)
+    n = 600
+    means = rng.uniform((-0.6, -0.45, 1.5), (0.6, 0.45, 3.5), size=(n, 3))
+    scales = np.exp(rng.uniform(np.log(0.002), np.log(0.02), size=(n, 3)))
+    scales[:12] = rng.uniform(0.15, 0.35, size=(12, 3))       # huge footprints
+    scales[12:40] = rng.uniform(0.0005, 0.001, size=(28, 3))  # sub-pixel
+    arr = P.GaussianArrays(means, random_unit_quats(rng, n), scales, rng.uniform(0.05, 0.95, n),
+                           rng.uniform(0, 1, (n, 3)))
+    from conftest import Cam
+    ocam = Cam(300, 220, 260.0, 250.0, 150.0, 110.0, np.eye(3), np.zeros(3))
+    cam = cam_from(P, ocam)
+    cache, bins, st = _tile_check(P, R, cam, arr, ocam)
+    x0, x1, y0, y1 = cache["bbox"]
+    ntile = (((x1 - 1) // 16) - (x0 // 16) + 1) * (((y1 - 1) // 16) - (y0 // 16) + 1)
+    assert ntile.max() > 64
+    ref = O.blend_forward_tiled(cache, cam.height, cam.width, nthreads=8, bins=bins)
+    img = R.render_arrays(cam, arr).pixels
+    assert np.abs(img - ref["image"]).max() <= IMG_TOL
+    gdir = rng.normal(size=img.shape)
+    g = R.render_arrays_backward(cam, arr, gdir)
+    gref = O.projection_backward(ocam, cache, n, *O.blend_backward_tiled(
+        cache, bins, cam.height, cam.width, gdir, nthreads=8))
+    grad_check(g, gref, what="huge/tiny")
+
+
+@pytest.mark.slow
+def test_config3_full_view_image_and_gradients(ss):
+    """A whole 1352x1014 view of the 300k-splat config-3 scene: image within
+    1e-4 of the fp64 oracle everywhere, gradients within 1e-3 of the max."""
+    P, R = ss
+    n = 300_000
+    arr = _synth_scene(P, n, (300.0 / n) ** (1 / 3), seed=7)
+    ocam = arc_camera(7, 20, 1352, 1014)
+    cam = cam_from(P, ocam)
+    cache, bins, st = _tile_check(P, R, cam, arr, ocam)
+    ref = O.blend_forward_tiled(cache, cam.height, cam.width, nthreads=O.default_threads(),
+                                bins=bins)
+    img = R.render_arrays(cam, arr).pixels
+    err = np.abs(img - ref["image"])
+    assert err.max() <= IMG_TOL, err.max()
+    gdir = np.random.default_rng(3).normal(size=img.shape) * 1e-6
+    g = R.render_arrays_backward(cam, arr, gdir)
+    gref = O.projection_backward(ocam, cache, n, *O.blend_backward_tiled(
+        cache, bins, cam.height, cam.width, gdir, nthreads=O.default_threads()))
+    grad_check(g, gref, what="config3 full view")
+
+
+def test_deterministic_backward_bit_identical(ss):
+    """Fixed-order gradient sums: bit-identical across runs and within the
+    oracle tolerance (also the >64-tile emit-position path)."""
+    P, R = ss
+    rng = np.random.default_rng(4)
+    arr = _synth_scene(P, 20_000, (300.0 / 30_000) ** (1 / 3), seed=2)
+    big = arr.scales.copy()
+    big[:5] *= 8.0
+    arr = P.GaussianArrays(arr.means, arr.quats, big, arr.opacities, arr.colors)
+    ocam = arc_camera(1, 5, 320, 240)
+    cam = cam_from(P, ocam)
+    gdir = rng.normal(size=(240, 320, 3))
+    R.set_deterministic(True)
+    try:
+        g1 = R.render_arrays_backward(cam, arr, gdir)
+        g2 = R.render_arrays_backward(cam, arr, gdir)
+    finally:
+        R.set_deterministic(False)
+    for k in g1:
+        assert np.array_equal(g1[k], g2[k]), k
+    gref = O.render_arrays_backward(ocam, arr.means, arr.quats, arr.scales, arr.opacities,
+                                    arr.colors, gdir, tiled=True, nthreads=8)
+    grad_check(g1, gref, what="deterministic")
+    ga = R.render_arrays_backward(cam, arr, gdir)
+    grad_check(ga, g1, tol=1e-5, what="atomic vs deterministic")

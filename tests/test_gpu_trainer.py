@@ -170,3 +170,18 @@ def test_device_relocation_conserves_and_revives(T):
     for r in dead.cpu().numpy()[:200]:
         assert tuple(after[r, :3].cpu().numpy().tolist()) in alive_means
     assert after.shape == before.shape
+
+
+def test_deterministic_training_is_bit_reproducible(T, tmp_path):
+    """With fixed-order gradient sums the whole device step (render, loss,
+    backward, Adam + Philox SGLD, relocation) is bit-reproducible: two
+    train_video runs write identical containers (test_trainer.py:468-473)."""
+    import paper_2409_07759_b200 as P
+    from paper_2409_07759_b200 import synth
+    _, ds = synth.synth_scene(3, 5, 2, 300, tmp_path / "ds", width=48, height=40)
+    cfg = T.TrainConfig(swin_size=2, num_gs=200, genesis_iterations=12, window_iterations=6,
+                        relocate_period=5, rng_seed=0, max_cached_frames=4)
+    T.train_video(ds, cfg, tmp_path / "a.swin", deterministic=True)
+    ds2 = type(ds)(tmp_path / "ds", max_cached_frames=4)
+    T.train_video(ds2, cfg, tmp_path / "b.swin", deterministic=True)
+    assert (tmp_path / "a.swin").read_bytes() == (tmp_path / "b.swin").read_bytes()
