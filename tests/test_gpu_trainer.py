@@ -185,3 +185,66 @@ def test_deterministic_training_is_bit_reproducible(T, tmp_path):
     ds2 = type(ds)(tmp_path / "ds", max_cached_frames=4)
     T.train_video(ds2, cfg, tmp_path / "b.swin", deterministic=True)
     assert (tmp_path / "a.swin").read_bytes() == (tmp_path / "b.swin").read_bytes()
+
+
+def test_ground_truth_prefetch_pipeline(T, tmp_path):
+    """§8(f)-3: PNG decode on the thread pool + pinned async H2D gives exactly
+    the bytes of the synchronous path; the model is independent of cache size
+    and prefetching (test_trainer.py:475-484, test_dataset_synth.py:56-84)."""
+    import torch
+    from paper_2409_07759_b200 import synth
+    from paper_2409_07759_b200.dataset import DatasetError, FrameDataset
+    _, ds = synth.synth_scene(4, 6, 2, 200, tmp_path / "ds", width=40, height=32)
+    pre = FrameDataset(tmp_path / "ds", max_cached_frames=1)
+    keys = [(f, v) for f in range(6) for v in range(2)]
+    pre.prefetch(keys + [(99, 0)])
+    for f, v in keys:
+        got = pre.device_frame(f, v).cpu().numpy()
+        assert np.array_equal(got, ds.load_u8(f, v))
+    with pytest.raises(DatasetError):
+        pre.device_frame(99, 0)
+    cfg = T.TrainConfig(swin_size=2, num_gs=100, genesis_iterations=6, window_iterations=4,
+                        relocate_period=5, rng_seed=1, max_cached_frames=4)
+    small = FrameDataset(tmp_path / "ds", max_cached_frames=1, gpu_cache_frames=1)
+    T.train_video(small, cfg, tmp_path / "a.swin", deterministic=True)
+    big = FrameDataset(tmp_path / "ds", max_cached_frames=1000)
+    T.train_video(big, cfg, tmp_path / "b.swin", deterministic=True)
+    assert (tmp_path / "a.swin").read_bytes() == (tmp_path / "b.swin").read_bytes()
+
+
+def test_failure_leaves_partial_container(T, tmp_path):
+    """A DatasetError mid-training leaves a container without end marker
+    (test_trainer.py:514-522)."""
+    from paper_2409_07759_b200 import synth
+    from paper_2409_07759_b200.codec import ContainerReader
+    _, ds = synth.synth_scene(7, 6, 1, 10, tmp_path / "ds", width=16, height=16)
+    cfg = T.TrainConfig(swin_size=2, num_gs=20, genesis_iterations=3, window_iterations=2,
+                        relocate_period=1000, rng_seed=0, max_cached_frames=4)
+    ds.total_frames = 99
+    with pytest.raises(Exception):
+        T.train_video(ds, cfg, tmp_path / "broken.swin")
+    r = ContainerReader(tmp_path / "broken.swin")
+    assert not r.complete
+    r.close()
+
+
+def test_train_video_schedule_and_counts(T, tmp_path):
+    """Schedule simulation and count conservation on the GPU trainer
+    (test_trainer.py:454-495)."""
+    from paper_2409_07759_b200 import synth
+    from paper_2409_07759_b200.codec import ContainerReader
+    _, ds = synth.synth_scene(2, 7, 1, 10, tmp_path / "ds", width=16, height=16)
+    cfg = T.TrainConfig(swin_size=3, num_gs=30, genesis_iterations=3, window_iterations=2,
+                        relocate_period=1000, rng_seed=0, max_cached_frames=4)
+    res = T.train_video(ds, cfg, tmp_path / "c.swin", keep_archive=True)
+    exp = list(range(1, 7 - 1 + 3))
+    assert [e.target_frame for e in res.emitted[3:]] == exp
+    assert [e.slot for e in res.emitted[3:]] == [t % 3 for t in exp]
+    assert [e.slot for e in res.emitted[:3]] == [0, 1, 2]
+    for frame in range(7):
+        assert sum(len(m.arrays) for m in res.archive
+                   if m.lifespan.start <= frame < m.lifespan.expire) == 30
+    with ContainerReader(res.container_path) as r:
+        assert r.complete
+        recs = sum(int(g.valid.sum()) for g in r.all_generations())
+        assert recs == 30 + (7 - 1) * 10 + (3 - 1) * 10
