@@ -107,13 +107,13 @@ int ss_compact_active(const int32_t* row_start, const int32_t* row_expire, int64
  * rec_b = (k inv2, log2 alpha, r, g), rec_c = b (float32, rounded once from fp64;
  * k = -log2(e)/2 so alpha exp(-m/2) = 2^(k m + log2 alpha));
  * depth_key = fp64 z bits (UINT64_MAX when culled); bbox = (x0,x1,y0,y1)
- * pixels, half open; geom = (u, v, inv0, inv1, inv2, 1/inv0, 1/inv2) fp64
- * (n x 7); n_tiles = 16x16 tiles of the bbox that the maha <= 64 ellipse
+ * pixels, half open; geom = (u, v, inv0, inv1, inv2, 1/inv0, 1/inv2, 0) fp32
+ * (n x 8); n_tiles = 16x16 tiles of the bbox that the maha <= 64 ellipse
  * reaches (exact ellipse-vs-tile test; 0 when culled); tile_mask = kept bits
  * of the first 64 bbox tiles (row-major). */
 int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_t n, const ss_camera* cam,
                    void* rec_a, void* rec_b, float* rec_c, uint64_t* depth_key, int32_t* bbox,
-                   int32_t* n_tiles, double* geom, uint64_t* tile_mask, ss_stream_t stream);
+                   int32_t* n_tiles, float* geom, uint64_t* tile_mask, ss_stream_t stream);
 
 /* ---- a-4 binning: raster.py:153 global (z, src) order reproduced per tile.
  * (1) stable radix sort of the 64-bit depth keys -> order (rank -> i);
@@ -128,7 +128,7 @@ int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* order, void* w
 int ss_tile_offsets(const int32_t* order, const int32_t* n_tiles, int32_t n, int32_t* offsets,
                     void* ws, size_t ws_bytes, ss_stream_t stream);
 int ss_emit_tile_pairs(const int32_t* order, const int32_t* offsets, const int32_t* bbox,
-                       const double* geom, const uint64_t* tile_mask, int32_t n,
+                       const float* geom, const uint64_t* tile_mask, int32_t n,
                        int32_t tiles_x, uint32_t* keys, int32_t* vals, ss_stream_t stream);
 /* *out_sel (HOST int) = 0 when the sorted pairs are in keys/vals, 1 when in
  * keys_alt/vals_alt. */
@@ -163,7 +163,7 @@ int ss_raster_bwd_deterministic(const int32_t* ranges, const int32_t* vals, cons
                                 int32_t height, const int32_t* tile_order, const float* dimg,
                                 const float* t_final, const int32_t* n_contrib,
                                 const int32_t* order, const int32_t* offsets, const int32_t* bbox,
-                                const uint64_t* tile_mask, const double* geom, int32_t n,
+                                const uint64_t* tile_mask, const float* geom, int32_t n,
                                 int32_t* rank, float* partial, float* g2d, ss_stream_t stream);
 
 /* Tuning knob: pixels per lane in the raster kernels (2, 4 or 8); a warp
@@ -245,7 +245,7 @@ typedef struct {
   uint64_t* depth_key;
   int32_t* bbox;        /* int4 x n                                      */
   int32_t* n_tiles;
-  double* geom;         /* 7 x n                                         */
+  float* geom;          /* 8 x n                                         */
   uint64_t* tile_mask;
   int32_t* order;
   int32_t* offsets;     /* n + 1                                         */

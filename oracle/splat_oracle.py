@@ -625,40 +625,43 @@ def relocate(params_list, m_list, v_list, threshold, uniforms):
 # exact ellipse-vs-tile culling (build refinement of a-4; no pixel changes)
 # --------------------------------------------------------------------------
 
-CULL_MARGIN = 64.0 * (1.0 + 1e-9)
+CULL_MARGIN = np.float32(64.0625)
+_F = np.float32
 
 
-def tile_min_maha(i0, i1, i2, u, v, X0, X1, Y0, Y1, r0=None, r2=None):
+def tile_min_maha(i0, i1, i2, u, v, X0, X1, Y0, Y1):
     """Minimum over the continuous rectangle [X0, X1] x [Y0, Y1] (pixel-centre
     coordinates) of m = i0 dx^2 + 2 i1 dx dy + i2 dy^2, dx = x - u, dy = y - v.
-    Vectorised restatement of project.cu tile_min_maha (same operation order).
-    A tile whose minimum exceeds CULL_MARGIN holds no pixel the reference's
-    loop would blend (maha > 64 skip, _kernels.py:39-41)."""
-    r0 = 1.0 / i0 if r0 is None else r0
-    r2 = 1.0 / i2 if r2 is None else r2
-    ax, bx = X0 - u, X1 - u
-    ay, by = Y0 - v, Y1 - v
-    inside = (ax <= 0.0) & (bx >= 0.0) & (ay <= 0.0) & (by >= 0.0)
+    float32 restatement of ss_common.cuh tile_keeps (same rounded operation
+    sequence, numpy float32 = IEEE single without FMA).  A tile whose minimum
+    exceeds CULL_MARGIN holds no pixel the reference's loop would blend
+    (maha > 64 skip, _kernels.py:39-41)."""
+    i0, i1, i2, u, v = (np.asarray(a, dtype=np.float64).astype(_F) for a in (i0, i1, i2, u, v))
+    r0 = _F(1) / i0
+    r2 = _F(1) / i2
+    ax, bx = np.asarray(X0).astype(_F) - u, np.asarray(X1).astype(_F) - u
+    ay, by = np.asarray(Y0).astype(_F) - v, np.asarray(Y1).astype(_F) - v
+    inside = (ax <= 0) & (bx >= 0) & (ay <= 0) & (by >= 0)
 
     def q(dx, dy):
-        return (i0 * dx) * dx + ((2.0 * i1) * dx) * dy + (i2 * dy) * dy
+        return ((i0 * dx) * dx + ((_F(2) * i1) * dx) * dy) + (i2 * dy) * dy
 
-    best = np.full(np.shape(u), np.inf)
+    best = np.full(np.shape(u), np.inf, dtype=_F)
     for ex in (ax, bx):          # vertical edges: dx fixed, minimise over dy
         dy = np.clip(-(i1 * ex) * r2, ay, by)
         best = np.minimum(best, q(ex, dy))
     for ey in (ay, by):          # horizontal edges: dy fixed, minimise over dx
         dx = np.clip(-(i1 * ey) * r0, ax, bx)
         best = np.minimum(best, q(dx, ey))
-    return np.where(inside, 0.0, best)
+    return np.where(inside, _F(0), best)
 
 
 def tile_keep_mask(cache, owner, tx, ty, tile=TILE):
     x0, x1, y0, y1 = cache["bbox"]
     i0, i1, i2 = cache["inv2d"][owner].T
     u, v = cache["mean2d"][owner].T
-    X0 = np.maximum(tx * tile, x0[owner]).astype(np.float64)
-    X1 = np.minimum(tx * tile + tile - 1, x1[owner] - 1).astype(np.float64)
-    Y0 = np.maximum(ty * tile, y0[owner]).astype(np.float64)
-    Y1 = np.minimum(ty * tile + tile - 1, y1[owner] - 1).astype(np.float64)
+    X0 = np.maximum(tx * tile, x0[owner])
+    X1 = np.minimum(tx * tile + tile - 1, x1[owner] - 1)
+    Y0 = np.maximum(ty * tile, y0[owner])
+    Y1 = np.minimum(ty * tile + tile - 1, y1[owner] - 1)
     return tile_min_maha(i0, i1, i2, u, v, X0, X1, Y0, Y1) <= CULL_MARGIN

@@ -32,7 +32,7 @@ __global__ void gather_counts_kernel(const int32_t* __restrict__ order,
 // write its run [offsets[k], offsets[k+1]) of (tile id, splat) pairs.
 __global__ void emit_pairs_kernel(const int32_t* __restrict__ order,
                                   const int32_t* __restrict__ offsets,
-                                  const int4* __restrict__ bbox, const double* __restrict__ geom,
+                                  const int4* __restrict__ bbox, const float* __restrict__ geom,
                                   const uint64_t* __restrict__ tile_mask, int32_t n,
                                   int32_t tiles_x, uint32_t* __restrict__ keys,
                                   int32_t* __restrict__ vals) {
@@ -56,7 +56,7 @@ __global__ void emit_pairs_kernel(const int32_t* __restrict__ order,
     ++off;
   }
   if (total > 64) {
-    double gl[kGeom];
+    float gl[kGeom];
 #pragma unroll
     for (int c = 0; c < kGeom; ++c) gl[c] = geom[(int64_t)i * kGeom + c];
     for (int j = 64; j < total; ++j) {
@@ -161,7 +161,7 @@ extern "C" int ss_tile_offsets(const int32_t* order, const int32_t* n_tiles, int
 }
 
 extern "C" int ss_emit_tile_pairs(const int32_t* order, const int32_t* offsets,
-                                  const int32_t* bbox, const double* geom,
+                                  const int32_t* bbox, const float* geom,
                                   const uint64_t* tile_mask, int32_t n, int32_t tiles_x,
                                   uint32_t* keys, int32_t* vals, cudaStream_t stream) {
   if (n < 0 || tiles_x <= 0) return set_error(SS_ERR_INVALID, "ss_emit_tile_pairs: bad sizes");

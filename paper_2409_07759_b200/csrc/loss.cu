@@ -40,7 +40,28 @@ __device__ __forceinline__ constexpr float win(int t) {
 
 __device__ __forceinline__ float gt_value(const uint8_t* gt_u8, const float* lut,
                                           const float* gt_f32, int64_t idx) {
-  return gt_u8 ? __ldg(lut + gt_u8[idx]) : gt_f32[idx];
+  return gt_u8 ? lut[gt_u8[idx]] : gt_f32[idx];
+}
+
+// Loads the (42 x 42) halo region of all three channels of x and y, row by
+// row as contiguous 3-channel runs (coalesced), zero outside the image.
+__device__ __forceinline__ void load_region3(const float* __restrict__ pred,
+                                             const uint8_t* __restrict__ gt_u8,
+                                             const float* s_lut, const float* __restrict__ gt_f32,
+                                             int W, int H, int x0, int y0, float* s_x3, float* s_y3) {
+  constexpr int kRow = 3 * 42;
+  for (int idx = threadIdx.x; idx < 42 * kRow; idx += blockDim.x) {
+    const int r = idx / kRow, q = idx % kRow;
+    const int gy = y0 - 5 + r, gx = x0 - 5 + q / 3;
+    float xv = 0.f, yv = 0.f;
+    if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+      const int64_t e = ((int64_t)gy * W + (x0 - 5)) * 3 + q;
+      xv = pred[e];
+      yv = gt_u8 ? s_lut[gt_u8[e]] : gt_f32[e];
+    }
+    s_x3[idx] = xv;
+    s_y3[idx] = yv;
+  }
 }
 
 struct LossArgs {
@@ -108,32 +129,25 @@ __device__ __forceinline__ void hblur(const float (*v)[kLT][kLP], int r, int c0,
 }
 
 __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
-  __shared__ float s_x[kLR][kLP];
-  __shared__ float s_y[kLR][kLP];
-  __shared__ float s_v[5][kLT][kLP];
+  extern __shared__ float smem[];
+  float* s_x3 = smem;                      // 42 x 126 (3 interleaved channels)
+  float* s_y3 = s_x3 + kLR * 3 * kLR;
+  float (*s_v)[kLT][kLP] = reinterpret_cast<float (*)[kLT][kLP]>(s_y3 + kLR * 3 * kLR);
+  float* s_lut = reinterpret_cast<float*>(s_v + 5);
   __shared__ double s_red[2][kLossThreads / 32];
   const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
   const int W = a.width, H = a.height;
   const int64_t plane = (int64_t)W * H;
+  if (a.gt_u8)
+    for (int i = threadIdx.x; i < 256; i += kLossThreads) s_lut[i] = a.lut[i];
+  __syncthreads();
+  load_region3(a.pred, a.gt_u8, s_lut, a.gt_f32, W, H, x0, y0, s_x3, s_y3);
   double l1 = 0.0, ss = 0.0;
   for (int ch = 0; ch < 3; ++ch) {
     __syncthreads();
-    for (int idx = threadIdx.x; idx < kLR * kLR; idx += kLossThreads) {
-      const int r = idx / kLR, q = idx % kLR;
-      const int gy = y0 - kHalo + r, gx = x0 - kHalo + q;
-      float xv = 0.f, yv = 0.f;
-      if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-        const int64_t e = ((int64_t)gy * W + gx) * 3 + ch;
-        xv = a.pred[e];
-        yv = gt_value(a.gt_u8, a.lut, a.gt_f32, e);
-      }
-      s_x[r][q] = xv;
-      s_y[r][q] = yv;
-    }
-    __syncthreads();
     // vertical pass (axis 0, loss.py:31) of x, y, xx, xy, yy
     vblur<5>(s_v, [&](int r, int c, float* v) {
-      const float xv = s_x[r][c], yv = s_y[r][c];
+      const float xv = s_x3[r * 3 * kLR + 3 * c + ch], yv = s_y3[r * 3 * kLR + 3 * c + ch];
       v[0] = xv;
       v[1] = yv;
       v[2] = xv * xv;
@@ -160,17 +174,19 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
         const float a2 = 2.f * sig_xy + C2;
         const float b1 = mu_x * mu_x + mu_y * mu_y + C1;
         const float b2 = sig_x + sig_y + C2;
-        const float denom = b1 * b2;
-        const float s = (a1 * a2) / denom;
-        const float ds_dmu = (2.f * mu_y * (a2 - a1) - 2.f * mu_x * s * (b2 - b1)) / denom;
-        const float ds_dmxx = -s / b2;
-        const float ds_dmxy = 2.f * a1 / denom;
+        const float inv_b2 = 1.f / b2;
+        const float inv_den = inv_b2 / b1;  // 1 / (b1 b2)
+        const float s = (a1 * a2) * inv_den;
+        const float ds_dmu = (2.f * mu_y * (a2 - a1) - 2.f * mu_x * s * (b2 - b1)) * inv_den;
+        const float ds_dmxx = -s * inv_b2;
+        const float ds_dmxy = 2.f * a1 * inv_den;
         const int64_t pix = (int64_t)gy * W + gx;
         a.maps[(0 * 3 + ch) * plane + pix] = ds_dmu;
         a.maps[(1 * 3 + ch) * plane + pix] = ds_dmxx;
         a.maps[(2 * 3 + ch) * plane + pix] = ds_dmxy;
         ss += (double)s;
-        l1 += (double)fabsf(s_x[r + kHalo][c0 + i + kHalo] - s_y[r + kHalo][c0 + i + kHalo]);
+        const int off = (r + kHalo) * 3 * kLR + 3 * (c0 + i + kHalo) + ch;
+        l1 += (double)fabsf(s_x3[off] - s_y3[off]);
       }
     }
   }
@@ -201,6 +217,9 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, floa
                                                                  float* __restrict__ dimg) {
   __shared__ float s_m[3][kLR][kLP];
   __shared__ float s_v[3][kLT][kLP];
+  __shared__ float s_lut[256];
+  if (a.gt_u8)
+    for (int i = threadIdx.x; i < 256; i += kLossThreads) s_lut[i] = a.lut[i];
   const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
   const int W = a.width, H = a.height;
   const int64_t plane = (int64_t)W * H;
@@ -232,7 +251,7 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, floa
       if (gy >= H || gx >= W) continue;
       const int64_t e = ((int64_t)gy * W + gx) * 3 + ch;
       const float x = a.pred[e];
-      const float y = gt_value(a.gt_u8, a.lut, a.gt_f32, e);
+      const float y = gt_value(a.gt_u8, s_lut, a.gt_f32, e);
       const float grad = (bl[0][i] + 2.f * x * bl[1][i] + y * bl[2][i]) * inv_n;
       const float d = x - y;
       const float sgn = (d > 0.f) ? 1.f : ((d < 0.f) ? -1.f : 0.f);
@@ -293,7 +312,14 @@ extern "C" int ss_loss_l1_ssim(const float* pred, const uint8_t* gt_u8, const fl
   const size_t plane = (size_t)width * height;
   LossArgs a{pred, gt_u8, lut, gt_f32, width, height, (float*)ws,
              (double*)((char*)ws + ((9 * plane * sizeof(float) + 255) & ~(size_t)255))};
-  ssim_fwd_kernel<<<grid, kLossThreads, 0, stream>>>(a);
+  const size_t fwd_smem = sizeof(float) * (2 * kLR * 3 * kLR + 5 * kLT * kLP + 256);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ssim_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)fwd_smem);
+    attr = true;
+  }
+  ssim_fwd_kernel<<<grid, kLossThreads, fwd_smem, stream>>>(a);
   ssim_bwd_kernel<<<grid, kLossThreads, 0, stream>>>(a, (float)ssim_weight, dimg);
   loss_reduce_kernel<<<1, 1024, 0, stream>>>(a.partials, grid.x * grid.y, out_sums);
   return check_launch("ss_loss_l1_ssim");

@@ -35,19 +35,22 @@ static HyperK to_hyper(const ss_step_hyper* h) {
   return k;
 }
 
-// Standard normal triple for `row` from Philox (Box-Muller on 32-bit uniforms).
+// Standard normal triple for `row` from Philox (Box-Muller on 32-bit
+// uniforms, evaluated in fp32: the noise sample needs no fp64 precision).
 __device__ __forceinline__ void philox_normal3(const HyperK& h, int64_t row, double out[3]) {
   Philox4 r = philox4x32_10((uint32_t)row, (uint32_t)(row >> 32), h.c0, h.c1, h.k0, h.k1);
-  const double two_pi = 6.283185307179586;
-  const double inv32 = 1.0 / 4294967296.0;
-  const double u1 = ((double)r.v[0] + 1.0) * inv32;  // (0, 1]
-  const double u2 = (double)r.v[1] * inv32;
-  const double u3 = ((double)r.v[2] + 1.0) * inv32;
-  const double u4 = (double)r.v[3] * inv32;
-  const double rad1 = sqrt(-2.0 * log(u1)), rad2 = sqrt(-2.0 * log(u3));
-  out[0] = rad1 * cos(two_pi * u2);
-  out[1] = rad1 * sin(two_pi * u2);
-  out[2] = rad2 * cos(two_pi * u4);
+  const float inv32 = 2.3283064365386963e-10f;  // 2^-32
+  const float u1 = ((float)(r.v[0] >> 8) + 1.0f) * 5.9604644775390625e-08f;  // (0, 1], 24 bits
+  const float u2 = (float)r.v[1] * inv32;
+  const float u3 = ((float)(r.v[2] >> 8) + 1.0f) * 5.9604644775390625e-08f;
+  const float u4 = (float)r.v[3] * inv32;
+  const float rad1 = sqrtf(-2.0f * logf(u1)), rad2 = sqrtf(-2.0f * logf(u3));
+  float s1, c1, s2, c2;
+  sincospif(2.0f * u2, &s1, &c1);
+  sincospif(2.0f * u4, &s2, &c2);
+  out[0] = (double)(rad1 * c1);
+  out[1] = (double)(rad1 * s1);
+  out[2] = (double)(rad2 * c2);
 }
 
 __device__ __forceinline__ double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
@@ -70,7 +73,7 @@ __device__ __forceinline__ void sgld_row(double* p, const HyperK& h, const doubl
   }
 }
 
-__global__ void adam_sgld_kernel(double* __restrict__ opt, const float* __restrict__ grads,
+__global__ void __launch_bounds__(128, 5) adam_sgld_kernel(double* __restrict__ opt, const float* __restrict__ grads,
                                  double* __restrict__ m, double* __restrict__ v, int64_t n_rows,
                                  int32_t rows_per_gen, const ss_gen_step* __restrict__ gens,
                                  HyperK h, const double* __restrict__ eta) {

@@ -108,7 +108,7 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
                                    CamK cam, float4* __restrict__ rec_a,
                                    float4* __restrict__ rec_b, float* __restrict__ rec_c,
                                    uint64_t* __restrict__ depth_key, int4* __restrict__ bbox,
-                                   int32_t* __restrict__ n_tiles, double* __restrict__ geom,
+                                   int32_t* __restrict__ n_tiles, float* __restrict__ geom,
                                    uint64_t* __restrict__ tile_mask) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -138,8 +138,10 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
   const int y0 = (int)fmax(ceil(dsub(p.uy, r8)), 0.0);
   const int y1 = (int)fmin(dadd(floor(dadd(p.uy, r8)), 1.0), (double)cam.height);
   bbox[i] = make_int4(x0, x1, y0, y1);
-  double gl[kGeom] = {p.ux, p.uy, i0, i1, i2, ddiv(1.0, i0), ddiv(1.0, i2)};
-  double* gm = geom + (int64_t)i * kGeom;
+  const float fi0 = __double2float_rn(i0), fi2 = __double2float_rn(i2);
+  float gl[kGeom] = {__double2float_rn(p.ux), __double2float_rn(p.uy), fi0,
+                     __double2float_rn(i1), fi2, __frcp_rn(fi0), __frcp_rn(fi2), 0.0f};
+  float* gm = geom + (int64_t)i * kGeom;
 #pragma unroll
   for (int c = 0; c < kGeom; ++c) gm[c] = gl[c];
   int nt = 0;
@@ -303,7 +305,7 @@ using namespace ss;
 extern "C" int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_t n,
                               const ss_camera* cam, void* rec_a, void* rec_b, float* rec_c,
                               uint64_t* depth_key, int32_t* bbox, int32_t* n_tiles,
-                              double* geom, uint64_t* tile_mask, cudaStream_t stream) {
+                              float* geom, uint64_t* tile_mask, cudaStream_t stream) {
   if (!store || !cam || n < 0) return set_error(SS_ERR_INVALID, "ss_project_fwd: bad arguments");
   if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0) || !(cam->fy > 0))
     return set_error(SS_ERR_INVALID, "ss_project_fwd: bad camera");

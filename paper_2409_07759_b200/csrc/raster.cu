@@ -230,7 +230,7 @@ struct DetArgs {
   const int32_t* offsets;
   const int4* bbox;
   const uint64_t* tile_mask;
-  const double* geom;
+  const float* geom;
 };
 
 __device__ __forceinline__ int64_t emit_position(const DetArgs& d, int g, int tx, int ty) {
@@ -244,7 +244,7 @@ __device__ __forceinline__ int64_t emit_position(const DetArgs& d, int g, int tx
     j = __popcll(mask & ((1ull << local) - 1ull));
   } else {
     j = __popcll(mask);
-    double gl[kGeom];
+    float gl[kGeom];
 #pragma unroll
     for (int c = 0; c < kGeom; ++c) gl[c] = d.geom[(int64_t)g * kGeom + c];
     for (int q = 64; q < local; ++q) j += tile_keeps(gl, tx0 + q % w, ty0 + q / w, bb);
@@ -492,7 +492,7 @@ extern "C" int ss_raster_bwd_deterministic(
     const int32_t* ranges, const int32_t* vals, const void* rec_a, const void* rec_b,
     const float* rec_c, int32_t width, int32_t height, const int32_t* tile_order,
     const float* dimg, const float* t_final, const int32_t* n_contrib, const int32_t* order,
-    const int32_t* offsets, const int32_t* bbox, const uint64_t* tile_mask, const double* geom,
+    const int32_t* offsets, const int32_t* bbox, const uint64_t* tile_mask, const float* geom,
     int32_t n, int32_t* rank, float* partial, float* g2d, cudaStream_t stream) {
   if (n <= 0) return SS_OK;
   rank_kernel<<<grid_for(n, 256), 256, 0, stream>>>(order, n, rank);

@@ -85,36 +85,41 @@ __device__ __forceinline__ void quat_to_rot(const double q[4], double r[3][3]) {
 
 // Exact ellipse-vs-tile test (a-4 refinement): minimum over the continuous
 // rectangle [X0, X1] x [Y0, Y1] of pixel centres of m = i0 dx^2 + 2 i1 dx dy +
-// i2 dy^2.  Same operation order as oracle/splat_oracle.py tile_min_maha, so
-// keep/drop decisions (and therefore tile keys) are bit-identical to it.
-constexpr double kCullMargin = 64.0 * (1.0 + 1e-9);
+// i2 dy^2.  fp32 with every operation explicitly rounded (no FMA
+// contraction), the same sequence as oracle/splat_oracle.py tile_min_maha in
+// numpy float32, so keep/drop decisions (and therefore tile keys) are
+// bit-identical to it.  The margin keeps tiles whose minimum is within
+// 2^-10 relative of 64 (those pixels blend nothing: maha > 64).
+constexpr float kCullMargin = 64.0625f;
+constexpr int kGeom = 8;  // floats per splat: u, v, i0, i1, i2, 1/i0, 1/i2, pad
 
-__device__ __forceinline__ double quad_form(double i0, double i1, double i2, double dx, double dy) {
-  return dadd(dadd(dmul(dmul(i0, dx), dx), dmul(dmul(dmul(2.0, i1), dx), dy)),
-              dmul(dmul(i2, dy), dy));
+__device__ __forceinline__ float fmr(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float far_(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fsr(float a, float b) { return __fsub_rn(a, b); }
+
+__device__ __forceinline__ float quad_form(float i0, float i1, float i2, float dx, float dy) {
+  return far_(far_(fmr(fmr(i0, dx), dx), fmr(fmr(fmr(2.0f, i1), dx), dy)), fmr(fmr(i2, dy), dy));
 }
 
-__device__ __forceinline__ double clampd(double x, double lo, double hi) {
-  return fmin(fmax(x, lo), hi);
+__device__ __forceinline__ float clampf(float x, float lo, float hi) {
+  return fminf(fmaxf(x, lo), hi);
 }
 
-// geom = (u, v, i0, i1, i2, 1/i0, 1/i2) in fp64; bb = pixel bbox (x0, x1, y0, y1)
-__device__ __forceinline__ bool tile_keeps(const double* geom, int tx, int ty, int4 bb) {
-  const double u = geom[0], v = geom[1], i0 = geom[2], i1 = geom[3], i2 = geom[4];
-  const double r0 = geom[5], r2 = geom[6];
-  const double ax = (double)max(tx * SS_TILE, bb.x) - u;
-  const double bx = (double)min(tx * SS_TILE + SS_TILE - 1, bb.y - 1) - u;
-  const double ay = (double)max(ty * SS_TILE, bb.z) - v;
-  const double by = (double)min(ty * SS_TILE + SS_TILE - 1, bb.w - 1) - v;
-  if (ax <= 0.0 && bx >= 0.0 && ay <= 0.0 && by >= 0.0) return true;
-  double best = quad_form(i0, i1, i2, ax, clampd(dmul(-dmul(i1, ax), r2), ay, by));
-  best = fmin(best, quad_form(i0, i1, i2, bx, clampd(dmul(-dmul(i1, bx), r2), ay, by)));
-  best = fmin(best, quad_form(i0, i1, i2, clampd(dmul(-dmul(i1, ay), r0), ax, bx), ay));
-  best = fmin(best, quad_form(i0, i1, i2, clampd(dmul(-dmul(i1, by), r0), ax, bx), by));
+// geom = (u, v, i0, i1, i2, 1/i0, 1/i2) fp32; bb = pixel bbox (x0, x1, y0, y1)
+__device__ __forceinline__ bool tile_keeps(const float* geom, int tx, int ty, int4 bb) {
+  const float u = geom[0], v = geom[1], i0 = geom[2], i1 = geom[3], i2 = geom[4];
+  const float r0 = geom[5], r2 = geom[6];
+  const float ax = fsr((float)max(tx * SS_TILE, bb.x), u);
+  const float bx = fsr((float)min(tx * SS_TILE + SS_TILE - 1, bb.y - 1), u);
+  const float ay = fsr((float)max(ty * SS_TILE, bb.z), v);
+  const float by = fsr((float)min(ty * SS_TILE + SS_TILE - 1, bb.w - 1), v);
+  if (ax <= 0.0f && bx >= 0.0f && ay <= 0.0f && by >= 0.0f) return true;
+  float best = quad_form(i0, i1, i2, ax, clampf(fmr(-fmr(i1, ax), r2), ay, by));
+  best = fminf(best, quad_form(i0, i1, i2, bx, clampf(fmr(-fmr(i1, bx), r2), ay, by)));
+  best = fminf(best, quad_form(i0, i1, i2, clampf(fmr(-fmr(i1, ay), r0), ax, bx), ay));
+  best = fminf(best, quad_form(i0, i1, i2, clampf(fmr(-fmr(i1, by), r0), ax, bx), by));
   return best <= kCullMargin;
 }
-
-constexpr int kGeom = 7;  // doubles per splat in the binning geometry record
 
 // Philox4x32-10 counter-based generator (Salmon et al., SC'11).
 struct Philox4 {

@@ -118,7 +118,7 @@ class ViewPipeline:
         for name, shape, dt in (("rec_a", (nn, 4), torch.float32), ("rec_b", (nn, 4), torch.float32),
                                 ("rec_c", (nn,), torch.float32), ("depth_key", (nn,), torch.int64),
                                 ("bbox", (nn, 4), torch.int32), ("n_tiles", (nn,), torch.int32),
-                                ("geom", (nn, 7), torch.float64), ("tile_mask", (nn,), torch.int64),
+                                ("geom", (nn, 8), torch.float32), ("tile_mask", (nn,), torch.int64),
                                 ("order", (nn,), torch.int32), ("offsets", (nn + 1,), torch.int32),
                                 ("ranges", (n_tiles, 2), torch.int32),
                                 ("tile_order", (n_tiles,), torch.int32),
