@@ -19,6 +19,43 @@ __global__ void iota_kernel(int32_t* v, int32_t n) {
   if (i < n) v[i] = i;
 }
 
+__global__ void high_keys_kernel(const uint64_t* __restrict__ key64, int32_t n,
+                                 uint32_t* __restrict__ hi, int32_t* __restrict__ vals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  hi[i] = (uint32_t)(key64[i] >> 32);
+  vals[i] = i;
+}
+
+// After a stable sort on the high 32 bits, each run of equal high keys is
+// re-sorted by (full 64-bit key, index) -- an insertion sort from the run's
+// first position (runs are a few elements; equal full keys stay in index
+// order, so long runs of identical depths cost O(run)).
+__global__ void fix_runs_kernel(const uint32_t* __restrict__ hi_sorted,
+                                const uint64_t* __restrict__ key64, int32_t n,
+                                int32_t* __restrict__ order) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t h = hi_sorted[p];
+  if (p > 0 && hi_sorted[p - 1] == h) return;          // not a run start
+  if (p + 1 >= n || hi_sorted[p + 1] != h) return;      // singleton run
+  int q = p + 1;
+  while (q < n && hi_sorted[q] == h) ++q;
+  for (int a = p + 1; a < q; ++a) {
+    const int32_t v = order[a];
+    const uint64_t kv = key64[v];
+    int b = a - 1;
+    while (b >= p) {
+      const int32_t w = order[b];
+      const uint64_t kw = key64[w];
+      if (kw < kv || (kw == kv && w < v)) break;
+      order[b + 1] = w;
+      --b;
+    }
+    order[b + 1] = v;
+  }
+}
+
 __global__ void gather_counts_kernel(const int32_t* __restrict__ order,
                                      const int32_t* __restrict__ n_tiles, int32_t n,
                                      int32_t* __restrict__ out) {
@@ -127,21 +164,24 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
   if (n == 0) return SS_OK;
   if (ws_bytes < ss_binning_workspace_bytes(n, 1, 1))
     return set_error(SS_ERR_WORKSPACE, "ss_depth_order: workspace too small");
+  // stable radix sort of the high 32 key bits (4 passes instead of 8), then a
+  // fix-up of equal-high-key runs on the exact 64-bit keys: the result is the
+  // stable 64-bit order, i.e. np.lexsort((src, z)) (raster.py:153)
   char* w = (char*)ws;
   const size_t nn = (size_t)n;
   const size_t tb = align256(cub_bytes(n, 1));
-  uint64_t* keys_a = (uint64_t*)(w + tb + align256((nn + 1) * 4));
-  uint64_t* keys_b = (uint64_t*)((char*)keys_a + align256(nn * 8));
-  int32_t* vals_in = (int32_t*)((char*)keys_b + align256(nn * 8));
-  cudaMemcpyAsync(keys_a, depth_key, nn * 8, cudaMemcpyDeviceToDevice, stream);
-  iota_kernel<<<grid_for(n, 256), 256, 0, stream>>>(vals_in, n);
-  cub::DoubleBuffer<uint64_t> dk(keys_a, keys_b);
+  uint32_t* hi_a = (uint32_t*)(w + tb + align256((nn + 1) * 4));
+  uint32_t* hi_b = (uint32_t*)((char*)hi_a + align256(nn * 8));
+  int32_t* vals_in = (int32_t*)((char*)hi_a + 2 * align256(nn * 8));
+  high_keys_kernel<<<grid_for(n, 256), 256, 0, stream>>>(depth_key, n, hi_a, vals_in);
+  cub::DoubleBuffer<uint32_t> dk(hi_a, hi_b);
   cub::DoubleBuffer<int32_t> dv(vals_in, order);
   size_t tmp_bytes = tb;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(w, tmp_bytes, dk, dv, n, 0, 64, stream);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(w, tmp_bytes, dk, dv, n, 0, 32, stream);
   if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_depth_order: %s", cudaGetErrorString(e));
   if (dv.Current() != order)
     cudaMemcpyAsync(order, dv.Current(), nn * 4, cudaMemcpyDeviceToDevice, stream);
+  fix_runs_kernel<<<grid_for(n, 256), 256, 0, stream>>>(dk.Current(), depth_key, n, order);
   return check_launch("ss_depth_order");
 }
 
@@ -202,42 +242,44 @@ extern "C" int ss_tile_ranges(const uint32_t* sorted_keys, int64_t n_pairs, int3
   return check_launch("ss_tile_ranges");
 }
 
-// Longest-first tile order in one CTA: bitonic sort of (maxlen - len) << 13 | tile
-// over up to 8192 tiles in shared memory (ties by tile id).
-constexpr int kOrderMax = 8192;
+// Longest-first tile order in one CTA: counting sort of the tiles by a
+// length bucket (4 buckets per octave, longest first).  Only the launch
+// order depends on it (each tile's work is independent), so ties within a
+// bucket need no fixed order.
+constexpr int kOrderMax = 1 << 20;
+constexpr int kBuckets = 128;
 
-__global__ void __launch_bounds__(1024) tile_order_bitonic_kernel(const int2* __restrict__ ranges,
-                                                                  int n_tiles,
-                                                                  int32_t* __restrict__ out) {
-  __shared__ uint32_t key[kOrderMax];
-  int n2 = 1;
-  while (n2 < n_tiles) n2 <<= 1;
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    if (i < n_tiles) {
-      const int2 r = ranges[i];
-      const uint32_t len = (uint32_t)min(r.y - r.x, (1 << 18) - 1);
-      key[i] = (((1u << 18) - 1 - len) << 13) | (uint32_t)i;
-    } else {
-      key[i] = 0xffffffffu;
+__device__ __forceinline__ int len_bucket(int len) {
+  // 4 * log2(len + 1) without a log: exponent and the top two mantissa bits
+  const float f = (float)(len + 1);
+  const int b = ((__float_as_int(f) >> 21) - (127 << 2));  // 4 * floor-ish(log2)
+  return kBuckets - 1 - min(max(b, 0), kBuckets - 1);
+}
+
+__global__ void __launch_bounds__(1024) tile_order_bucket_kernel(const int2* __restrict__ ranges,
+                                                                 int n_tiles,
+                                                                 int32_t* __restrict__ out) {
+  __shared__ int hist[kBuckets];
+  __shared__ int cursor[kBuckets];
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const int2 r = ranges[t];
+    atomicAdd(&hist[len_bucket(r.y - r.x)], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < kBuckets; ++b) {
+      cursor[b] = acc;
+      acc += hist[b];
     }
   }
   __syncthreads();
-  for (int size = 2; size <= n2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
-        const int lo = 2 * i - (i & (stride - 1));
-        const int hi = lo + stride;
-        const bool asc = (lo & size) == 0;
-        const uint32_t a = key[lo], b = key[hi];
-        if ((a > b) == asc) {
-          key[lo] = b;
-          key[hi] = a;
-        }
-      }
-      __syncthreads();
-    }
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const int2 r = ranges[t];
+    out[atomicAdd(&cursor[len_bucket(r.y - r.x)], 1)] = t;
   }
-  for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) out[i] = (int32_t)(key[i] & 0x1fffu);
 }
 
 static size_t tile_order_cub_bytes(int32_t n_tiles) {
@@ -257,7 +299,7 @@ extern "C" int ss_tile_order(const int32_t* ranges, int32_t n_tiles, int32_t* ti
                              void* ws, size_t ws_bytes, cudaStream_t stream) {
   if (n_tiles <= 0) return set_error(SS_ERR_INVALID, "ss_tile_order: n_tiles <= 0");
   if (n_tiles <= kOrderMax) {
-    tile_order_bitonic_kernel<<<1, 1024, 0, stream>>>((const int2*)ranges, n_tiles, tile_order);
+    tile_order_bucket_kernel<<<1, 1024, 0, stream>>>((const int2*)ranges, n_tiles, tile_order);
     return check_launch("ss_tile_order");
   }
   if (ws_bytes < ss_tile_order_workspace_bytes(n_tiles))

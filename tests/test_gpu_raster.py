@@ -303,3 +303,29 @@ def test_deterministic_backward_bit_identical(ss):
     grad_check(g1, gref, what="deterministic")
     ga = R.render_arrays_backward(cam, arr, gdir)
     grad_check(ga, g1, tol=1e-5, what="atomic vs deterministic")
+
+
+def test_depth_order_exact_on_adversarial_keys():
+    """ss_depth_order (32-bit high-key radix sort + run fix-up) equals the
+    stable 64-bit order, i.e. np.lexsort((index, z)) (raster.py:153): depths
+    sharing their high 32 bits, exact ties, culled keys, long runs."""
+    import torch
+    from paper_2409_07759_b200 import _lib as L
+    rng = np.random.default_rng(0)
+    n = 200_000
+    z = rng.uniform(2.0, 3.0, n)
+    z[:50_000] = 2.5 + rng.integers(0, 1000, 50_000) * 2.0 ** -44   # same high bits
+    z[50_000:60_000] = 2.75                                          # exact ties
+    z[60_000:61_000] = 2.75 + np.arange(1000)[::-1] * 2.0 ** -50     # long reversed run
+    keys = z.view(np.uint64).copy()
+    keys[rng.choice(n, 5000, replace=False)] = np.uint64(0xFFFFFFFFFFFFFFFF)  # culled
+    perm = rng.permutation(n)
+    keys = keys[perm]
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    order = torch.empty(n, dtype=torch.int32, device="cuda")
+    lib = L.lib()
+    ws = torch.empty(int(lib.ss_binning_workspace_bytes(n, 1, 1)), dtype=torch.uint8, device="cuda")
+    L.check(lib.ss_depth_order(L.ptr(kt), n, L.ptr(order), L.ptr(ws), ws.numel(),
+                               L.stream_ptr()), "depth_order")
+    ref = np.lexsort((np.arange(n), keys))
+    assert np.array_equal(order.cpu().numpy(), ref)
