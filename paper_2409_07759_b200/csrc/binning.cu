@@ -28,12 +28,17 @@ __global__ void high_keys_kernel(const uint64_t* __restrict__ key64, int32_t n,
 }
 
 // After a stable sort on the high 32 bits, each run of equal high keys is
-// re-sorted by (full 64-bit key, index) -- an insertion sort from the run's
-// first position (runs are a few elements; equal full keys stay in index
-// order, so long runs of identical depths cost O(run)).
+// re-sorted by (full 64-bit key, index).  Runs of <= 32 (the usual case: a
+// few splats per 2^-20 relative depth) take a per-thread insertion sort; longer
+// runs are queued for long_runs_kernel (one CTA per run, bitonic sort of
+// (low 32 key bits, position in run) -- positions keep it stable).
+constexpr int kShortRun = 32;
+constexpr int kSmemRun = 8192;
+
 __global__ void fix_runs_kernel(const uint32_t* __restrict__ hi_sorted,
                                 const uint64_t* __restrict__ key64, int32_t n,
-                                int32_t* __restrict__ order) {
+                                int32_t* __restrict__ order, int2* __restrict__ long_runs,
+                                int32_t* __restrict__ n_long) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const uint32_t h = hi_sorted[p];
@@ -41,6 +46,10 @@ __global__ void fix_runs_kernel(const uint32_t* __restrict__ hi_sorted,
   if (p + 1 >= n || hi_sorted[p + 1] != h) return;      // singleton run
   int q = p + 1;
   while (q < n && hi_sorted[q] == h) ++q;
+  if (q - p > kShortRun) {
+    long_runs[atomicAdd(n_long, 1)] = make_int2(p, q);
+    return;
+  }
   for (int a = p + 1; a < q; ++a) {
     const int32_t v = order[a];
     const uint64_t kv = key64[v];
@@ -53,6 +62,49 @@ __global__ void fix_runs_kernel(const uint32_t* __restrict__ hi_sorted,
       --b;
     }
     order[b + 1] = v;
+  }
+}
+
+// Bitonic sort of n2 (power of two) 64-bit keys in `a` by one CTA.
+__device__ void cta_bitonic(uint64_t* a, int n2) {
+  for (int size = 2; size <= n2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const uint64_t x = a[lo], y = a[hi];
+        if ((x > y) == asc) {
+          a[lo] = y;
+          a[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(1024) long_runs_kernel(const uint64_t* __restrict__ key64,
+                                                         int32_t* __restrict__ order,
+                                                         const int2* __restrict__ long_runs,
+                                                         const int32_t* __restrict__ n_long,
+                                                         uint64_t* __restrict__ scratch,
+                                                         int32_t* __restrict__ tmp) {
+  extern __shared__ uint64_t s_keys[];
+  for (int r = blockIdx.x; r < *n_long; r += gridDim.x) {
+    const int2 run = long_runs[r];
+    const int L = run.y - run.x;
+    int n2 = 1;
+    while (n2 < L) n2 <<= 1;
+    // long runs use a private slice of the scratch buffer at the run's offset
+    uint64_t* a = n2 <= kSmemRun ? s_keys : scratch + 2 * (int64_t)run.x;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x)
+      a[i] = i < L ? (((uint64_t)(uint32_t)key64[order[run.x + i]]) << 32) | (uint32_t)i : ~0ull;
+    __syncthreads();
+    cta_bitonic(a, n2);
+    for (int i = threadIdx.x; i < L; i += blockDim.x) tmp[run.x + i] = order[run.x + (int)(a[i] & 0xffffffffu)];
+    __syncthreads();
+    for (int i = threadIdx.x; i < L; i += blockDim.x) order[run.x + i] = tmp[run.x + i];
+    __syncthreads();
   }
 }
 
@@ -154,8 +206,9 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 extern "C" size_t ss_binning_workspace_bytes(int32_t n, int64_t max_pairs, int32_t n_tiles) {
   (void)n_tiles;
   size_t nn = (size_t)(n > 0 ? n : 1);
+  // [cub temp | n+1 int32 | n u64 | n u64 | n int32 | 4n u64 (long-run bitonic scratch)]
   return align256(cub_bytes(n, max_pairs)) + align256((nn + 1) * 4) + 2 * align256(nn * 8) +
-         align256(nn * 4) + 1024;
+         align256(nn * 4) + align256(4 * nn * 8) + 1024;
 }
 
 extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* order, void* ws,
@@ -170,9 +223,13 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
   char* w = (char*)ws;
   const size_t nn = (size_t)n;
   const size_t tb = align256(cub_bytes(n, 1));
-  uint32_t* hi_a = (uint32_t*)(w + tb + align256((nn + 1) * 4));
-  uint32_t* hi_b = (uint32_t*)((char*)hi_a + align256(nn * 8));
-  int32_t* vals_in = (int32_t*)((char*)hi_a + 2 * align256(nn * 8));
+  // workspace regions (see ss_binning_workspace_bytes): [cub | n+1 int32 | 2 x n u64 | n int32 | ...]
+  int32_t* scratch32 = (int32_t*)(w + tb);
+  uint64_t* u64a = (uint64_t*)((char*)scratch32 + align256((nn + 1) * 4));
+  uint64_t* u64b = (uint64_t*)((char*)u64a + align256(nn * 8));
+  int32_t* vals_in = (int32_t*)((char*)u64b + align256(nn * 8));
+  uint32_t* hi_a = (uint32_t*)u64a;
+  uint32_t* hi_b = hi_a + nn;  // both high-key buffers fit in region u64a
   high_keys_kernel<<<grid_for(n, 256), 256, 0, stream>>>(depth_key, n, hi_a, vals_in);
   cub::DoubleBuffer<uint32_t> dk(hi_a, hi_b);
   cub::DoubleBuffer<int32_t> dv(vals_in, order);
@@ -181,7 +238,23 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
   if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_depth_order: %s", cudaGetErrorString(e));
   if (dv.Current() != order)
     cudaMemcpyAsync(order, dv.Current(), nn * 4, cudaMemcpyDeviceToDevice, stream);
-  fix_runs_kernel<<<grid_for(n, 256), 256, 0, stream>>>(dk.Current(), depth_key, n, order);
+  // long-run list in region u64b (int2 per potential run start), its count in scratch32[0]
+  int2* long_runs = (int2*)u64b;
+  cudaMemsetAsync(scratch32, 0, sizeof(int32_t), stream);
+  fix_runs_kernel<<<grid_for(n, 256), 256, 0, stream>>>(dk.Current(), depth_key, n, order,
+                                                         long_runs, scratch32);
+  // long runs: a run of length L >= 33 sorts in place via the vals_in region
+  // (tmp) and, beyond kSmemRun, the u64 region after it (scratch, 2x run.x
+  // offset keeps runs disjoint: next_pow2(L) <= 2 L)
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(long_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemRun * 8);
+    attr = true;
+  }
+  long_runs_kernel<<<64, 1024, kSmemRun * 8, stream>>>(depth_key, order, long_runs, scratch32,
+                                                        (uint64_t*)((char*)vals_in + align256(nn * 4)),
+                                                        vals_in);
   return check_launch("ss_depth_order");
 }
 

@@ -44,12 +44,21 @@ def main():
         else:
             cur_e = max(cur_e, e)
     busy += cur_e - cur_s
+    gaps = collections.Counter()
+    prev_end = spans[0][1]
+    prev_name = spans[0][2]
+    for s_, e_, n_ in spans[1:]:
+        if s_ > prev_end:
+            gaps[(prev_name.split("(")[0][:40] + " -> " + n_.split("(")[0][:40])] += s_ - prev_end
+        if e_ > prev_end:
+            prev_end, prev_name = e_, n_
     by = collections.Counter()
     for s, e, n in spans:
         by[n.split("(")[0][:60]] += e - s
     out = {"steps": a.steps, "span_us_per_step": (t1 - t0) / a.steps,
            "gpu_busy_us_per_step": busy / a.steps,
            "idle_us_per_step": (t1 - t0 - busy) / a.steps,
+           "gaps_us_per_step": {k: v / a.steps for k, v in gaps.most_common(12)},
            "kernels_us_per_step": {k: v / a.steps for k, v in by.most_common(25)}}
     print(json.dumps(out, indent=1))
 
