@@ -137,6 +137,26 @@ int ss_sort_tile_pairs(uint32_t* keys, int32_t* vals, uint32_t* keys_alt, int32_
                        size_t ws_bytes, ss_stream_t stream);
 int ss_tile_ranges(const uint32_t* sorted_keys, int64_t n_pairs, int32_t n_tiles,
                    int32_t* ranges, ss_stream_t stream);
+/* Chunked binning (ss_render_fwd's default): builds the same per-tile lists
+ * as emit -> stable pair sort -> ranges.  The rank range is cut into chunks
+ * of ~8k pairs; per chunk, pairs are emitted (tile id u16 in keys, splat id in
+ * vals, at emit positions) with a tile histogram; histograms are scanned
+ * over chunks and tiles (-> ranges); then each chunk's pairs are written,
+ * in emit order, to vals_out at their tile's slots.
+ * offsets = ss_tile_offsets' output, n_pairs = K = offsets[n].  Usable when
+ * ss_bin_tiles_supported(K, tiles) (shared-memory cursors: <= 18432 tiles). */
+size_t ss_bin_tiles_workspace_bytes(int64_t n_pairs, int32_t n_tiles);
+int32_t ss_bin_tiles_supported(int64_t n_pairs, int32_t n_tiles);
+int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const int32_t* bbox,
+                 const float* geom, const uint64_t* tile_mask, int32_t n, int64_t n_pairs,
+                 int32_t tiles_x, int32_t tiles_y, uint16_t* keys, int32_t* vals,
+                 int32_t* vals_out, int32_t* ranges, void* ws, size_t ws_bytes,
+                 ss_stream_t stream);
+/* Binning used by ss_render_fwd: 0 = ss_bin_tiles (default), 1 = emit +
+ * radix pair sort + ranges (kept as a cross-check; keys are only written here). */
+int ss_set_binning(int32_t mode);
+int ss_get_binning(void);
+
 /* Tiles ordered by list length, longest first (raster scheduling order:
  * longest-processing-time-first across the SMs).  ws >= ss_tile_order_workspace_bytes. */
 size_t ss_tile_order_workspace_bytes(int32_t n_tiles);

@@ -76,6 +76,11 @@ _SIGNATURES = {
     "ss_raster_fwd": ([P, P, P, P, P, I32, I32, P, P, P, P, P], c_int),
     "ss_raster_bwd": ([P, P, P, P, P, I32, I32, P, P, P, P, P, P], c_int),
     "ss_set_raster_strip": ([I32], c_int),
+    "ss_set_binning": ([I32], c_int),
+    "ss_get_binning": ([], c_int),
+    "ss_bin_tiles_workspace_bytes": ([I64, I32], c_size_t),
+    "ss_bin_tiles_supported": ([I64, I32], I32),
+    "ss_bin_tiles": ([P, P, P, P, P, I32, I64, I32, I32, P, P, P, P, P, c_size_t, P], c_int),
     "ss_raster_partial_floats": ([I64], c_int64),
     "ss_raster_bwd_deterministic": ([P, P, P, P, P, I32, I32, P, P, P, P, P, P, P, P, P, I32, P, P,
                                      P, P], c_int),

@@ -9,6 +9,7 @@
 //                 SURVEY's 34-bit keys tile << 21 | rank
 //   ranges      : boundary detection over the sorted tile ids
 #include <cub/cub.cuh>
+#include <stdlib.h>
 
 #include "ss_common.cuh"
 
@@ -177,6 +178,318 @@ __global__ void tile_len_kernel(const int2* __restrict__ ranges, int n_tiles,
   ids[t] = t;
 }
 
+// ---------------------------------------------------------------------------
+// Chunked binning (default): the rank range [0, n) is cut into C chunks of
+// about equal pair counts (bounds from the offsets prefix).
+//   emit   : CTA per chunk; lane-per-pair waves write every pair's tile id
+//            (u16) and splat id at its emit position offsets[k] + j, and a
+//            shared-memory histogram of the chunk's tiles -> counts[c][t]
+//   scan   : per tile, exclusive scan of counts[.][t] over the chunks (in
+//            place -> base[c][t]) and the tile totals; one CTA scans the
+//            totals into tile starts -> ranges
+//   scatter: CTA per chunk; waves of 256 pairs in emit order go to their
+//            tile's slot start[t] + base[c][t] + (earlier pairs of the chunk
+//            in that tile), ranked stably inside the wave (see below).
+// Chunks are rank ranges laid out in chunk order inside every tile list and
+// each step is stable, so the lists equal the stable global pair sort's.
+constexpr int kBinThreads = 256;
+constexpr int kBinWarps = kBinThreads / 32;
+
+// Chunk c covers ranks [bounds[c], bounds[c+1]): equal shares of the K pairs
+// (offsets is the exclusive per-rank pair prefix), so a chunk of near, large
+// splats is as short as one of far, small splats.
+__global__ void bin_bounds_kernel(const int32_t* __restrict__ offsets, int32_t n, int32_t n_chunks,
+                                  int32_t* __restrict__ bounds) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > n_chunks) return;
+  const int64_t K = offsets[n];
+  const int32_t target = (int32_t)(K * c / n_chunks);
+  int lo = 0, hi = n;  // first k with offsets[k] >= target
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (offsets[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  bounds[c] = c == n_chunks ? n : (c == 0 ? 0 : lo);
+}
+
+// q = x / w for 0 <= x < 2^20, 1 <= w via the float reciprocal rw = 1/w:
+// (x + 0.5) / w is at least 0.5 / w from an integer, far above the rounding.
+__device__ __forceinline__ int div_small(int x, float rw) {
+  return (int)(((float)x + 0.5f) * rw);
+}
+
+__device__ __forceinline__ bool kept_tile(uint64_t mask, int j, const float* gl, int tx, int ty,
+                                          int4 bb) {
+  return j < 64 ? (bool)((mask >> j) & 1ull) : tile_keeps(gl, tx, ty, bb);
+}
+
+// j-th (0-based) set bit of a 64-bit mask (j < popc(mask)).
+__device__ __forceinline__ int nth_set_bit(uint64_t mask, int j) {
+  const uint32_t lo = (uint32_t)mask;
+  const int pl = __popc(lo);
+  uint32_t m = j < pl ? lo : (uint32_t)(mask >> 32);
+  int jj = j < pl ? j : j - pl;
+  int pos = j < pl ? 0 : 32;
+#pragma unroll
+  for (int width = 16; width >= 1; width >>= 1) {
+    const int c = __popc(m & ((1u << width) - 1u));
+    if (jj >= c) {
+      jj -= c;
+      m >>= width;
+      pos += width;
+    }
+  }
+  return pos;
+}
+
+__global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
+    const int32_t* __restrict__ order, const int32_t* __restrict__ offsets,
+    const int4* __restrict__ bbox, const float* __restrict__ geom,
+    const uint64_t* __restrict__ tile_mask, const int32_t* __restrict__ bounds, int32_t n_tiles,
+    int32_t tiles_x, uint16_t* __restrict__ keys, int32_t* __restrict__ vals,
+    int32_t* __restrict__ counts) {
+  extern __shared__ int32_t s_hist[];
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_hist[t] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k0 = bounds[blockIdx.x], k1 = bounds[blockIdx.x + 1];
+  for (int kb = k0 + warp * 32; kb < k1; kb += kBinWarps * 32) {
+    const int k = kb + lane;
+    int32_t i = 0, o0 = 0, cnt = 0, tx0 = 0, ty0 = 0, w = 1, total = 0;
+    int4 bb = make_int4(0, 0, 0, 0);
+    uint64_t mask = 0;
+    if (k < k1) {
+      o0 = offsets[k];
+      cnt = offsets[k + 1] - o0;
+      if (cnt > 0) {
+        i = order[k];
+        bb = bbox[i];
+        mask = tile_mask[i];
+        tx0 = bb.x / kTile;
+        ty0 = bb.z / kTile;
+        w = (bb.y - 1) / kTile + 1 - tx0;
+        total = w * ((bb.w - 1) / kTile + 1 - ty0);
+      }
+    }
+    const float rw = 1.f / (float)w;
+    const int nm = __popcll(mask);  // the first nm pairs of the splat
+    // lane-per-pair waves over the batch's in-mask pairs
+    int incl = nm;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int excl = incl - nm;
+    const int P = __shfl_sync(0xffffffffu, incl, 31);
+    for (int q = 0; q < P; q += 32) {
+      const int p = q + lane;
+      int src = 0;  // last lane with excl <= p
+#pragma unroll
+      for (int b = 16; b >= 1; b >>= 1) {
+        const int e = __shfl_sync(0xffffffffu, excl, src + b);
+        if (e <= p) src += b;
+      }
+      const int j = p - __shfl_sync(0xffffffffu, excl, src);
+      const int32_t si = __shfl_sync(0xffffffffu, i, src);
+      const uint32_t mlo = __shfl_sync(0xffffffffu, (uint32_t)mask, src);
+      const uint32_t mhi = __shfl_sync(0xffffffffu, (uint32_t)(mask >> 32), src);
+      const int stx0 = __shfl_sync(0xffffffffu, tx0, src);
+      const int sty0 = __shfl_sync(0xffffffffu, ty0, src);
+      const int sw = __shfl_sync(0xffffffffu, w, src);
+      const float srw = __shfl_sync(0xffffffffu, rw, src);
+      const int so0 = __shfl_sync(0xffffffffu, o0, src);
+      if (p < P) {
+        const int bit = nth_set_bit(((uint64_t)mhi << 32) | mlo, j);
+        const int r = div_small(bit, srw);
+        const int t = (sty0 + r) * tiles_x + stx0 + bit - r * sw;
+        keys[so0 + j] = (uint16_t)t;
+        vals[so0 + j] = si;
+        atomicAdd(&s_hist[t], 1);
+      }
+    }
+    // tiles past the 64-bit mask of large splats: splat by splat, lanes over
+    // the bbox tiles, emit positions by ballot prefix (bbox order)
+    uint32_t far = __ballot_sync(0xffffffffu, total > 64);
+    while (far) {
+      const int src = __ffs(far) - 1;
+      far &= far - 1;
+      const int32_t si = __shfl_sync(0xffffffffu, i, src);
+      const int4 sbb = make_int4(__shfl_sync(0xffffffffu, bb.x, src),
+                                 __shfl_sync(0xffffffffu, bb.y, src),
+                                 __shfl_sync(0xffffffffu, bb.z, src),
+                                 __shfl_sync(0xffffffffu, bb.w, src));
+      const int stx0 = __shfl_sync(0xffffffffu, tx0, src);
+      const int sty0 = __shfl_sync(0xffffffffu, ty0, src);
+      const int sw = __shfl_sync(0xffffffffu, w, src);
+      const int stot = __shfl_sync(0xffffffffu, total, src);
+      const float srw = __shfl_sync(0xffffffffu, rw, src);
+      int e = __shfl_sync(0xffffffffu, o0 + nm, src);
+      float gl[kGeom];
+#pragma unroll
+      for (int q = 0; q < kGeom; ++q) gl[q] = geom[(int64_t)si * kGeom + q];
+      for (int j0 = 64; j0 < stot; j0 += 32) {
+        const int j = j0 + lane;
+        int t = 0;
+        bool keep = false;
+        if (j < stot) {
+          const int r = div_small(j, srw);
+          const int ty = sty0 + r, tx = stx0 + j - r * sw;
+          keep = tile_keeps(gl, tx, ty, sbb);
+          t = ty * tiles_x + tx;
+        }
+        const uint32_t kb2 = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          const int q = e + __popc(kb2 & ((1u << lane) - 1u));
+          keys[q] = (uint16_t)t;
+          vals[q] = si;
+          atomicAdd(&s_hist[t], 1);
+        }
+        e += __popc(kb2);
+      }
+    }
+  }
+  __syncthreads();
+  int32_t* row = counts + (int64_t)blockIdx.x * n_tiles;
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) row[t] = s_hist[t];
+}
+
+// Block (32 tiles) x (8 warps); warp w scans chunks [w C8, (w+1) C8).
+__global__ void __launch_bounds__(kBinThreads) bin_col_scan_kernel(int32_t* __restrict__ counts,
+                                                                   int32_t n_chunks,
+                                                                   int32_t n_tiles,
+                                                                   int32_t* __restrict__ totals) {
+  __shared__ int32_t s_part[kBinWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
+  const int per = (n_chunks + kBinWarps - 1) / kBinWarps;
+  const int c0 = warp * per, c1 = min(n_chunks, c0 + per);
+  int32_t sum = 0;
+  if (t < n_tiles) {
+#pragma unroll 8
+    for (int c = c0; c < c1; ++c) sum += counts[(int64_t)c * n_tiles + t];
+  }
+  s_part[warp][lane] = sum;
+  __syncthreads();
+  int32_t run = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < kBinWarps; ++w) {
+    run += w < warp ? s_part[w][lane] : 0;
+    all += s_part[w][lane];
+  }
+  if (t >= n_tiles) return;
+  if (warp == 0) totals[t] = all;
+  for (int cb = c0; cb < c1; cb += 8) {
+    int32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = cb + u < c1 ? counts[(int64_t)(cb + u) * n_tiles + t] : 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (cb + u < c1) counts[(int64_t)(cb + u) * n_tiles + t] = run;
+      run += v[u];
+    }
+  }
+}
+
+// One CTA: exclusive scan of the tile totals -> start[t], ranges[t].
+__global__ void __launch_bounds__(1024) bin_tile_scan_kernel(const int32_t* __restrict__ totals,
+                                                             int32_t n_tiles,
+                                                             int32_t* __restrict__ start,
+                                                             int2* __restrict__ ranges) {
+  __shared__ int32_t s_warp[32];
+  const int per = (n_tiles + blockDim.x - 1) / blockDim.x;
+  const int t0 = threadIdx.x * per, t1 = min(n_tiles, t0 + per);
+  int32_t local = 0;
+  for (int t = t0; t < t1; ++t) local += totals[t];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t inc = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t v = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    s_warp[lane] = v;  // inclusive over warps
+  }
+  __syncthreads();
+  int32_t run = inc - local + (warp > 0 ? s_warp[warp - 1] : 0);
+  for (int t = t0; t < t1; ++t) {
+    const int32_t c = totals[t];
+    start[t] = run;
+    ranges[t] = make_int2(run, run + c);
+    run += c;
+  }
+}
+
+// Stable scatter of one chunk: waves of 256 pairs in emit order, one per
+// thread.  Equal tiles inside a warp are ranked by lane (__match_any); the
+// warps' counts per tile sit in byte w of a 64-bit shared word per tile, so
+// a pair's slot is cur[t] + (counts of lower warps) + (rank in its warp) --
+// the wave's pairs land in emit order.  The highest warp holding a tile then
+// advances cur[t] and clears the word.
+__global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(
+    const int32_t* __restrict__ offsets, const int32_t* __restrict__ bounds,
+    const uint16_t* __restrict__ keys, const int32_t* __restrict__ vals, int32_t n_tiles,
+    const int32_t* __restrict__ base, const int32_t* __restrict__ start,
+    int32_t* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  unsigned long long* s_wc = reinterpret_cast<unsigned long long*>(s_dyn);  // n_tiles
+  int32_t* s_cur = reinterpret_cast<int32_t*>(s_wc + n_tiles);              // n_tiles
+  const int c = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int32_t* brow = base + (int64_t)c * n_tiles;
+#pragma unroll 4
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    s_cur[t] = start[t] + brow[t];
+    s_wc[t] = 0ull;
+  }
+  const int q0 = offsets[bounds[c]], q1 = offsets[bounds[c + 1]];
+  const uint32_t lt = (1u << lane) - 1u;
+  const unsigned long long below_mask = (1ull << (8 * warp)) - 1ull;
+  unsigned char* s_wc8 = reinterpret_cast<unsigned char*>(s_wc);
+  // software pipelined: the next wave's pair is loaded while this one is placed
+  int q = q0 + threadIdx.x;
+  int t_next = q < q1 ? keys[q] : n_tiles;  // n_tiles: no tile
+  int32_t v_next = q < q1 ? vals[q] : 0;
+  for (int qb = q0; qb < q1; qb += kBinThreads) {
+    const bool ok = qb + threadIdx.x < q1;
+    const int t = t_next;
+    const int32_t v = v_next;
+    q = qb + kBinThreads + threadIdx.x;
+    t_next = q < q1 ? keys[q] : n_tiles;
+    v_next = q < q1 ? vals[q] : 0;
+    const uint32_t peers = __match_any_sync(0xffffffffu, t);
+    const int leader = __ffs(peers) - 1;
+    const int cnt = __popc(peers), rin = __popc(peers & lt);
+    __syncthreads();  // previous wave's cursor updates / clears are done
+    if (ok && lane == leader) s_wc8[(size_t)t * 8 + warp] = (unsigned char)cnt;
+    __syncthreads();
+    int prefix = 0;
+    bool last = false;
+    if (ok) {
+      const unsigned long long word = s_wc[t];
+      // byte sum of the lower warps' counts (each <= 32, sum <= 224 < 256)
+      prefix = (int)(((word & below_mask) * 0x0101010101010101ull) >> 56);
+      last = warp == 7 || (word >> (8 * (warp + 1))) == 0ull;
+      out[s_cur[t] + prefix + rin] = v;
+    }
+    __syncthreads();
+    if (ok && lane == leader && last) {
+      s_cur[t] += prefix + cnt;
+      s_wc[t] = 0ull;
+    }
+  }
+}
+
 static int bits_for(int64_t v) {
   int b = 1;
   while ((1ll << b) < v) ++b;
@@ -282,6 +595,82 @@ extern "C" int ss_emit_tile_pairs(const int32_t* order, const int32_t* offsets,
   emit_pairs_kernel<<<grid_for(n, 128), 128, 0, stream>>>(
       order, offsets, (const int4*)bbox, geom, tile_mask, n, tiles_x, keys, vals);
   return check_launch("ss_emit_tile_pairs");
+}
+
+static int g_binning = 0;  // 0 = counting sort, 1 = pair radix sort
+
+extern "C" int ss_set_binning(int32_t mode) {
+  if (mode != 0 && mode != 1) return set_error(SS_ERR_INVALID, "ss_set_binning: mode must be 0 or 1");
+  g_binning = mode;
+  return SS_OK;
+}
+
+extern "C" int ss_get_binning(void) { return g_binning; }
+
+// Chunks: ~8k pairs each (bounds balance them by pairs), at most 4096.
+constexpr int kBinPairsPerChunk = 8192;
+constexpr int kBinChunksCap = 4096;
+constexpr int kBinMaxTiles = 18 * 1024;  // 12 bytes of shared memory per tile in the scatter
+
+static int bin_chunks(int64_t n_pairs) {
+  int64_t c = (n_pairs + kBinPairsPerChunk - 1) / kBinPairsPerChunk;
+  return (int)(c < 1 ? 1 : (c > kBinChunksCap ? kBinChunksCap : c));
+}
+
+extern "C" size_t ss_bin_tiles_workspace_bytes(int64_t n_pairs, int32_t n_tiles) {
+  const size_t nt = (size_t)(n_tiles > 0 ? n_tiles : 1);
+  const size_t C = (size_t)bin_chunks(n_pairs);
+  return align256(C * nt * 4) + 2 * align256(nt * 4) + align256((C + 1) * 4) + 256;
+}
+
+extern "C" int32_t ss_bin_tiles_supported(int64_t n_pairs, int32_t n_tiles) {
+  return n_tiles > 0 && n_tiles <= kBinMaxTiles && n_pairs < (1ll << 31) ? 1 : 0;
+}
+
+extern "C" int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const int32_t* bbox,
+                            const float* geom, const uint64_t* tile_mask, int32_t n,
+                            int64_t n_pairs, int32_t tiles_x, int32_t tiles_y, uint16_t* keys,
+                            int32_t* vals, int32_t* vals_out, int32_t* ranges, void* ws,
+                            size_t ws_bytes, cudaStream_t stream) {
+  const int n_tiles = tiles_x * tiles_y;
+  if (n < 0 || tiles_x <= 0 || tiles_y <= 0 || n_pairs < 0)
+    return set_error(SS_ERR_INVALID, "ss_bin_tiles: bad sizes");
+  if (!ss_bin_tiles_supported(n_pairs, n_tiles))
+    return set_error(SS_ERR_INVALID, "ss_bin_tiles: %d tiles / %lld pairs unsupported (use the pair sort)",
+                     n_tiles, (long long)n_pairs);
+  if (ws_bytes < ss_bin_tiles_workspace_bytes(n_pairs, n_tiles))
+    return set_error(SS_ERR_WORKSPACE, "ss_bin_tiles: workspace too small");
+  if (n == 0 || n_pairs == 0) {
+    cudaMemsetAsync(ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, stream);
+    return check_launch("ss_bin_tiles");
+  }
+  const int C = bin_chunks(n_pairs);
+  char* w = (char*)ws;
+  int32_t* counts = (int32_t*)w;
+  int32_t* totals = (int32_t*)(w + align256((size_t)C * n_tiles * 4));
+  int32_t* start = (int32_t*)((char*)totals + align256((size_t)n_tiles * 4));
+  int32_t* bounds = (int32_t*)((char*)start + align256((size_t)n_tiles * 4));
+  const size_t smem = (size_t)n_tiles * 4;
+  const size_t smem_scatter = (size_t)n_tiles * 12;
+  static size_t attr = 0, attr_scatter = 0;
+  if (smem > 32 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(bin_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  if (smem_scatter > 32 * 1024 && smem_scatter > attr_scatter) {
+    cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_scatter);
+    attr_scatter = smem_scatter;
+  }
+  bin_bounds_kernel<<<(C + 1 + 127) / 128, 128, 0, stream>>>(offsets, n, C, bounds);
+  bin_emit_kernel<<<C, kBinThreads, smem, stream>>>(order, offsets, (const int4*)bbox, geom,
+                                                    tile_mask, bounds, n_tiles, tiles_x, keys,
+                                                    vals, counts);
+  bin_col_scan_kernel<<<(n_tiles + 31) / 32, kBinThreads, 0, stream>>>(counts, C, n_tiles, totals);
+  bin_tile_scan_kernel<<<1, 1024, 0, stream>>>(totals, n_tiles, start, (int2*)ranges);
+  bin_scatter_kernel<<<C, kBinThreads, smem_scatter, stream>>>(offsets, bounds, keys, vals,
+                                                               n_tiles, counts, start, vals_out);
+  return check_launch("ss_bin_tiles");
 }
 
 extern "C" int ss_sort_tile_pairs(uint32_t* keys, int32_t* vals, uint32_t* keys_alt,

@@ -70,17 +70,31 @@ extern "C" int ss_render_fwd(const ss_store* store, const ss_camera* cam, ss_vie
     return check_launch("ss_render_fwd: pair count");
   v->n_pairs = k_host;
   if (k_host > v->pair_cap) return set_error(SS_ERR_CAPACITY, "ss_render_fwd: %d pairs > capacity", k_host);
-  if ((rc = ss_emit_tile_pairs(v->order, v->offsets, v->bbox, v->geom, v->tile_mask, n, tiles_x,
-                               v->keys, v->vals, stream)))
-    return rc;
-  int32_t sel = 0;
-  if ((rc = ss_sort_tile_pairs(v->keys, v->vals, v->keys_alt, v->vals_alt, k_host, n_tiles, &sel,
-                               v->ws, v->ws_bytes, stream)))
-    return rc;
-  v->sorted_sel = sel;
-  const uint32_t* sk = sel ? v->keys_alt : v->keys;
-  const int32_t* sv = sel ? v->vals_alt : v->vals;
-  if ((rc = ss_tile_ranges(sk, k_host, n_tiles, v->ranges, stream))) return rc;
+  const int32_t* sv = v->vals;
+  if (ss_get_binning() == 0 && ss_bin_tiles_supported(k_host, n_tiles)) {
+    const size_t need_bin = ss_bin_tiles_workspace_bytes(k_host, n_tiles);
+    if (v->ws_bytes < need_bin) {
+      v->ws_needed = need_bin;
+      return set_error(SS_ERR_WORKSPACE, "ss_render_fwd: workspace %zu < %zu", v->ws_bytes, need_bin);
+    }
+    if ((rc = ss_bin_tiles(v->order, v->offsets, v->bbox, v->geom, v->tile_mask, n, k_host,
+                           tiles_x, tiles_y, (uint16_t*)v->keys, v->vals, v->vals_alt, v->ranges,
+                           v->ws, v->ws_bytes, stream)))
+      return rc;
+    v->sorted_sel = 1;
+    sv = v->vals_alt;
+  } else {
+    if ((rc = ss_emit_tile_pairs(v->order, v->offsets, v->bbox, v->geom, v->tile_mask, n,
+                                 tiles_x, v->keys, v->vals, stream)))
+      return rc;
+    int32_t sel = 0;
+    if ((rc = ss_sort_tile_pairs(v->keys, v->vals, v->keys_alt, v->vals_alt, k_host, n_tiles,
+                                 &sel, v->ws, v->ws_bytes, stream)))
+      return rc;
+    v->sorted_sel = sel;
+    sv = sel ? v->vals_alt : v->vals;
+    if ((rc = ss_tile_ranges(sel ? v->keys_alt : v->keys, k_host, n_tiles, v->ranges, stream))) return rc;
+  }
   if ((rc = ss_tile_order(v->ranges, n_tiles, v->tile_order, v->ws, v->ws_bytes, stream))) return rc;
   record(v->events[0], stream);
   rc = ss_raster_fwd(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,

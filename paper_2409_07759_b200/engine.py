@@ -236,7 +236,12 @@ class ViewPipeline:
             "n_contrib": b["n_contrib"][: self.width * self.height].cpu(),
         }
         if self.n_pairs:
-            out["keys"] = self.sorted_keys[: self.n_pairs].cpu()
+            # tile id of every list entry, from the ranges (both binning paths
+            # leave the lists contiguous in tile order)
+            rg = b["ranges"][: self.n_tiles].long()
+            lens = (rg[:, 1] - rg[:, 0]).clamp(min=0)
+            out["keys"] = torch.repeat_interleave(
+                torch.arange(self.n_tiles, device=rg.device), lens).to(torch.int32).cpu()
             out["vals"] = self.sorted_vals[: self.n_pairs].cpu()
             out["ranges"] = b["ranges"][: self.n_tiles].cpu()
         return out

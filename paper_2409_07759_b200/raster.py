@@ -86,6 +86,18 @@ def set_deterministic(flag: bool = True) -> None:
     pipeline().deterministic = bool(flag)
 
 
+def set_binning(mode: str = "counting") -> None:
+    """Tile binning used by the forward: "counting" (default; chunked
+    histograms + stable scatter, ss_bin_tiles) or "sort" (emit pairs + stable
+    radix sort on tile ids).  Both give bit-identical tile lists."""
+    modes = {"counting": 0, "sort": 1}
+    if mode not in modes:
+        raise InvalidParameterError(f"binning must be one of {sorted(modes)}, got {mode!r}")
+    from . import _lib as L
+
+    L.check(L.lib().ss_set_binning(modes[mode]), "set_binning")
+
+
 def _upload(arrays: GaussianArrays) -> Store:
     rows = torch.from_numpy(arrays.rows()).to(device())
     return Store(opt=None, mat=rows)

@@ -10,7 +10,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def declared():
     text = (ROOT / "include" / "swings.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(ss_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|size_t|const char\*)\s+(ss_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_hot_path():

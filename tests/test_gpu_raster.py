@@ -329,3 +329,53 @@ def test_depth_order_exact_on_adversarial_keys():
                                L.stream_ptr()), "depth_order")
     ref = np.lexsort((np.arange(n), keys))
     assert np.array_equal(order.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("scene", ["config3_full", "huge"])
+def test_binning_modes_agree(ss, scene):
+    """Counting-sort binning (default) and emit + radix pair sort build the same
+    tile lists bit for bit, hence the same image and gradients."""
+    P, R = ss
+    if scene == "config3_full":
+        arr = _synth_scene(P, 300_000, (300.0 / 300_000) ** (1 / 3), seed=7)
+        ocam = arc_camera(11, 20, 1352, 1014)
+    else:
+        rng = np.random.default_rng(12)
+        n = 2000
+        means = rng.uniform((-0.6, -0.45, 1.2), (0.6, 0.45, 3.5), size=(n, 3))
+        scales = np.exp(rng.uniform(np.log(0.002), np.log(0.03), size=(n, 3)))
+        scales[:30] = rng.uniform(0.2, 0.5, size=(30, 3))
+        arr = P.GaussianArrays(means, random_unit_quats(rng, n), scales,
+                               rng.uniform(0.05, 0.95, n), rng.uniform(0, 1, (n, 3)))
+        from conftest import Cam
+        ocam = Cam(700, 300, 500.0, 480.0, 350.0, 150.0, np.eye(3), np.zeros(3))
+    cam = cam_from(P, ocam)
+    gdir = np.random.default_rng(3).normal(size=(cam.height, cam.width, 3)) * 1e-6
+    out = {}
+    try:
+        for mode in ("counting", "sort"):
+            R.set_binning(mode)
+            R.set_deterministic(True)
+            img = R.render_arrays(cam, arr).pixels
+            st = R.pipeline().state()
+            g = R.render_arrays_backward(cam, arr, gdir)
+            out[mode] = (img, st, g)
+    finally:
+        R.set_binning("counting")
+        R.set_deterministic(False)
+    (ia, sa, ga), (ib, sb, gb) = out["counting"], out["sort"]
+    assert sa["n_pairs"] == sb["n_pairs"] > 0
+    for k in ("keys", "vals", "ranges"):
+        a, b = sa[k].numpy(), sb[k].numpy()
+        if k == "ranges":
+            a, b = a.reshape(-1, 2).copy(), b.reshape(-1, 2).copy()
+            a[a[:, 0] == a[:, 1]] = 0
+            b[b[:, 0] == b[:, 1]] = 0
+        assert np.array_equal(a, b), k
+    assert np.array_equal(ia, ib)
+    for k in g_keys():
+        assert np.array_equal(ga[k], gb[k]), k
+
+
+def g_keys():
+    return ("mean", "log_scale", "quat", "opacity_logit", "color")
