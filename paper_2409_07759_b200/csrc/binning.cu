@@ -200,17 +200,28 @@ constexpr int kBinWarps = kBinThreads / 32;
 // splats is as short as one of far, small splats.
 __global__ void bin_bounds_kernel(const int32_t* __restrict__ offsets, int32_t n, int32_t n_chunks,
                                   int32_t* __restrict__ bounds) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  // warp per boundary, 32-ary search: first k with offsets[k] >= target
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (c > n_chunks) return;
+  if (c == 0 || c == n_chunks) {
+    if (lane == 0) bounds[c] = c == 0 ? 0 : n;
+    return;
+  }
   const int64_t K = offsets[n];
   const int32_t target = (int32_t)(K * c / n_chunks);
-  int lo = 0, hi = n;  // first k with offsets[k] >= target
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (offsets[mid] < target) lo = mid + 1;
-    else hi = mid;
+  int lo = 0, hi = n;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) / 32;
+    const int probe = min(hi, lo + (lane + 1) * step);
+    const uint32_t below = __ballot_sync(0xffffffffu, offsets[probe] < target);
+    const int nb = __popc(below);  // probes below target form a prefix
+    const int nlo = lo + nb * step;
+    hi = min(hi, lo + (nb + 1) * step);
+    lo = nlo;
   }
-  bounds[c] = c == n_chunks ? n : (c == 0 ? 0 : lo);
+  const int k = lo + lane;
+  const uint32_t below = __ballot_sync(0xffffffffu, k < hi && offsets[k] < target);
+  if (lane == 0) bounds[c] = lo + __popc(below);
 }
 
 // q = x / w for 0 <= x < 2^20, 1 <= w via the float reciprocal rw = 1/w:
@@ -398,10 +409,13 @@ __global__ void __launch_bounds__(1024) bin_tile_scan_kernel(const int32_t* __re
                                                              int32_t* __restrict__ start,
                                                              int2* __restrict__ ranges) {
   __shared__ int32_t s_warp[32];
+  extern __shared__ int32_t s_tot[];  // totals staged by coalesced loads
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_tot[t] = totals[t];
+  __syncthreads();
   const int per = (n_tiles + blockDim.x - 1) / blockDim.x;
   const int t0 = threadIdx.x * per, t1 = min(n_tiles, t0 + per);
   int32_t local = 0;
-  for (int t = t0; t < t1; ++t) local += totals[t];
+  for (int t = t0; t < t1; ++t) local += s_tot[t];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int32_t inc = local;
 #pragma unroll
@@ -423,10 +437,15 @@ __global__ void __launch_bounds__(1024) bin_tile_scan_kernel(const int32_t* __re
   __syncthreads();
   int32_t run = inc - local + (warp > 0 ? s_warp[warp - 1] : 0);
   for (int t = t0; t < t1; ++t) {
-    const int32_t c = totals[t];
-    start[t] = run;
-    ranges[t] = make_int2(run, run + c);
+    const int32_t c = s_tot[t];
+    s_tot[t] = run;
     run += c;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const int32_t a = s_tot[t];
+    start[t] = a;
+    ranges[t] = make_int2(a, a + totals[t]);
   }
 }
 
@@ -447,19 +466,19 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(
   const int c = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t* brow = base + (int64_t)c * n_tiles;
+  const int q0 = offsets[bounds[c]], q1 = offsets[bounds[c + 1]];
+  // software pipelined: the next wave's pair is loaded while this one is placed
+  int q = q0 + threadIdx.x;
+  int t_next = q < q1 ? keys[q] : n_tiles;  // n_tiles: no tile
+  int32_t v_next = q < q1 ? vals[q] : 0;
 #pragma unroll 4
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
     s_cur[t] = start[t] + brow[t];
     s_wc[t] = 0ull;
   }
-  const int q0 = offsets[bounds[c]], q1 = offsets[bounds[c + 1]];
   const uint32_t lt = (1u << lane) - 1u;
   const unsigned long long below_mask = (1ull << (8 * warp)) - 1ull;
   unsigned char* s_wc8 = reinterpret_cast<unsigned char*>(s_wc);
-  // software pipelined: the next wave's pair is loaded while this one is placed
-  int q = q0 + threadIdx.x;
-  int t_next = q < q1 ? keys[q] : n_tiles;  // n_tiles: no tile
-  int32_t v_next = q < q1 ? vals[q] : 0;
   for (int qb = q0; qb < q1; qb += kBinThreads) {
     const bool ok = qb + threadIdx.x < q1;
     const int t = t_next;
@@ -607,19 +626,24 @@ extern "C" int ss_set_binning(int32_t mode) {
 
 extern "C" int ss_get_binning(void) { return g_binning; }
 
-// Chunks: ~8k pairs each (bounds balance them by pairs), at most 4096.
-constexpr int kBinPairsPerChunk = 8192;
+// Chunks: a whole number of scatter waves (resident CTAs on 148 SMs), each
+// chunk at most ~16k pairs (bounds balance them by pairs), at most 4096.
+constexpr int kBinPairsPerChunk = 16384;
 constexpr int kBinChunksCap = 4096;
 constexpr int kBinMaxTiles = 18 * 1024;  // 12 bytes of shared memory per tile in the scatter
 
-static int bin_chunks(int64_t n_pairs) {
-  int64_t c = (n_pairs + kBinPairsPerChunk - 1) / kBinPairsPerChunk;
-  return (int)(c < 1 ? 1 : (c > kBinChunksCap ? kBinChunksCap : c));
+static int bin_chunks(int64_t n_pairs, int n_tiles) {
+  int per_sm = (int)(228 * 1024 / ((size_t)n_tiles * 12 + 1024));
+  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+  const int64_t slots = 148ll * per_sm;
+  const int64_t waves = (n_pairs + slots * kBinPairsPerChunk - 1) / (slots * kBinPairsPerChunk);
+  const int64_t c = slots * (waves < 1 ? 1 : waves);
+  return (int)(c > kBinChunksCap ? kBinChunksCap : c);
 }
 
 extern "C" size_t ss_bin_tiles_workspace_bytes(int64_t n_pairs, int32_t n_tiles) {
   const size_t nt = (size_t)(n_tiles > 0 ? n_tiles : 1);
-  const size_t C = (size_t)bin_chunks(n_pairs);
+  const size_t C = (size_t)bin_chunks(n_pairs, (int)nt);
   return align256(C * nt * 4) + 2 * align256(nt * 4) + align256((C + 1) * 4) + 256;
 }
 
@@ -644,7 +668,7 @@ extern "C" int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const 
     cudaMemsetAsync(ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, stream);
     return check_launch("ss_bin_tiles");
   }
-  const int C = bin_chunks(n_pairs);
+  const int C = bin_chunks(n_pairs, n_tiles);
   char* w = (char*)ws;
   int32_t* counts = (int32_t*)w;
   int32_t* totals = (int32_t*)(w + align256((size_t)C * n_tiles * 4));
@@ -655,6 +679,7 @@ extern "C" int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const 
   static size_t attr = 0, attr_scatter = 0;
   if (smem > 32 * 1024 && smem > attr) {
     cudaFuncSetAttribute(bin_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(bin_tile_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
   if (smem_scatter > 32 * 1024 && smem_scatter > attr_scatter) {
@@ -662,12 +687,12 @@ extern "C" int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const 
                          (int)smem_scatter);
     attr_scatter = smem_scatter;
   }
-  bin_bounds_kernel<<<(C + 1 + 127) / 128, 128, 0, stream>>>(offsets, n, C, bounds);
+  bin_bounds_kernel<<<(32 * (C + 1) + 127) / 128, 128, 0, stream>>>(offsets, n, C, bounds);
   bin_emit_kernel<<<C, kBinThreads, smem, stream>>>(order, offsets, (const int4*)bbox, geom,
                                                     tile_mask, bounds, n_tiles, tiles_x, keys,
                                                     vals, counts);
   bin_col_scan_kernel<<<(n_tiles + 31) / 32, kBinThreads, 0, stream>>>(counts, C, n_tiles, totals);
-  bin_tile_scan_kernel<<<1, 1024, 0, stream>>>(totals, n_tiles, start, (int2*)ranges);
+  bin_tile_scan_kernel<<<1, 1024, (size_t)n_tiles * 4, stream>>>(totals, n_tiles, start, (int2*)ranges);
   bin_scatter_kernel<<<C, kBinThreads, smem_scatter, stream>>>(offsets, bounds, keys, vals,
                                                                n_tiles, counts, start, vals_out);
   return check_launch("ss_bin_tiles");
