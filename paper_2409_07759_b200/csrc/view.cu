@@ -3,13 +3,32 @@
 // as single C-ABI calls, so the host issues two calls per view instead of ~25
 // (the Python-side launch overhead left the GPU idle ~16 % of a step).
 //
-// The forward synchronizes the stream once, to read the number of
-// (splat, tile) pairs K that sizes the pair sort; if K exceeds the caller's
-// pair capacity it returns SS_ERR_CAPACITY with K in v->n_pairs and the
-// caller grows the buffers and calls again.
+// The forward waits once for the number of (splat, tile) pairs K that sizes
+// the binning (read back right after the projection, so the depth sort runs
+// meanwhile); if K exceeds the caller's pair capacity it returns
+// SS_ERR_CAPACITY with K in v->n_pairs and the caller grows the buffers and
+// calls again.
 #include "ss_common.cuh"
 
 using namespace ss;
+
+// out[0] += sum of v[0..n) (int32; out zeroed by the caller): grid-stride,
+// one atomic per CTA.
+__global__ void __launch_bounds__(256) sum_kernel(const int32_t* __restrict__ v, int32_t n,
+                                                  int32_t* __restrict__ out) {
+  __shared__ int32_t s_part[8];
+  int32_t acc = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    acc += v[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) acc += s_part[w];
+    atomicAdd(out, acc);
+  }
+}
 
 static void record(void* ev, cudaStream_t stream) {
   if (ev) cudaEventRecord((cudaEvent_t)ev, stream);
@@ -60,14 +79,27 @@ extern "C" int ss_render_fwd(const ss_store* store, const ss_camera* cam, ss_vie
   if ((rc = ss_project_fwd(store, v->rows, n, cam, v->rec_a, v->rec_b, v->rec_c, v->depth_key,
                            v->bbox, v->n_tiles, v->geom, v->tile_mask, stream)))
     return rc;
+  // K = sum of the per-splat tile counts, read back early: the host waits on
+  // it (to size the binning) while the GPU runs the depth sort and offsets.
+  // It is parked in offsets[n], which ss_tile_offsets rewrites with K.
+  static int32_t* k_pinned = nullptr;
+  static cudaEvent_t k_event = nullptr;
+  if (!k_pinned) {
+    if (cudaMallocHost(&k_pinned, sizeof(int32_t)) != cudaSuccess ||
+        cudaEventCreateWithFlags(&k_event, cudaEventDisableTiming) != cudaSuccess)
+      return check_launch("ss_render_fwd: pinned pair count");
+  }
+  cudaMemsetAsync(v->offsets + n, 0, sizeof(int32_t), stream);
+  sum_kernel<<<min(296, (n + 255) / 256), 256, 0, stream>>>(v->n_tiles, n, v->offsets + n);
+  if (cudaMemcpyAsync(k_pinned, v->offsets + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream) !=
+          cudaSuccess ||
+      cudaEventRecord(k_event, stream) != cudaSuccess)
+    return check_launch("ss_render_fwd: pair count");
   if ((rc = ss_depth_order(v->depth_key, n, v->order, v->ws, v->ws_bytes, stream))) return rc;
   if ((rc = ss_tile_offsets(v->order, v->n_tiles, n, v->offsets, v->ws, v->ws_bytes, stream)))
     return rc;
-  int32_t k_host = 0;
-  if (cudaMemcpyAsync(&k_host, v->offsets + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream) !=
-          cudaSuccess ||
-      cudaStreamSynchronize(stream) != cudaSuccess)
-    return check_launch("ss_render_fwd: pair count");
+  if (cudaEventSynchronize(k_event) != cudaSuccess) return check_launch("ss_render_fwd: pair count");
+  const int32_t k_host = *k_pinned;
   v->n_pairs = k_host;
   if (k_host > v->pair_cap) return set_error(SS_ERR_CAPACITY, "ss_render_fwd: %d pairs > capacity", k_host);
   const int32_t* sv = v->vals;
