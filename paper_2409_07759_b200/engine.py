@@ -75,12 +75,10 @@ class ViewPipeline:
 
     def enable_timing(self, on: bool = True):
         """Record CUDA events around the raster kernels (inside the native
-        driver, on the launch stream) for kernel_ms()."""
-        if not on and self.events:
-            for evs in self.events.get("_pending", []):
-                for e in evs:
-                    L.lib().ss_event_destroy(e)
-        self.events = {} if on else None
+        driver, on the launch stream) for kernel_ms().  Event quads come from
+        a pool that persists across calls (no event creation per view)."""
+        self._event_pool = getattr(self, "_event_pool", [])
+        self.events = {"_pending": []} if on else None
 
     def kernel_ms(self) -> dict:
         """Total milliseconds of raster_fwd / raster_bwd over the timed views
@@ -150,6 +148,8 @@ class ViewPipeline:
                     v.events[i] = evs[i]
             rc = lib.ss_render_fwd(ctypes.byref(self.store_struct), ctypes.byref(self.cam_struct),
                                    ctypes.byref(v), sp)
+            if rc in (L.SS_ERR_CAPACITY, L.SS_ERR_WORKSPACE) and self.events is not None:
+                self.events["_pending"].pop()  # this attempt recorded nothing
             if rc == L.SS_ERR_CAPACITY:
                 cap = int(v.n_pairs * 1.25) + 1024
                 for name in ("keys", "vals", "keys_alt", "vals_alt"):
@@ -171,12 +171,17 @@ class ViewPipeline:
         return b["img"][: H * W * 3].view(H, W, 3)
 
     def _new_events(self):
-        evs = []
-        for _ in range(4):
-            e = ctypes.c_void_p()
-            L.check(L.lib().ss_event_create(ctypes.byref(e)), "event_create")
-            evs.append(e.value)
-        self.events.setdefault("_pending", []).append(evs)
+        pending = self.events.setdefault("_pending", [])
+        if len(pending) < len(self._event_pool):
+            evs = self._event_pool[len(pending)]
+        else:
+            evs = []
+            for _ in range(4):
+                e = ctypes.c_void_p()
+                L.check(L.lib().ss_event_create(ctypes.byref(e)), "event_create")
+                evs.append(e.value)
+            self._event_pool.append(evs)
+        pending.append(evs)
         return evs
 
     # ------------------------------------------------------------------ bwd
