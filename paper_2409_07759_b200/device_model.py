@@ -219,9 +219,17 @@ class DeviceModel:
         _, n, n_opt_here = self.compact(frame)
         self.grads.zero_()
         cam = dataset.cameras[view]
-        gt = dataset.device_frame(frame, view)
+        # ground truth may still be in flight on a copy stream: only the loss
+        # waits for it, the projection / binning / raster run meanwhile
+        get_async = getattr(dataset, "device_frame_async", None)
+        if get_async is not None:
+            gt, gt_ready = get_async(frame, view)
+        else:
+            gt, gt_ready = dataset.device_frame(frame, view), None
         self.pipe.deterministic = state.deterministic
         img = self.pipe.forward(self.store, self.active_rows, n, cam)
+        if gt_ready is not None:
+            torch.cuda.current_stream().wait_event(gt_ready)
         dimg, sums = self.lossbuf.run(img, cam.height, cam.width, gt_u8=gt, lut=self.lut,
                                       ssim_weight=cfg.ssim_weight)
         self.pipe.backward(dimg, self.grads, trainable_rows=self.num_gs)
