@@ -1,7 +1,8 @@
 // a-8 photometric loss: (1-w) L1 + w (1 - SSIM) with its exact image
 // gradient (loss.py:29-60, 73-96).
 //
-// Two shared-memory tiled passes over 32x32 pixel tiles, channel by channel:
+// Two shared-memory tiled passes over 32x32 pixel tiles, one CTA per tile and
+// channel:
 //   pass 1: load x (prediction) and y (ground truth, u8 sRGB through the
 //           256-entry linearisation LUT, raster.py:428-432) with a 5-px halo,
 //           separable 11-tap blur of x, y, xx, xy, yy (zero padding), SSIM
@@ -43,24 +44,24 @@ __device__ __forceinline__ float gt_value(const uint8_t* gt_u8, const float* lut
   return gt_u8 ? lut[gt_u8[idx]] : gt_f32[idx];
 }
 
-// Loads the (42 x 42) halo region of all three channels of x and y, row by
-// row as contiguous 3-channel runs (coalesced), zero outside the image.
-__device__ __forceinline__ void load_region3(const float* __restrict__ pred,
-                                             const uint8_t* __restrict__ gt_u8,
-                                             const float* s_lut, const float* __restrict__ gt_f32,
-                                             int W, int H, int x0, int y0, float* s_x3, float* s_y3) {
-  constexpr int kRow = 3 * 42;
-  for (int idx = threadIdx.x; idx < 42 * kRow; idx += blockDim.x) {
-    const int r = idx / kRow, q = idx % kRow;
-    const int gy = y0 - 5 + r, gx = x0 - 5 + q / 3;
+// Loads the (42 x 42) halo region of channel ch of x and y (zero outside
+// the image) into padded (42 x kLP) tiles.
+__device__ __forceinline__ void load_region(const float* __restrict__ pred,
+                                            const uint8_t* __restrict__ gt_u8,
+                                            const float* s_lut, const float* __restrict__ gt_f32,
+                                            int W, int H, int x0, int y0, int ch, float* s_x,
+                                            float* s_y) {
+  for (int idx = threadIdx.x; idx < kLR * kLR; idx += blockDim.x) {
+    const int r = idx / kLR, q = idx % kLR;
+    const int gy = y0 - kHalo + r, gx = x0 - kHalo + q;
     float xv = 0.f, yv = 0.f;
     if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-      const int64_t e = ((int64_t)gy * W + (x0 - 5)) * 3 + q;
+      const int64_t e = ((int64_t)gy * W + gx) * 3 + ch;
       xv = pred[e];
       yv = gt_u8 ? s_lut[gt_u8[e]] : gt_f32[e];
     }
-    s_x3[idx] = xv;
-    s_y3[idx] = yv;
+    s_x[r * kLP + q] = xv;
+    s_y[r * kLP + q] = yv;
   }
 }
 
@@ -128,66 +129,64 @@ __device__ __forceinline__ void hblur(const float (*v)[kLT][kLP], int r, int c0,
   }
 }
 
+// grid (tiles_x, tiles_y, 3): one CTA per 32x32 tile and channel
 __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
-  extern __shared__ float smem[];
-  float* s_x3 = smem;                      // 42 x 126 (3 interleaved channels)
-  float* s_y3 = s_x3 + kLR * 3 * kLR;
-  float (*s_v)[kLT][kLP] = reinterpret_cast<float (*)[kLT][kLP]>(s_y3 + kLR * 3 * kLR);
-  float* s_lut = reinterpret_cast<float*>(s_v + 5);
+  __shared__ float s_x[kLR * kLP];
+  __shared__ float s_y[kLR * kLP];
+  __shared__ float s_v[5][kLT][kLP];
+  __shared__ float s_lut[256];
   __shared__ double s_red[2][kLossThreads / 32];
-  const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
+  const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT, ch = blockIdx.z;
   const int W = a.width, H = a.height;
   const int64_t plane = (int64_t)W * H;
   if (a.gt_u8)
     for (int i = threadIdx.x; i < 256; i += kLossThreads) s_lut[i] = a.lut[i];
   __syncthreads();
-  load_region3(a.pred, a.gt_u8, s_lut, a.gt_f32, W, H, x0, y0, s_x3, s_y3);
+  load_region(a.pred, a.gt_u8, s_lut, a.gt_f32, W, H, x0, y0, ch, s_x, s_y);
+  __syncthreads();
+  // vertical pass (axis 0, loss.py:31) of x, y, xx, xy, yy
+  vblur<5>(s_v, [&](int r, int c, float* v) {
+    const float xv = s_x[r * kLP + c], yv = s_y[r * kLP + c];
+    v[0] = xv;
+    v[1] = yv;
+    v[2] = xv * xv;
+    v[3] = xv * yv;
+    v[4] = yv * yv;
+  });
+  __syncthreads();
+  // horizontal pass (axis 1, loss.py:32) + SSIM terms (loss.py:39-59)
   double l1 = 0.0, ss = 0.0;
-  for (int ch = 0; ch < 3; ++ch) {
-    __syncthreads();
-    // vertical pass (axis 0, loss.py:31) of x, y, xx, xy, yy
-    vblur<5>(s_v, [&](int r, int c, float* v) {
-      const float xv = s_x3[r * 3 * kLR + 3 * c + ch], yv = s_y3[r * 3 * kLR + 3 * c + ch];
-      v[0] = xv;
-      v[1] = yv;
-      v[2] = xv * xv;
-      v[3] = xv * yv;
-      v[4] = yv * yv;
-    });
-    __syncthreads();
-    // horizontal pass (axis 1, loss.py:32) + SSIM terms (loss.py:39-59)
-    {
-      const int r = threadIdx.x / (kLT / kHC), c0 = (threadIdx.x % (kLT / kHC)) * kHC;
-      float m[5][kHC];
-      hblur<5>(s_v, r, c0, m);
-      const int gy = y0 + r;
+  {
+    const int r = threadIdx.x / (kLT / kHC), c0 = (threadIdx.x % (kLT / kHC)) * kHC;
+    float m[5][kHC];
+    hblur<5>(s_v, r, c0, m);
+    const int gy = y0 + r;
 #pragma unroll
-      for (int i = 0; i < kHC; ++i) {
-        const int gx = x0 + c0 + i;
-        if (gy >= H || gx >= W) continue;
-        const float mu_x = m[0][i], mu_y = m[1][i], mxx = m[2][i], mxy = m[3][i], myy = m[4][i];
-        const float C1 = 1e-4f, C2 = 9e-4f;
-        const float sig_x = mxx - mu_x * mu_x;
-        const float sig_y = myy - mu_y * mu_y;
-        const float sig_xy = mxy - mu_x * mu_y;
-        const float a1 = 2.f * mu_x * mu_y + C1;
-        const float a2 = 2.f * sig_xy + C2;
-        const float b1 = mu_x * mu_x + mu_y * mu_y + C1;
-        const float b2 = sig_x + sig_y + C2;
-        const float inv_b2 = 1.f / b2;
-        const float inv_den = inv_b2 / b1;  // 1 / (b1 b2)
-        const float s = (a1 * a2) * inv_den;
-        const float ds_dmu = (2.f * mu_y * (a2 - a1) - 2.f * mu_x * s * (b2 - b1)) * inv_den;
-        const float ds_dmxx = -s * inv_b2;
-        const float ds_dmxy = 2.f * a1 * inv_den;
-        const int64_t pix = (int64_t)gy * W + gx;
-        a.maps[(0 * 3 + ch) * plane + pix] = ds_dmu;
-        a.maps[(1 * 3 + ch) * plane + pix] = ds_dmxx;
-        a.maps[(2 * 3 + ch) * plane + pix] = ds_dmxy;
-        ss += (double)s;
-        const int off = (r + kHalo) * 3 * kLR + 3 * (c0 + i + kHalo) + ch;
-        l1 += (double)fabsf(s_x3[off] - s_y3[off]);
-      }
+    for (int i = 0; i < kHC; ++i) {
+      const int gx = x0 + c0 + i;
+      if (gy >= H || gx >= W) continue;
+      const float mu_x = m[0][i], mu_y = m[1][i], mxx = m[2][i], mxy = m[3][i], myy = m[4][i];
+      const float C1 = 1e-4f, C2 = 9e-4f;
+      const float sig_x = mxx - mu_x * mu_x;
+      const float sig_y = myy - mu_y * mu_y;
+      const float sig_xy = mxy - mu_x * mu_y;
+      const float a1 = 2.f * mu_x * mu_y + C1;
+      const float a2 = 2.f * sig_xy + C2;
+      const float b1 = mu_x * mu_x + mu_y * mu_y + C1;
+      const float b2 = sig_x + sig_y + C2;
+      const float inv_b2 = 1.f / b2;
+      const float inv_den = inv_b2 / b1;  // 1 / (b1 b2)
+      const float s = (a1 * a2) * inv_den;
+      const float ds_dmu = (2.f * mu_y * (a2 - a1) - 2.f * mu_x * s * (b2 - b1)) * inv_den;
+      const float ds_dmxx = -s * inv_b2;
+      const float ds_dmxy = 2.f * a1 * inv_den;
+      const int64_t pix = (int64_t)gy * W + gx;
+      a.maps[(0 * 3 + ch) * plane + pix] = ds_dmu;
+      a.maps[(1 * 3 + ch) * plane + pix] = ds_dmxx;
+      a.maps[(2 * 3 + ch) * plane + pix] = ds_dmxy;
+      ss += (double)s;
+      const int off = (r + kHalo) * kLP + (c0 + i + kHalo);
+      l1 += (double)fabsf(s_x[off] - s_y[off]);
     }
   }
   // block reduction of the two sums (fixed order -> deterministic)
@@ -207,7 +206,7 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
       t0 += s_red[0][i];
       t1 += s_red[1][i];
     }
-    const int b = blockIdx.y * gridDim.x + blockIdx.x;
+    const int b = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     a.partials[2 * b] = t0;
     a.partials[2 * b + 1] = t1;
   }
@@ -220,43 +219,40 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, floa
   __shared__ float s_lut[256];
   if (a.gt_u8)
     for (int i = threadIdx.x; i < 256; i += kLossThreads) s_lut[i] = a.lut[i];
-  const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
+  const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT, ch = blockIdx.z;
   const int W = a.width, H = a.height;
   const int64_t plane = (int64_t)W * H;
   const float inv_n = 1.0f / (float)((double)plane * 3.0);
-  for (int ch = 0; ch < 3; ++ch) {
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < kLR * kLR; idx += kLossThreads) {
-      const int r = idx / kLR, q = idx % kLR;
-      const int gy = y0 - kHalo + r, gx = x0 - kHalo + q;
-      const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-      const int64_t pix = (int64_t)gy * W + gx;
+  for (int idx = threadIdx.x; idx < kLR * kLR; idx += kLossThreads) {
+    const int r = idx / kLR, q = idx % kLR;
+    const int gy = y0 - kHalo + r, gx = x0 - kHalo + q;
+    const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+    const int64_t pix = (int64_t)gy * W + gx;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) s_m[k][r][q] = in ? a.maps[(k * 3 + ch) * plane + pix] : 0.f;
-    }
-    __syncthreads();
-    vblur<3>(s_v, [&](int r, int c, float* v) {
-      v[0] = s_m[0][r][c];
-      v[1] = s_m[1][r][c];
-      v[2] = s_m[2][r][c];
-    });
-    __syncthreads();
-    const int r = threadIdx.x / (kLT / kHC), c0 = (threadIdx.x % (kLT / kHC)) * kHC;
-    float bl[3][kHC];
-    hblur<3>(s_v, r, c0, bl);
-    const int gy = y0 + r;
+    for (int k = 0; k < 3; ++k) s_m[k][r][q] = in ? a.maps[(k * 3 + ch) * plane + pix] : 0.f;
+  }
+  __syncthreads();
+  vblur<3>(s_v, [&](int r, int c, float* v) {
+    v[0] = s_m[0][r][c];
+    v[1] = s_m[1][r][c];
+    v[2] = s_m[2][r][c];
+  });
+  __syncthreads();
+  const int r = threadIdx.x / (kLT / kHC), c0 = (threadIdx.x % (kLT / kHC)) * kHC;
+  float bl[3][kHC];
+  hblur<3>(s_v, r, c0, bl);
+  const int gy = y0 + r;
 #pragma unroll
-    for (int i = 0; i < kHC; ++i) {
-      const int gx = x0 + c0 + i;
-      if (gy >= H || gx >= W) continue;
-      const int64_t e = ((int64_t)gy * W + gx) * 3 + ch;
-      const float x = a.pred[e];
-      const float y = gt_value(a.gt_u8, s_lut, a.gt_f32, e);
-      const float grad = (bl[0][i] + 2.f * x * bl[1][i] + y * bl[2][i]) * inv_n;
-      const float d = x - y;
-      const float sgn = (d > 0.f) ? 1.f : ((d < 0.f) ? -1.f : 0.f);
-      dimg[e] = (1.f - w_ssim) * sgn * inv_n - w_ssim * grad;
-    }
+  for (int i = 0; i < kHC; ++i) {
+    const int gx = x0 + c0 + i;
+    if (gy >= H || gx >= W) continue;
+    const int64_t e = ((int64_t)gy * W + gx) * 3 + ch;
+    const float x = a.pred[e];
+    const float y = gt_value(a.gt_u8, s_lut, a.gt_f32, e);
+    const float grad = (bl[0][i] + 2.f * x * bl[1][i] + y * bl[2][i]) * inv_n;
+    const float d = x - y;
+    const float sgn = (d > 0.f) ? 1.f : ((d < 0.f) ? -1.f : 0.f);
+    dimg[e] = (1.f - w_ssim) * sgn * inv_n - w_ssim * grad;
   }
 }
 
@@ -295,7 +291,7 @@ using namespace ss;
 
 extern "C" size_t ss_loss_workspace_bytes(int32_t width, int32_t height) {
   size_t plane = (size_t)width * height;
-  size_t nb = (size_t)((width + kLT - 1) / kLT) * ((height + kLT - 1) / kLT);
+  size_t nb = 3 * (size_t)((width + kLT - 1) / kLT) * ((height + kLT - 1) / kLT);
   return 9 * plane * sizeof(float) + 2 * nb * sizeof(double) + 256;
 }
 
@@ -308,19 +304,12 @@ extern "C" int ss_loss_l1_ssim(const float* pred, const uint8_t* gt_u8, const fl
   if (gt_u8 && !lut) return set_error(SS_ERR_INVALID, "ss_loss: u8 ground truth needs a LUT");
   if (ws_bytes < ss_loss_workspace_bytes(width, height))
     return set_error(SS_ERR_WORKSPACE, "ss_loss: workspace too small");
-  dim3 grid((width + kLT - 1) / kLT, (height + kLT - 1) / kLT);
+  dim3 grid((width + kLT - 1) / kLT, (height + kLT - 1) / kLT, 3);
   const size_t plane = (size_t)width * height;
   LossArgs a{pred, gt_u8, lut, gt_f32, width, height, (float*)ws,
              (double*)((char*)ws + ((9 * plane * sizeof(float) + 255) & ~(size_t)255))};
-  const size_t fwd_smem = sizeof(float) * (2 * kLR * 3 * kLR + 5 * kLT * kLP + 256);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ssim_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)fwd_smem);
-    attr = true;
-  }
-  ssim_fwd_kernel<<<grid, kLossThreads, fwd_smem, stream>>>(a);
+  ssim_fwd_kernel<<<grid, kLossThreads, 0, stream>>>(a);
   ssim_bwd_kernel<<<grid, kLossThreads, 0, stream>>>(a, (float)ssim_weight, dimg);
-  loss_reduce_kernel<<<1, 1024, 0, stream>>>(a.partials, grid.x * grid.y, out_sums);
+  loss_reduce_kernel<<<1, 1024, 0, stream>>>(a.partials, grid.x * grid.y * grid.z, out_sums);
   return check_launch("ss_loss_l1_ssim");
 }
