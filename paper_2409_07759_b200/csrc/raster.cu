@@ -52,6 +52,66 @@ __device__ __forceinline__ float rcp(float x) {
   return y;
 }
 
+// Packed fp32 pairs (Blackwell FFMA2 / FMUL2 / FADD2, PTX *.f32x2): a strip
+// lane's pixels k = 2p (low half) and 2p + 1 (high half) share one 64-bit
+// register pair, so the per-pixel blend arithmetic issues once per two
+// pixels.  A scalar operand broadcast with bc() folds into the instruction.
+typedef unsigned long long f2;
+
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo2(f2 r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  (void)b;
+  return a;
+}
+__device__ __forceinline__ float hi2(f2 r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  (void)a;
+  return b;
+}
+__device__ __forceinline__ f2 bc(float s) { return pk2(s, s); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// in-place accumulator forms (the result stays in the accumulator's registers)
+__device__ __forceinline__ void fma2_acc(f2& c, f2 a, f2 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void sub2_acc(f2& c, f2 a) {
+  asm("sub.rn.f32x2 %0, %0, %1;" : "+l"(c) : "l"(a));
+}
+__device__ __forceinline__ void mul2_acc(f2& c, f2 a) {
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(c) : "l"(a));
+}
+// (k, k + 1) and (k^2, (k + 1)^2) for pair p (k = 2p)
+__device__ __forceinline__ f2 kpair(int p) { return pk2((float)(2 * p), (float)(2 * p + 1)); }
+__device__ __forceinline__ f2 kkpair(int p) {
+  return pk2((float)(4 * p * p), (float)((2 * p + 1) * (2 * p + 1)));
+}
+
 struct WarpStage {
   float4 a[32];
   float4 b[32];
@@ -112,6 +172,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                       int32_t* __restrict__ n_contrib) {
   __shared__ WarpStage s_stage[kWarps];
   constexpr int WPT = kTile / (2 * STRIP);  // warps per tile
+  constexpr int NP = STRIP / 2;             // pixel pairs per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gwarp = blockIdx.x * kWarps + warp;
   const int slot_id = gwarp / WPT, sub = gwarp % WPT;
@@ -122,20 +183,23 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int px = tx * kTile + (lane & 15);
   const int py0 = ty * kTile + sub * 2 * STRIP + (lane >> 4) * STRIP;
   const float fx = (float)px, fy0 = (float)py0;
-  float T[STRIP], c0[STRIP], c1[STRIP], c2[STRIP];
+  f2 T[NP], c0[NP], c1[NP], c2[NP];
   int last[STRIP];
 #pragma unroll
-  for (int k = 0; k < STRIP; ++k) {
+  for (int p = 0; p < NP; ++p) {
     // pixels outside the image start "saturated" (T = 0) and never contribute
-    T[k] = (px < width && py0 + k < height) ? 1.f : 0.f;
-    c0[k] = c1[k] = c2[k] = 0.f;
-    last[k] = 0;
+    const float tl = (px < width && py0 + 2 * p < height) ? 1.f : 0.f;
+    const float th = (px < width && py0 + 2 * p + 1 < height) ? 1.f : 0.f;
+    T[p] = pk2(tl, th);
+    c0[p] = c1[p] = c2[p] = bc(0.f);
   }
+#pragma unroll
+  for (int k = 0; k < STRIP; ++k) last[k] = 0;
   const int2 rg = ranges[tile];
   for (int base = rg.x; base < rg.y; base += 32) {
     bool live = false;
 #pragma unroll
-    for (int k = 0; k < STRIP; ++k) live |= T[k] >= kTMin;
+    for (int p = 0; p < NP; ++p) live |= (lo2(T[p]) >= kTMin) | (hi2(T[p]) >= kTMin);
     if (!__any_sync(0xffffffffu, live)) break;
     __syncwarp();
     stage_load(st, lane, base + lane, rg.y, vals, rec_a, rec_b, rec_c);
@@ -149,40 +213,45 @@ __global__ void __launch_bounds__(kWarps * 32)
       const int pos = base - rg.x + j + 1;
       // exponents and validity of the whole strip first: a warp skips the
       // entry when none of its pixels is live and inside the maha <= 64 ellipse
-      float e[STRIP];
+      f2 e[NP];
       bool valid[STRIP];
       bool any = false;
 #pragma unroll
-      for (int k = 0; k < STRIP; ++k) {
-        e[k] = strip_exp(s, k);
-        valid[k] = (T[k] >= kTMin) && (e[k] >= s.thr);
-        any |= valid[k];
+      for (int p = 0; p < NP; ++p) {
+        e[p] = fma2(kkpair(p), bc(s.quad), fma2(kpair(p), bc(s.lin), bc(s.q0)));
+        valid[2 * p] = (lo2(T[p]) >= kTMin) && (lo2(e[p]) >= s.thr);
+        valid[2 * p + 1] = (hi2(T[p]) >= kTMin) && (hi2(e[p]) >= s.thr);
+        any |= valid[2 * p] | valid[2 * p + 1];
       }
-      if (!__any_sync(0xffffffffu, any)) continue;
+      (void)any;
       // branch-free over the strip: invalid pixels get alpha' = 0, which
-      // leaves C and T untouched, so the chains interleave freely
+      // leaves C and T untouched
 #pragma unroll
-      for (int k = 0; k < STRIP; ++k) {
-        const float ap = valid[k] ? fminf(ex2(e[k]), kAlphaMax) : 0.f;
-        const float w = ap * T[k];
-        c0[k] = fmaf(b.z, w, c0[k]);
-        c1[k] = fmaf(b.w, w, c1[k]);
-        c2[k] = fmaf(cb, w, c2[k]);
-        T[k] = fmaf(-ap, T[k], T[k]);
-        last[k] = valid[k] ? pos : last[k];
+      for (int p = 0; p < NP; ++p) {
+        const float al = valid[2 * p] ? fminf(ex2(lo2(e[p])), kAlphaMax) : 0.f;
+        const float ah = valid[2 * p + 1] ? fminf(ex2(hi2(e[p])), kAlphaMax) : 0.f;
+        const f2 w = mul2(pk2(al, ah), T[p]);
+        fma2_acc(c0[p], bc(b.z), w);
+        fma2_acc(c1[p], bc(b.w), w);
+        fma2_acc(c2[p], bc(cb), w);
+        sub2_acc(T[p], w);
+        last[2 * p] = valid[2 * p] ? pos : last[2 * p];
+        last[2 * p + 1] = valid[2 * p + 1] ? pos : last[2 * p + 1];
       }
     }
   }
 #pragma unroll
   for (int k = 0; k < STRIP; ++k) {
     const int py = py0 + k;
+    const int p = k >> 1;
+    const bool h = k & 1;
     if (px < width && py < height) {
-      const int64_t p = (int64_t)py * width + px;
-      img[3 * p] = c0[k];
-      img[3 * p + 1] = c1[k];
-      img[3 * p + 2] = c2[k];
-      t_final[p] = T[k];
-      n_contrib[p] = last[k];
+      const int64_t q = (int64_t)py * width + px;
+      img[3 * q] = h ? hi2(c0[p]) : lo2(c0[p]);
+      img[3 * q + 1] = h ? hi2(c1[p]) : lo2(c1[p]);
+      img[3 * q + 2] = h ? hi2(c2[p]) : lo2(c2[p]);
+      t_final[q] = h ? hi2(T[p]) : lo2(T[p]);
+      n_contrib[q] = last[k];
     }
   }
 }
@@ -274,26 +343,37 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int px = tx * kTile + (lane & 15);
   const int py0 = ty * kTile + sub * 2 * STRIP + (lane >> 4) * STRIP;
   const float fx = (float)px, fy0 = (float)py0;
-  float T[STRIP], d0[STRIP], d1[STRIP], d2[STRIP], Q[STRIP];
+  constexpr int NP = STRIP / 2;
+  // T: transmittance (after the current entry, walking back to front);
+  // nQ = -(suffix colour Q); dimg channels per pixel pair
+  f2 T[NP], d0[NP], d1[NP], d2[NP], nQ[NP];
   int last[STRIP];
   int my_max = 0;
 #pragma unroll
-  for (int k = 0; k < STRIP; ++k) {
-    const int py = py0 + k;
-    Q[k] = 0.f;
-    if (px < width && py < height) {
-      const int64_t p = (int64_t)py * width + px;
-      T[k] = t_final[p];
-      last[k] = n_contrib[p];
-      d0[k] = dimg[3 * p];
-      d1[k] = dimg[3 * p + 1];
-      d2[k] = dimg[3 * p + 2];
-    } else {
-      T[k] = 1.f;
-      last[k] = 0;
-      d0[k] = d1[k] = d2[k] = 0.f;
+  for (int p = 0; p < NP; ++p) {
+    float tv[2], dv0[2], dv1[2], dv2[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = 2 * p + h, py = py0 + k;
+      if (px < width && py < height) {
+        const int64_t q = (int64_t)py * width + px;
+        tv[h] = t_final[q];
+        last[k] = n_contrib[q];
+        dv0[h] = dimg[3 * q];
+        dv1[h] = dimg[3 * q + 1];
+        dv2[h] = dimg[3 * q + 2];
+      } else {
+        tv[h] = 1.f;
+        last[k] = 0;
+        dv0[h] = dv1[h] = dv2[h] = 0.f;
+      }
+      my_max = max(my_max, last[k]);
     }
-    my_max = max(my_max, last[k]);
+    T[p] = pk2(tv[0], tv[1]);
+    d0[p] = pk2(dv0[0], dv0[1]);
+    d1[p] = pk2(dv1[0], dv1[1]);
+    d2[p] = pk2(dv2[0], dv2[1]);
+    nQ[p] = bc(0.f);
   }
   const int2 rg = ranges[tile];
   const int walk_end = rg.x + __reduce_max_sync(0xffffffffu, my_max);
@@ -320,67 +400,73 @@ __global__ void __launch_bounds__(kWarps * 32)
       const float4 b = st.b[j];
       const float cb = st.c[j];
       const StripQuad s = strip_quad(a, b, fx, fy0);
-      float e[STRIP];
+      f2 e[NP];
       bool valid[STRIP];
       bool any = false;
 #pragma unroll
-      for (int k = 0; k < STRIP; ++k) {
-        e[k] = strip_exp(s, k);
-        valid[k] = (pos < last[k]) && (e[k] >= s.thr);
-        any |= valid[k];
+      for (int p = 0; p < NP; ++p) {
+        e[p] = fma2(kkpair(p), bc(s.quad), fma2(kpair(p), bc(s.lin), bc(s.q0)));
+        valid[2 * p] = (pos < last[2 * p]) && (lo2(e[p]) >= s.thr);
+        valid[2 * p + 1] = (pos < last[2 * p + 1]) && (hi2(e[p]) >= s.thr);
+        any |= valid[2 * p] | valid[2 * p + 1];
       }
       if (!__any_sync(0xffffffffu, any)) {
         if (DET && slot_ok) det.partial[(s_epos[warp][j] * WPT + sub) * 9 + slot] = 0.f;
         continue;
       }
-      float sc0, sc1, sc2, st0, st1, st2;
+      f2 nsc0, nsc1, nsc2, st0, st1, st2;
 #pragma unroll
-      for (int k = 0; k < STRIP; ++k) {
-        // branch-free: an invalid pixel has alpha' = 0 (T and Q unchanged) and
-        // a zero gradient weight g
-        const float aG = ex2(e[k]);
-        const float ap = valid[k] ? fminf(aG, kAlphaMax) : 0.f;
+      for (int p = 0; p < NP; ++p) {
+        // branch-free: an invalid pixel has alpha' = 0 (T and Q unchanged)
+        // and a zero gradient weight g
+        const float gl = ex2(lo2(e[p])), gh = ex2(hi2(e[p]));
+        const bool vl = valid[2 * p], vh = valid[2 * p + 1];
+        const f2 nap = pk2(vl ? fmaxf(-gl, -kAlphaMax) : 0.f, vh ? fmaxf(-gh, -kAlphaMax) : 0.f);
         // clamped splats pass no alpha/footprint gradient (_kernels.py:120-121)
-        const float g = (valid[k] && aG <= kAlphaMax) ? aG : 0.f;
-        const float inv = rcp(1.f - ap);
-        T[k] *= inv;  // T before this splat
-        const float w = ap * T[k];
-        const float dc = fmaf(d2[k], cb, fmaf(d1[k], b.w, d0[k] * b.z));
-        const float dap = fmaf(T[k], dc, -Q[k] * inv);
-        Q[k] = fmaf(w, dc, Q[k]);
-        const float t = g * dap;
-        if (k == 0) {
-          sc0 = d0[k] * w;
-          sc1 = d1[k] * w;
-          sc2 = d2[k] * w;
+        const f2 g = pk2((vl && gl <= kAlphaMax) ? gl : 0.f, (vh && gh <= kAlphaMax) ? gh : 0.f);
+        const f2 om = add2(bc(1.f), nap);  // 1 - alpha'
+        const f2 inv = pk2(rcp(lo2(om)), rcp(hi2(om)));
+        const f2 Ta = T[p];
+        mul2_acc(T[p], inv);                  // T before this splat
+        const f2 nw = mul2(nap, T[p]);        // -w
+        const f2 dc = fma2(d2[p], bc(cb), fma2(d1[p], bc(b.w), mul2(d0[p], bc(b.z))));
+        const f2 dap = mul2(inv, fma2(Ta, dc, nQ[p]));  // T dc - Q / (1 - alpha')
+        fma2_acc(nQ[p], nw, dc);
+        const f2 t = mul2(g, dap);
+        if (p == 0) {
+          nsc0 = mul2(d0[p], nw);
+          nsc1 = mul2(d1[p], nw);
+          nsc2 = mul2(d2[p], nw);
           st0 = t;
-          st1 = 0.f;
-          st2 = 0.f;
+          st1 = mul2(kpair(0), t);
+          st2 = mul2(kkpair(0), t);
         } else {
-          sc0 = fmaf(d0[k], w, sc0);
-          sc1 = fmaf(d1[k], w, sc1);
-          sc2 = fmaf(d2[k], w, sc2);
-          st0 += t;
-          st1 = k == 1 ? st1 + t : fmaf((float)k, t, st1);
-          st2 = k == 1 ? st2 + t : fmaf((float)(k * k), t, st2);
+          nsc0 = fma2(d0[p], nw, nsc0);
+          nsc1 = fma2(d1[p], nw, nsc1);
+          nsc2 = fma2(d2[p], nw, nsc2);
+          st0 = add2(st0, t);
+          st1 = fma2(kpair(p), t, st1);
+          st2 = fma2(kkpair(p), t, st2);
         }
       }
       // strip sums -> 9 gradient components; dm = -t/2, G d alpha' = t / alpha
+      const float s_t = lo2(st0) + hi2(st0), s_tk = lo2(st1) + hi2(st1),
+                  s_tkk = lo2(st2) + hi2(st2);
       const float i0 = a.z * kInvKappa, i1 = a.w * kInvKappa, i2 = b.x * kInvKappa;
       const float dx = s.dx, dy0 = s.dy0;
-      const float sdm = -0.5f * st0;
-      const float sdmy = -0.5f * fmaf(dy0, st0, st1);
-      const float sdmyy = -0.5f * fmaf(dy0, fmaf(dy0, st0, 2.f * st1), st2);
+      const float sdm = -0.5f * s_t;
+      const float sdmy = -0.5f * fmaf(dy0, s_t, s_tk);
+      const float sdmyy = -0.5f * fmaf(dy0, fmaf(dy0, s_t, 2.f * s_tk), s_tkk);
       float v[9];
       v[0] = -2.f * (i0 * dx * sdm + i1 * sdmy);
       v[1] = -2.f * (i1 * dx * sdm + i2 * sdmy);
       v[2] = dx * dx * sdm;
       v[3] = 2.f * dx * sdmy;
       v[4] = sdmyy;
-      v[5] = st0 * ex2(-b.y);
-      v[6] = sc0;
-      v[7] = sc1;
-      v[8] = sc2;
+      v[5] = s_t * ex2(-b.y);
+      v[6] = -(lo2(nsc0) + hi2(nsc0));
+      v[7] = -(lo2(nsc1) + hi2(nsc1));
+      v[8] = -(lo2(nsc2) + hi2(nsc2));
       const float tot = reduce9(v, lane);
       if (slot_ok) {
         if (DET) det.partial[(s_epos[warp][j] * WPT + sub) * 9 + slot] = tot;
