@@ -144,7 +144,8 @@ int ss_tile_ranges(const uint32_t* sorted_keys, int64_t n_pairs, int32_t n_tiles
  * over chunks and tiles (-> ranges); then each chunk's pairs are written,
  * in emit order, to vals_out at their tile's slots.
  * offsets = ss_tile_offsets' output, n_pairs = K = offsets[n].  Usable when
- * ss_bin_tiles_supported(K, tiles) (shared-memory cursors: <= 18432 tiles). */
+ * ss_bin_tiles_supported(K, tiles) (shared-memory cursors: <= 18432 tiles,
+ * e.g. 1920x1080 = 8160 tiles). */
 size_t ss_bin_tiles_workspace_bytes(int64_t n_pairs, int32_t n_tiles);
 int32_t ss_bin_tiles_supported(int64_t n_pairs, int32_t n_tiles);
 int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const int32_t* bbox,
