@@ -192,7 +192,8 @@ int ss_raster_bwd_deterministic(const int32_t* ranges, const int32_t* vals, cons
 int ss_set_raster_strip(int32_t strip);
 
 /* ---- a-6 blend backward: _kernels.py:56-130.  Accumulates into g2d
- * (n x 12 floats: g_mean2d[2] g_inv2d[3] g_alpha g_color[3] pad[3]),
+ * (n x 12 floats: the 9 basis sums t dx, t dy, t dx^2, t dx dy, t dy^2, t,
+ * colour[3] over the splat's (pixel, entry) slots, t = alpha G d alpha', pad[3]),
  * which the caller zeroes. */
 int ss_raster_bwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                   const void* rec_b, const float* rec_c, int32_t width, int32_t height,

@@ -188,12 +188,19 @@ __global__ void project_bwd_kernel(StoreView store, const int32_t* __restrict__ 
   load_row(store, row, g);
   Proj p;
   project_one(cam, g, p);
+  // g2d holds the rasterizer's basis sums over every (pixel, entry) of this
+  // splat (raster.cu): W = (t dx, t dy, t dx^2, t dx dy, t dy^2, t, colour[3])
+  // with t = alpha G d alpha'.  With dm = -t/2 and the conic (i0, i1, i2):
+  //   d mean2d = (i0 W0 + i1 W1, i1 W0 + i2 W1),  d inv2d = -(W2/2, W3, W4/2),
+  //   d alpha = W5 / alpha, so d logit = W5 (1 - alpha)   (raster.py:231-246)
   const float* gg = g2d + (int64_t)i * SS_G2D_ROW;
-  const double gm2x = gg[0], gm2y = gg[1];
-  const double gia = gg[2], gib = gg[3], gic = gg[4];
-  const double g_alpha = gg[5];
   const double ad = p.a + kDilation, cd = p.c + kDilation, b = p.b;
   const double det = ad * cd - b * b;
+  const double ci0 = cd / det, ci1 = -b / det, ci2 = ad / det;
+  const double W0 = gg[0], W1 = gg[1];
+  const double gm2x = ci0 * W0 + ci1 * W1, gm2y = ci1 * W0 + ci2 * W1;
+  const double gia = -0.5 * gg[2], gib = -(double)gg[3], gic = -0.5 * gg[4];
+  const double g_alpha_x_alpha = gg[5];  // d alpha times alpha
   const double det2 = det * det;
   // raster.py:262-266
   const double g_a = (gia * (-cd * cd) + gib * (b * cd) + gic * (-b * b)) / det2;
@@ -277,7 +284,7 @@ __global__ void project_bwd_kernel(StoreView store, const int32_t* __restrict__ 
 #pragma unroll
   for (int qi = 0; qi < 4; ++qi) out[3 + qi] = (float)((gqn[qi] - p.qn[qi] * dot) / p.qnorm);
   // raster.py:336-343
-  out[10] = (float)(g_alpha * g.opacity * (1.0 - g.opacity));
+  out[10] = (float)(g_alpha_x_alpha * (1.0 - g.opacity));  // d alpha * alpha (1 - alpha)
   out[11] = gg[6];
   out[12] = gg[7];
   out[13] = gg[8];

@@ -29,8 +29,10 @@
 // carries the scalar Q = dC . S (Q += w dC . c) and d alpha' = T dC.c - Q/(1-a').
 // With t = alpha G d alpha' (zero when clamped), g_alpha = sum t / alpha and
 // dm = -t/2, and the strip sums sum t, sum t k, sum t k^2 give every
-// footprint gradient; one 12-shuffle transposed warp reduction and one 9-lane float
-// atomic per (warp, entry).
+// footprint gradient.  g2d receives the 9 linear basis sums (see the strip
+// epilogue) that ss_project_bwd turns into mean2d / conic / alpha gradients;
+// one 12-shuffle transposed warp reduction and one 9-lane float atomic per
+// (warp, entry).
 #include "ss_common.cuh"
 
 namespace ss {
@@ -449,21 +451,22 @@ __global__ void __launch_bounds__(kWarps * 32)
           st2 = fma2(kkpair(p), t, st2);
         }
       }
-      // strip sums -> 9 gradient components; dm = -t/2, G d alpha' = t / alpha
+      // strip sums -> the 9 basis sums of the footprint gradient (with
+      // dy = dy0 + k):  t dx, t dy, t dx^2, t dx dy, t dy^2, t, colour.  The
+      // per-splat constants (the conic, 1/alpha) are applied once per splat
+      // in ss_project_bwd, so only lane-dependent factors are formed here.
       const float s_t = lo2(st0) + hi2(st0), s_tk = lo2(st1) + hi2(st1),
                   s_tkk = lo2(st2) + hi2(st2);
-      const float i0 = a.z * kInvKappa, i1 = a.w * kInvKappa, i2 = b.x * kInvKappa;
       const float dx = s.dx, dy0 = s.dy0;
-      const float sdm = -0.5f * s_t;
-      const float sdmy = -0.5f * fmaf(dy0, s_t, s_tk);
-      const float sdmyy = -0.5f * fmaf(dy0, fmaf(dy0, s_t, 2.f * s_tk), s_tkk);
+      const float s_dy = fmaf(dy0, s_t, s_tk);                               // sum t dy
+      const float s_dyy = fmaf(dy0, fmaf(dy0, s_t, s_tk + s_tk), s_tkk);     // sum t dy^2
       float v[9];
-      v[0] = -2.f * (i0 * dx * sdm + i1 * sdmy);
-      v[1] = -2.f * (i1 * dx * sdm + i2 * sdmy);
-      v[2] = dx * dx * sdm;
-      v[3] = 2.f * dx * sdmy;
-      v[4] = sdmyy;
-      v[5] = s_t * ex2(-b.y);
+      v[0] = dx * s_t;
+      v[1] = s_dy;
+      v[2] = dx * v[0];
+      v[3] = dx * s_dy;
+      v[4] = s_dyy;
+      v[5] = s_t;
       v[6] = -(lo2(nsc0) + hi2(nsc0));
       v[7] = -(lo2(nsc1) + hi2(nsc1));
       v[8] = -(lo2(nsc2) + hi2(nsc2));
