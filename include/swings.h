@@ -115,6 +115,33 @@ int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_t n, const 
                    void* rec_a, void* rec_b, float* rec_c, uint64_t* depth_key, int32_t* bbox,
                    int32_t* n_tiles, float* geom, uint64_t* tile_mask, ss_stream_t stream);
 
+/* ---- a-5 / a-6 on already projected 2D splats (the reference's
+ * _kernels.blend_forward / blend_backward, _kernels.py:20-130): fp64 arrays
+ * mean2d (n,2), inv2d (n,3), alpha (n), color (n,3); bbox (n,4) int32
+ * (x0, x1, y0, y1, half open); rank[i] = position of splat i in the blend
+ * order (-1: not blended; ranks distinct). */
+typedef struct {
+  const double* mean2d;
+  const double* inv2d;
+  const double* alpha;
+  const double* color;
+  const int32_t* bbox;
+  const int32_t* rank;
+  int32_t n;
+  int32_t pad;
+} ss_splats2d;
+/* Records, depth keys (= rank), clipped bbox, kept tiles -- ss_project_fwd's
+ * outputs for 2D input. */
+int ss_records_2d(const ss_splats2d* splats, int32_t width, int32_t height, void* rec_a,
+                  void* rec_b, float* rec_c, uint64_t* depth_key, int32_t* bbox,
+                  int32_t* n_tiles, float* geom, uint64_t* tile_mask, ss_stream_t stream);
+/* Adds the 2D gradients of the raster backward's basis sums g2d (see
+ * ss_raster_bwd) into g_mean2d (n,2), g_inv2d (n,3), g_alpha (n),
+ * g_color (n,3), fp64 device arrays (blend_backward's += contract). */
+int ss_basis_to_2d(const float* g2d, const ss_splats2d* splats, const void* rec_b,
+                   const uint64_t* depth_key, double* g_mean2d, double* g_inv2d, double* g_alpha,
+                   double* g_color, ss_stream_t stream);
+
 /* ---- a-4 binning: raster.py:153 global (z, src) order reproduced per tile.
  * (1) stable radix sort of the 64-bit depth keys -> order (rank -> i);
  * (2) tile counts in rank order, exclusive scan -> offsets[0..n], K = offsets[n];
@@ -297,6 +324,17 @@ typedef struct {
  * SS_ERR_CAPACITY (K in v->n_pairs) when K > pair_cap, SS_ERR_WORKSPACE
  * (size in v->ws_needed) when ws is too small; call again after growing. */
 int ss_render_fwd(const ss_store* store, const ss_camera* cam, ss_view* v, ss_stream_t stream);
+/* The same view pipeline on 2D splats (_kernels.blend_forward, _kernels.py:20-53):
+ * records from splats (blend order = rank), then as ss_render_fwd, with the
+ * per-pixel bbox test of _kernels.py:35-36 applied explicitly.  Sets v->n. */
+int ss_render2d_fwd(const ss_splats2d* splats, int32_t width, int32_t height, ss_view* v,
+                    ss_stream_t stream);
+/* _kernels.blend_backward (_kernels.py:56-130) for the view ss_render2d_fwd
+ * left in v: adds the 2D gradients into g_mean2d / g_inv2d / g_alpha /
+ * g_color (fp64 device arrays); g2d (n x 12 floats) is scratch. */
+int ss_render2d_bwd(const ss_splats2d* splats, int32_t width, int32_t height, const ss_view* v,
+                    const float* dimg, float* g2d, double* g_mean2d, double* g_inv2d,
+                    double* g_alpha, double* g_color, ss_stream_t stream);
 /* Raster backward -> projection backward for the view ss_render_fwd left in v;
  * g2d (n x 12 floats) is zeroed here; grads are accumulated (caller zeroes). */
 int ss_render_bwd(const ss_store* store, const ss_camera* cam, const ss_view* v,

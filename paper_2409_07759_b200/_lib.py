@@ -57,6 +57,11 @@ class SSView(Structure):
                 ("sorted_sel", c_int32), ("pad1", c_int32), ("events", P * 4),
                 ("partial", P), ("rank", P)]
 
+class SSSplats2D(Structure):
+    _fields_ = [("mean2d", P), ("inv2d", P), ("alpha", P), ("color", P), ("bbox", P),
+                ("rank", P), ("n", c_int32), ("pad", c_int32)]
+
+
 _SIGNATURES = {
     "ss_last_error": ([], ctypes.c_char_p),
     "ss_version": ([], c_int),
@@ -94,6 +99,11 @@ _SIGNATURES = {
                     c_int),
     "ss_to_direct": ([P, P, I64, P], c_int),
     "ss_render_fwd": ([POINTER(SSStore), POINTER(SSCamera), POINTER(SSView), P], c_int),
+    "ss_render2d_fwd": ([POINTER(SSSplats2D), I32, I32, POINTER(SSView), P], c_int),
+    "ss_render2d_bwd": ([POINTER(SSSplats2D), I32, I32, POINTER(SSView), P, P, P, P, P, P, P],
+                        c_int),
+    "ss_records_2d": ([POINTER(SSSplats2D), I32, I32, P, P, P, P, P, P, P, P, P], c_int),
+    "ss_basis_to_2d": ([P, POINTER(SSSplats2D), P, P, P, P, P, P, P], c_int),
     "ss_render_bwd": ([POINTER(SSStore), POINTER(SSCamera), POINTER(SSView), P, P, P, I64, P, P],
                       c_int),
     "ss_event_create": ([POINTER(P)], c_int),

@@ -104,6 +104,65 @@ __device__ __forceinline__ void project_one(const CamK& cam, const Gauss64& g, P
   p.keep = in_front && on_image;
 }
 
+// Everything a-4 / a-5 need from one kept splat: the fp32 binning geometry,
+// the exact kept-tile count and mask of its bbox, the depth key and the
+// rasterizer record (raster.cu: conic pre-scaled by kappa = -log2(e)/2 so
+// alpha G = 2^(kappa m + log2 alpha); alpha floored at 2^-100).
+__device__ __forceinline__ void write_record(int i, double ux, double uy, double i0, double i1,
+                                             double i2, int x0, int x1, int y0, int y1,
+                                             double opacity, const double* color, uint64_t key,
+                                             float4* __restrict__ rec_a, float4* __restrict__ rec_b,
+                                             float* __restrict__ rec_c,
+                                             uint64_t* __restrict__ depth_key,
+                                             int4* __restrict__ bbox, int32_t* __restrict__ n_tiles,
+                                             float* __restrict__ geom,
+                                             uint64_t* __restrict__ tile_mask) {
+  bbox[i] = make_int4(x0, x1, y0, y1);
+  const float fi0 = __double2float_rn(i0), fi2 = __double2float_rn(i2);
+  float gl[kGeom] = {__double2float_rn(ux), __double2float_rn(uy), fi0,
+                     __double2float_rn(i1), fi2, __frcp_rn(fi0), __frcp_rn(fi2), 0.0f};
+  float* gm = geom + (int64_t)i * kGeom;
+#pragma unroll
+  for (int c = 0; c < kGeom; ++c) gm[c] = gl[c];
+  int nt = 0;
+  uint64_t mask = 0;
+  if (x1 > x0 && y1 > y0) {
+    // tiles of the bbox that the maha <= 64 ellipse actually reaches; the
+    // first 64 (row-major in the bbox tile rectangle) are also recorded as a
+    // bit mask so the binning does not repeat the test
+    const int4 bb = make_int4(x0, x1, y0, y1);
+    const int tx0 = x0 / kTile, tx1 = (x1 - 1) / kTile + 1;
+    const int ty0 = y0 / kTile, ty1 = (y1 - 1) / kTile + 1;
+    int j = 0;
+    for (int ty = ty0; ty < ty1; ++ty)
+      for (int tx = tx0; tx < tx1; ++tx, ++j) {
+        const bool keep = tile_keeps(gl, tx, ty, bb);
+        nt += keep;
+        if (keep && j < 64) mask |= 1ull << j;
+      }
+  }
+  tile_mask[i] = mask;
+  n_tiles[i] = nt;
+  depth_key[i] = key;
+  const double kappa = -0.72134752044448170368;
+  const double l2a = fmax(log2(opacity), -100.0);
+  rec_a[i] = make_float4((float)ux, (float)uy, (float)(kappa * i0), (float)(kappa * i1));
+  rec_b[i] = make_float4((float)(kappa * i2), (float)l2a, (float)color[0], (float)color[1]);
+  rec_c[i] = (float)color[2];
+}
+
+__device__ __forceinline__ void write_culled(int i, float4* rec_a, float4* rec_b, float* rec_c,
+                                             uint64_t* depth_key, int4* bbox, int32_t* n_tiles,
+                                             uint64_t* tile_mask) {
+  depth_key[i] = ~0ull;
+  n_tiles[i] = 0;
+  tile_mask[i] = 0;
+  bbox[i] = make_int4(0, 0, 0, 0);
+  rec_a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  rec_b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  rec_c[i] = 0.f;
+}
+
 __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ rows, int32_t n,
                                    CamK cam, float4* __restrict__ rec_a,
                                    float4* __restrict__ rec_b, float* __restrict__ rec_c,
@@ -118,12 +177,7 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
   Proj p;
   project_one(cam, g, p);
   if (!p.keep) {
-    depth_key[i] = ~0ull;
-    n_tiles[i] = 0;
-    bbox[i] = make_int4(0, 0, 0, 0);
-    rec_a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    rec_b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    rec_c[i] = 0.f;
+    write_culled(i, rec_a, rec_b, rec_c, depth_key, bbox, n_tiles, tile_mask);
     return;
   }
   // raster.py:139-150  dilation, conic, 8-sigma bbox of the dilated covariance
@@ -137,40 +191,58 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
   const int x1 = (int)fmin(dadd(floor(dadd(p.ux, r8)), 1.0), (double)cam.width);
   const int y0 = (int)fmax(ceil(dsub(p.uy, r8)), 0.0);
   const int y1 = (int)fmin(dadd(floor(dadd(p.uy, r8)), 1.0), (double)cam.height);
-  bbox[i] = make_int4(x0, x1, y0, y1);
-  const float fi0 = __double2float_rn(i0), fi2 = __double2float_rn(i2);
-  float gl[kGeom] = {__double2float_rn(p.ux), __double2float_rn(p.uy), fi0,
-                     __double2float_rn(i1), fi2, __frcp_rn(fi0), __frcp_rn(fi2), 0.0f};
-  float* gm = geom + (int64_t)i * kGeom;
-#pragma unroll
-  for (int c = 0; c < kGeom; ++c) gm[c] = gl[c];
-  int nt = 0;
-  uint64_t mask = 0;
-  if (x1 > x0 && y1 > y0) {
-    // tiles of the 8-sigma bbox that the maha <= 64 ellipse actually reaches;
-    // the first 64 (row-major in the bbox tile rectangle) are also recorded as
-    // a bit mask so the emit pass does not repeat the test
-    const int4 bb = make_int4(x0, x1, y0, y1);
-    const int tx0 = x0 / kTile, tx1 = (x1 - 1) / kTile + 1;
-    const int ty0 = y0 / kTile, ty1 = (y1 - 1) / kTile + 1;
-    int j = 0;
-    for (int ty = ty0; ty < ty1; ++ty)
-      for (int tx = tx0; tx < tx1; ++tx, ++j) {
-        const bool keep = tile_keeps(gl, tx, ty, bb);
-        nt += keep;
-        if (keep && j < 64) mask |= 1ull << j;
-      }
+  // z > 0.01: the fp64 bits are monotone
+  write_record(i, p.ux, p.uy, i0, i1, i2, x0, x1, y0, y1, g.opacity, g.color,
+               (uint64_t)__double_as_longlong(p.z), rec_a, rec_b, rec_c, depth_key, bbox, n_tiles,
+               geom, tile_mask);
+}
+
+// _kernels.blend_forward's inputs (already projected 2D splats, the blend
+// order given as a rank per splat, -1 = not blended): same records, bbox
+// clipped to the image, depth key = rank.
+__global__ void records2d_kernel(const double* __restrict__ mean2d, const double* __restrict__ inv2d,
+                                 const double* __restrict__ alpha, const double* __restrict__ color,
+                                 const int4* __restrict__ bbox_in, const int32_t* __restrict__ rank,
+                                 int32_t n, int32_t width, int32_t height, float4* __restrict__ rec_a,
+                                 float4* __restrict__ rec_b, float* __restrict__ rec_c,
+                                 uint64_t* __restrict__ depth_key, int4* __restrict__ bbox,
+                                 int32_t* __restrict__ n_tiles, float* __restrict__ geom,
+                                 uint64_t* __restrict__ tile_mask) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (rank[i] < 0) {
+    write_culled(i, rec_a, rec_b, rec_c, depth_key, bbox, n_tiles, tile_mask);
+    return;
   }
-  tile_mask[i] = mask;
-  n_tiles[i] = nt;
-  depth_key[i] = (uint64_t)__double_as_longlong(p.z);  // z > 0.01: bits are monotone
-  // rasterizer record (raster.cu): conic pre-scaled by kappa = -log2(e)/2 so
-  // alpha G = 2^(kappa m + log2 alpha); alpha floored at 2^-100
-  const double kappa = -0.72134752044448170368;
-  const double l2a = fmax(log2(g.opacity), -100.0);
-  rec_a[i] = make_float4((float)p.ux, (float)p.uy, (float)(kappa * i0), (float)(kappa * i1));
-  rec_b[i] = make_float4((float)(kappa * i2), (float)l2a, (float)g.color[0], (float)g.color[1]);
-  rec_c[i] = (float)g.color[2];
+  const int4 b = bbox_in[i];
+  const int x0 = max(b.x, 0), x1 = min(b.y, width), y0 = max(b.z, 0), y1 = min(b.w, height);
+  write_record(i, mean2d[2 * i], mean2d[2 * i + 1], inv2d[3 * i], inv2d[3 * i + 1], inv2d[3 * i + 2],
+               x0, max(x0, x1), y0, max(y0, y1), alpha[i], color + 3 * i, (uint64_t)rank[i], rec_a,
+               rec_b, rec_c, depth_key, bbox, n_tiles, geom, tile_mask);
+}
+
+// Basis sums (raster.cu) -> _kernels.blend_backward's 2D gradients, added
+// into the caller's arrays.  t = alpha' G d alpha' with alpha' the record's
+// alpha (floored at 2^-100), so d alpha = W5 / alpha' (finite for alpha = 0).
+__global__ void basis_to_2d_kernel(const float* __restrict__ g2d, const double* __restrict__ inv2d,
+                                   const float4* __restrict__ rec_b, const uint64_t* __restrict__ key,
+                                   int32_t n, double* __restrict__ g_mean2d,
+                                   double* __restrict__ g_inv2d, double* __restrict__ g_alpha,
+                                   double* __restrict__ g_color) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || key[i] == ~0ull) return;
+  const float* w = g2d + (int64_t)i * SS_G2D_ROW;
+  const double i0 = inv2d[3 * i], i1 = inv2d[3 * i + 1], i2 = inv2d[3 * i + 2];
+  const double W0 = w[0], W1 = w[1];
+  g_mean2d[2 * i] += i0 * W0 + i1 * W1;
+  g_mean2d[2 * i + 1] += i1 * W0 + i2 * W1;
+  g_inv2d[3 * i] += -0.5 * (double)w[2];
+  g_inv2d[3 * i + 1] += -(double)w[3];
+  g_inv2d[3 * i + 2] += -0.5 * (double)w[4];
+  g_alpha[i] += (double)w[5] * exp2(-(double)rec_b[i].y);
+  g_color[3 * i] += w[6];
+  g_color[3 * i + 1] += w[7];
+  g_color[3 * i + 2] += w[8];
 }
 
 __global__ void project_bwd_kernel(StoreView store, const int32_t* __restrict__ rows, int32_t n,
@@ -322,6 +394,30 @@ extern "C" int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_
       sv, rows, n, to_camk(cam), (float4*)rec_a, (float4*)rec_b, rec_c, depth_key, (int4*)bbox,
       n_tiles, geom, tile_mask);
   return check_launch("ss_project_fwd");
+}
+
+extern "C" int ss_records_2d(const ss_splats2d* sp, int32_t width, int32_t height, void* rec_a,
+                             void* rec_b, float* rec_c, uint64_t* depth_key, int32_t* bbox,
+                             int32_t* n_tiles, float* geom, uint64_t* tile_mask,
+                             cudaStream_t stream) {
+  if (!sp || sp->n < 0 || width <= 0 || height <= 0)
+    return set_error(SS_ERR_INVALID, "ss_records_2d: bad arguments");
+  if (sp->n == 0) return SS_OK;
+  records2d_kernel<<<grid_for(sp->n, 128), 128, 0, stream>>>(
+      sp->mean2d, sp->inv2d, sp->alpha, sp->color, (const int4*)sp->bbox, sp->rank, sp->n, width,
+      height, (float4*)rec_a, (float4*)rec_b, rec_c, depth_key, (int4*)bbox, n_tiles, geom,
+      tile_mask);
+  return check_launch("ss_records_2d");
+}
+
+extern "C" int ss_basis_to_2d(const float* g2d, const ss_splats2d* sp, const void* rec_b,
+                              const uint64_t* depth_key, double* g_mean2d, double* g_inv2d,
+                              double* g_alpha, double* g_color, cudaStream_t stream) {
+  if (!sp || sp->n < 0) return set_error(SS_ERR_INVALID, "ss_basis_to_2d: bad arguments");
+  if (sp->n == 0) return SS_OK;
+  basis_to_2d_kernel<<<grid_for(sp->n, 128), 128, 0, stream>>>(
+      g2d, sp->inv2d, (const float4*)rec_b, depth_key, sp->n, g_mean2d, g_inv2d, g_alpha, g_color);
+  return check_launch("ss_basis_to_2d");
 }
 
 extern "C" int ss_project_bwd(const ss_store* store, const int32_t* rows, int32_t n,

@@ -164,14 +164,18 @@ __device__ __forceinline__ float strip_exp(const StripQuad& s, int k) {
   return fmaf((float)(k * k), s.quad, fmaf((float)k, s.lin, s.q0));
 }
 
-template <int STRIP>
+// BB: also apply an explicit per-splat pixel bbox (pbox, x0 x1 y0 y1 half
+// open) -- _kernels.blend_forward's bbox test for 2D input whose bbox need
+// not enclose the maha <= 64 ellipse.  Off for the training path, where the
+// 8-sigma bbox is implied by the maha cut.
+template <int STRIP, bool BB = false>
 __global__ void __launch_bounds__(kWarps * 32)
     raster_fwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
                       const float4* __restrict__ rec_a, const float4* __restrict__ rec_b,
                       const float* __restrict__ rec_c, int width, int height, int tiles_x,
                       int n_tiles, const int32_t* __restrict__ tile_order,
                       float* __restrict__ img, float* __restrict__ t_final,
-                      int32_t* __restrict__ n_contrib) {
+                      int32_t* __restrict__ n_contrib, const int4* __restrict__ pbox = nullptr) {
   __shared__ WarpStage s_stage[kWarps];
   constexpr int WPT = kTile / (2 * STRIP);  // warps per tile
   constexpr int NP = STRIP / 2;             // pixel pairs per lane
@@ -218,11 +222,18 @@ __global__ void __launch_bounds__(kWarps * 32)
       f2 e[NP];
       bool valid[STRIP];
       bool any = false;
+      int4 q = make_int4(0, 0, 0, 0);
+      if (BB) q = __ldg(pbox + st.g[j]);
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         e[p] = fma2(kkpair(p), bc(s.quad), fma2(kpair(p), bc(s.lin), bc(s.q0)));
         valid[2 * p] = (lo2(T[p]) >= kTMin) && (lo2(e[p]) >= s.thr);
         valid[2 * p + 1] = (hi2(T[p]) >= kTMin) && (hi2(e[p]) >= s.thr);
+        if (BB) {
+          const bool xin = px >= q.x && px < q.y;
+          valid[2 * p] &= xin && py0 + 2 * p >= q.z && py0 + 2 * p < q.w;
+          valid[2 * p + 1] &= xin && py0 + 2 * p + 1 >= q.z && py0 + 2 * p + 1 < q.w;
+        }
         any |= valid[2 * p] | valid[2 * p + 1];
       }
       (void)any;
@@ -323,7 +334,7 @@ __device__ __forceinline__ int64_t emit_position(const DetArgs& d, int g, int tx
   return (int64_t)d.offsets[d.rank[g]] + j;
 }
 
-template <int STRIP, bool DET>
+template <int STRIP, bool DET, bool BB = false>
 __global__ void __launch_bounds__(kWarps * 32)
     raster_bwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
                       const float4* __restrict__ rec_a, const float4* __restrict__ rec_b,
@@ -331,7 +342,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                       int n_tiles, const int32_t* __restrict__ tile_order,
                       const float* __restrict__ dimg, const float* __restrict__ t_final,
                       const int32_t* __restrict__ n_contrib, float* __restrict__ g2d,
-                      DetArgs det) {
+                      DetArgs det, const int4* __restrict__ pbox = nullptr) {
   __shared__ int64_t s_epos[kWarps][32];
   __shared__ WarpStage s_stage[kWarps];
   constexpr int WPT = kTile / (2 * STRIP);
@@ -405,11 +416,18 @@ __global__ void __launch_bounds__(kWarps * 32)
       f2 e[NP];
       bool valid[STRIP];
       bool any = false;
+      int4 q = make_int4(0, 0, 0, 0);
+      if (BB) q = __ldg(pbox + st.g[j]);
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         e[p] = fma2(kkpair(p), bc(s.quad), fma2(kpair(p), bc(s.lin), bc(s.q0)));
         valid[2 * p] = (pos < last[2 * p]) && (lo2(e[p]) >= s.thr);
         valid[2 * p + 1] = (pos < last[2 * p + 1]) && (hi2(e[p]) >= s.thr);
+        if (BB) {
+          const bool xin = px >= q.x && px < q.y;
+          valid[2 * p] &= xin && py0 + 2 * p >= q.z && py0 + 2 * p < q.w;
+          valid[2 * p + 1] &= xin && py0 + 2 * p + 1 >= q.z && py0 + 2 * p + 1 < q.w;
+        }
         any |= valid[2 * p] | valid[2 * p + 1];
       }
       if (!__any_sync(0xffffffffu, any)) {
@@ -571,6 +589,36 @@ extern "C" int ss_raster_bwd(const int32_t* ranges, const int32_t* vals, const v
                              const int32_t* n_contrib, float* g2d, cudaStream_t stream) {
   return raster_bwd_launch(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, dimg,
                            t_final, n_contrib, g2d, nullptr, stream);
+}
+
+// Raster forward / backward with the explicit per-pixel bbox test (the 2D
+// path of the view driver; strip 4).
+int raster_fwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                    const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                    const int32_t* tile_order, float* img, float* t_final, int32_t* n_contrib,
+                    const int32_t* pbox, cudaStream_t stream) {
+  const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+  const int n_tiles = tiles_x * tiles_y;
+  const int blocks = (n_tiles * 2 + kWarps - 1) / kWarps;
+  raster_fwd_kernel<4, true><<<blocks, kWarps * 32, 0, stream>>>(
+      (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
+      tiles_x, n_tiles, tile_order, img, t_final, n_contrib, (const int4*)pbox);
+  return check_launch("raster_fwd_bbox");
+}
+
+int raster_bwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                    const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                    const int32_t* tile_order, const float* dimg, const float* t_final,
+                    const int32_t* n_contrib, float* g2d, const int32_t* pbox,
+                    cudaStream_t stream) {
+  const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+  const int n_tiles = tiles_x * tiles_y;
+  const int blocks = (n_tiles * 2 + kWarps - 1) / kWarps;
+  const DetArgs d{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  raster_bwd_kernel<4, false, true><<<blocks, kWarps * 32, 0, stream>>>(
+      (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
+      tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d, (const int4*)pbox);
+  return check_launch("raster_bwd_bbox");
 }
 
 extern "C" int64_t ss_raster_partial_floats(int64_t n_pairs) {

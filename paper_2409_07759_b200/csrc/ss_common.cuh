@@ -149,3 +149,15 @@ __device__ __forceinline__ double u01_53(uint32_t a, uint32_t b) {
 }
 
 }  // namespace ss
+
+// raster.cu: rasterizer launches with the explicit per-pixel bbox test (the
+// 2D-input path of the view driver, csrc/view.cu)
+int raster_fwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                    const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                    const int32_t* tile_order, float* img, float* t_final, int32_t* n_contrib,
+                    const int32_t* pbox, cudaStream_t stream);
+int raster_bwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                    const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                    const int32_t* tile_order, const float* dimg, const float* t_final,
+                    const int32_t* n_contrib, float* g2d, const int32_t* pbox,
+                    cudaStream_t stream);

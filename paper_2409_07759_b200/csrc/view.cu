@@ -52,11 +52,13 @@ extern "C" int ss_event_elapsed_ms(void* start, void* end, float* ms) {
   return SS_OK;
 }
 
-extern "C" int ss_render_fwd(const ss_store* store, const ss_camera* cam, ss_view* v,
-                             cudaStream_t stream) {
-  if (!store || !cam || !v || v->n < 0) return set_error(SS_ERR_INVALID, "ss_render_fwd: bad args");
-  const int W = cam->width, H = cam->height;
-  if (W <= 0 || H <= 0) return set_error(SS_ERR_INVALID, "ss_render_fwd: bad camera");
+// Shared by the 3D (store + camera) and 2D (_kernels) entries: workspace
+// check, records (via `make_records`), depth order, offsets, K, binning,
+// tile order, raster forward.  pbox != nullptr selects the per-pixel bbox test.
+template <typename MakeRecords>
+static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
+                             MakeRecords make_records, cudaStream_t stream) {
+  if (W <= 0 || H <= 0) return set_error(SS_ERR_INVALID, "ss_render_fwd: bad image size");
   const int tiles_x = (W + kTile - 1) / kTile, tiles_y = (H + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
   const int n = v->n;
@@ -76,9 +78,7 @@ extern "C" int ss_render_fwd(const ss_store* store, const ss_camera* cam, ss_vie
     v->ws_needed = need_ws;
     return set_error(SS_ERR_WORKSPACE, "ss_render_fwd: workspace %zu < %zu", v->ws_bytes, need_ws);
   }
-  if ((rc = ss_project_fwd(store, v->rows, n, cam, v->rec_a, v->rec_b, v->rec_c, v->depth_key,
-                           v->bbox, v->n_tiles, v->geom, v->tile_mask, stream)))
-    return rc;
+  if ((rc = make_records())) return rc;
   // K = sum of the per-splat tile counts, read back early: the host waits on
   // it (to size the binning) while the GPU runs the depth sort and offsets.
   // It is parked in offsets[n], which ss_tile_offsets rewrites with K.
@@ -125,14 +125,53 @@ extern "C" int ss_render_fwd(const ss_store* store, const ss_camera* cam, ss_vie
       return rc;
     v->sorted_sel = sel;
     sv = sel ? v->vals_alt : v->vals;
-    if ((rc = ss_tile_ranges(sel ? v->keys_alt : v->keys, k_host, n_tiles, v->ranges, stream))) return rc;
+    if ((rc = ss_tile_ranges(sel ? v->keys_alt : v->keys, k_host, n_tiles, v->ranges, stream)))
+      return rc;
   }
   if ((rc = ss_tile_order(v->ranges, n_tiles, v->tile_order, v->ws, v->ws_bytes, stream))) return rc;
   record(v->events[0], stream);
-  rc = ss_raster_fwd(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,
-                     v->t_final, v->n_contrib, stream);
+  if (pbox)
+    rc = raster_fwd_bbox(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,
+                         v->t_final, v->n_contrib, pbox, stream);
+  else
+    rc = ss_raster_fwd(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,
+                       v->t_final, v->n_contrib, stream);
   record(v->events[1], stream);
   return rc;
+}
+
+extern "C" int ss_render_fwd(const ss_store* store, const ss_camera* cam, ss_view* v,
+                             cudaStream_t stream) {
+  if (!store || !cam || !v || v->n < 0) return set_error(SS_ERR_INVALID, "ss_render_fwd: bad args");
+  return render_fwd_common(cam->width, cam->height, v, nullptr, [&]() {
+    return ss_project_fwd(store, v->rows, v->n, cam, v->rec_a, v->rec_b, v->rec_c, v->depth_key,
+                          v->bbox, v->n_tiles, v->geom, v->tile_mask, stream);
+  }, stream);
+}
+
+extern "C" int ss_render2d_fwd(const ss_splats2d* sp, int32_t width, int32_t height, ss_view* v,
+                               cudaStream_t stream) {
+  if (!sp || !v || sp->n < 0) return set_error(SS_ERR_INVALID, "ss_render2d_fwd: bad args");
+  v->n = sp->n;
+  return render_fwd_common(width, height, v, v->bbox, [&]() {
+    return ss_records_2d(sp, width, height, v->rec_a, v->rec_b, v->rec_c, v->depth_key, v->bbox,
+                         v->n_tiles, v->geom, v->tile_mask, stream);
+  }, stream);
+}
+
+extern "C" int ss_render2d_bwd(const ss_splats2d* sp, int32_t width, int32_t height,
+                               const ss_view* v, const float* dimg, float* g2d, double* g_mean2d,
+                               double* g_inv2d, double* g_alpha, double* g_color,
+                               cudaStream_t stream) {
+  if (!sp || !v) return set_error(SS_ERR_INVALID, "ss_render2d_bwd: bad args");
+  if (v->n == 0 || v->n_pairs == 0) return SS_OK;
+  cudaMemsetAsync(g2d, 0, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
+  const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
+  int rc = raster_bwd_bbox(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, width, height,
+                           v->tile_order, dimg, v->t_final, v->n_contrib, g2d, v->bbox, stream);
+  if (rc) return rc;
+  return ss_basis_to_2d(g2d, sp, v->rec_b, v->depth_key, g_mean2d, g_inv2d, g_alpha, g_color,
+                        stream);
 }
 
 extern "C" int ss_render_bwd(const ss_store* store, const ss_camera* cam, const ss_view* v,

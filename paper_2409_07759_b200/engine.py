@@ -59,6 +59,16 @@ def _grow(t: torch.Tensor | None, shape, dtype, dev) -> torch.Tensor:
     return t
 
 
+class Splats2D:
+    """Device copies of _kernels' 2D splat arrays + the ss_splats2d struct."""
+
+    def __init__(self, mean2d, inv2d, alpha, color, bbox, rank):
+        self.t = [mean2d, inv2d, alpha, color, bbox, rank]  # keep alive
+        self.n = int(alpha.numel())
+        self.struct = L.SSSplats2D(L.ptr(mean2d), L.ptr(inv2d), L.ptr(alpha), L.ptr(color),
+                                   L.ptr(bbox), L.ptr(rank), self.n, 0)
+
+
 class ViewPipeline:
     """Reusable buffers + the call sequence for one view."""
 
@@ -105,12 +115,35 @@ class ViewPipeline:
         internal buffer)."""
         lib = L.lib()
         sp = L.stream_ptr(stream)
-        W, H = int(cam.width), int(cam.height)
+        self.cam_struct = L.camera_struct(cam)
+        self.store, self.store_struct, self.rows = store, store.struct(), rows
+
+        def call(v):
+            v.rows = L.ptr(rows)
+            v.n = n
+            return lib.ss_render_fwd(ctypes.byref(self.store_struct),
+                                     ctypes.byref(self.cam_struct), ctypes.byref(v), sp)
+
+        return self._run_forward(n, int(cam.width), int(cam.height), call)
+
+    def forward2d(self, splats: "Splats2D", width: int, height: int, stream=None):
+        """_kernels.blend_forward on device-resident 2D splats (ss_render2d_fwd)."""
+        lib = L.lib()
+        sp = L.stream_ptr(stream)
+        self.splats2d = splats
+
+        def call(v):
+            v.rows = None
+            v.n = splats.n
+            return lib.ss_render2d_fwd(ctypes.byref(splats.struct), int(width), int(height),
+                                       ctypes.byref(v), sp)
+
+        return self._run_forward(splats.n, int(width), int(height), call)
+
+    def _run_forward(self, n: int, W: int, H: int, call):
         tiles_x, tiles_y = (W + TILE - 1) // TILE, (H + TILE - 1) // TILE
         n_tiles = tiles_x * tiles_y
         self.n, self.width, self.height, self.n_tiles = n, W, H, n_tiles
-        self.cam_struct = L.camera_struct(cam)
-        self.store, self.store_struct, self.rows = store, store.struct(), rows
         nn = max(n, 1)
         b = {}
         for name, shape, dt in (("rec_a", (nn, 4), torch.float32), ("rec_b", (nn, 4), torch.float32),
@@ -131,8 +164,6 @@ class ViewPipeline:
             self._b["ws_bin"] = torch.empty(1 << 20, dtype=torch.uint8, device=self.dev)
         v = L.SSView()
         for _ in range(4):
-            v.rows = L.ptr(rows)
-            v.n = n
             for name in ("rec_a", "rec_b", "rec_c", "depth_key", "bbox", "n_tiles", "geom",
                          "tile_mask", "order", "offsets", "ranges", "tile_order", "img", "t_final",
                          "n_contrib"):
@@ -146,8 +177,7 @@ class ViewPipeline:
                 evs = self._new_events()
                 for i in range(4):
                     v.events[i] = evs[i]
-            rc = lib.ss_render_fwd(ctypes.byref(self.store_struct), ctypes.byref(self.cam_struct),
-                                   ctypes.byref(v), sp)
+            rc = call(v)
             if rc in (L.SS_ERR_CAPACITY, L.SS_ERR_WORKSPACE) and self.events is not None:
                 self.events["_pending"].pop()  # this attempt recorded nothing
             if rc == L.SS_ERR_CAPACITY:
@@ -169,6 +199,18 @@ class ViewPipeline:
         sk, sv = (("keys", "vals") if self.sel == 0 else ("keys_alt", "vals_alt"))
         self.sorted_keys, self.sorted_vals = self._b[sk], self._b[sv]
         return b["img"][: H * W * 3].view(H, W, 3)
+
+    def backward2d(self, dimg: torch.Tensor, g_mean2d, g_inv2d, g_alpha, g_color, stream=None):
+        """_kernels.blend_backward for the view forward2d left: adds into the
+        fp64 device gradient arrays (ss_render2d_bwd)."""
+        if self.n == 0 or self.n_pairs == 0:
+            return
+        g2d = self._buf("g2d", (self.n, L.SS_G2D_ROW), torch.float32)
+        sp = self.splats2d
+        L.check(L.lib().ss_render2d_bwd(ctypes.byref(sp.struct), self.width, self.height,
+                                        ctypes.byref(self.view), L.ptr(dimg), L.ptr(g2d),
+                                        L.ptr(g_mean2d), L.ptr(g_inv2d), L.ptr(g_alpha),
+                                        L.ptr(g_color), L.stream_ptr(stream)), "render2d_bwd")
 
     def _new_events(self):
         pending = self.events.setdefault("_pending", [])
