@@ -107,7 +107,8 @@ int ss_compact_active(const int32_t* row_start, const int32_t* row_expire, int64
  * rec_b = (k inv2, log2 alpha, r, g), rec_c = b (float32, rounded once from fp64;
  * k = -log2(e)/2 so alpha exp(-m/2) = 2^(k m + log2 alpha));
  * depth_key = fp64 z bits (UINT64_MAX when culled); bbox = (x0,x1,y0,y1)
- * pixels, half open; geom = (u, v, inv0, inv1, inv2, 1/inv0, 1/inv2, 0) fp32
+ * pixels, half open; geom = (u, v, inv0, inv1, det, sy, ymax, 1/inv0) fp32 (the
+ * row-interval tile test's constants, ss_common.cuh make_geom)
  * (n x 8); n_tiles = 16x16 tiles of the bbox that the maha <= 64 ellipse
  * reaches (exact ellipse-vs-tile test; 0 when culled); tile_mask = kept bits
  * of the first 64 bbox tiles (row-major). */

@@ -629,39 +629,50 @@ CULL_MARGIN = np.float32(64.0625)
 _F = np.float32
 
 
-def tile_min_maha(i0, i1, i2, u, v, X0, X1, Y0, Y1):
-    """Minimum over the continuous rectangle [X0, X1] x [Y0, Y1] (pixel-centre
-    coordinates) of m = i0 dx^2 + 2 i1 dx dy + i2 dy^2, dx = x - u, dy = y - v.
-    float32 restatement of ss_common.cuh tile_keeps (same rounded operation
-    sequence, numpy float32 = IEEE single without FMA).  A tile whose minimum
-    exceeds CULL_MARGIN holds no pixel the reference's loop would blend
+def tile_geom(i0, i1, i2):
+    """Per-splat constants of the row-interval tile test, fp64 then rounded
+    once to float32 (ss_common.cuh make_geom): det = i0 i2 - i1^2,
+    sy = i1 sqrt(M / (i2 det)) (dy of the ellipse's rightmost point is -sy),
+    ymax = sqrt(M i0 / det) (its vertical half extent), M = CULL_MARGIN."""
+    i0, i1, i2 = (np.asarray(a, dtype=np.float64) for a in (i0, i1, i2))
+    m = float(CULL_MARGIN)
+    det = i0 * i2 - i1 * i1
+    sy = i1 * np.sqrt(m / (i2 * det))
+    ymax = np.sqrt((m * i0) / det)
+    f0 = i0.astype(_F)
+    return f0, i1.astype(_F), det.astype(_F), sy.astype(_F), ymax.astype(_F), _F(1) / f0
+
+
+def tile_row_span(i0, i1, det, sy, ymax, r0, v, Y0, Y1):
+    """x-interval [L, R] (relative to the splat centre) where the ellipse
+    m <= CULL_MARGIN meets the pixel-centre rows [Y0, Y1], and whether it
+    meets them at all.  float32 restatement of ss_common.cuh row_span (same
+    rounded operation sequence; numpy float32 = IEEE single without FMA).
+    Tiles outside the interval hold no pixel the reference's loop blends
     (maha > 64 skip, _kernels.py:39-41)."""
-    i0, i1, i2, u, v = (np.asarray(a, dtype=np.float64).astype(_F) for a in (i0, i1, i2, u, v))
-    r0 = _F(1) / i0
-    r2 = _F(1) / i2
-    ax, bx = np.asarray(X0).astype(_F) - u, np.asarray(X1).astype(_F) - u
-    ay, by = np.asarray(Y0).astype(_F) - v, np.asarray(Y1).astype(_F) - v
-    inside = (ax <= 0) & (bx >= 0) & (ay <= 0) & (by >= 0)
-
-    def q(dx, dy):
-        return ((i0 * dx) * dx + ((_F(2) * i1) * dx) * dy) + (i2 * dy) * dy
-
-    best = np.full(np.shape(u), np.inf, dtype=_F)
-    for ex in (ax, bx):          # vertical edges: dx fixed, minimise over dy
-        dy = np.clip(-(i1 * ex) * r2, ay, by)
-        best = np.minimum(best, q(ex, dy))
-    for ey in (ay, by):          # horizontal edges: dy fixed, minimise over dx
-        dx = np.clip(-(i1 * ey) * r0, ax, bx)
-        best = np.minimum(best, q(dx, ey))
-    return np.where(inside, _F(0), best)
+    v = np.asarray(v, dtype=np.float64).astype(_F)
+    lo = np.maximum(np.asarray(Y0).astype(_F) - v, -ymax)
+    hi = np.minimum(np.asarray(Y1).astype(_F) - v, ymax)
+    meets = lo <= hi
+    m0 = i0 * CULL_MARGIN
+    cR = np.minimum(np.maximum(-sy, lo), hi)
+    cL = np.minimum(np.maximum(sy, lo), hi)
+    sR = np.sqrt(np.maximum(m0 - (det * cR) * cR, _F(0)))
+    sL = np.sqrt(np.maximum(m0 - (det * cL) * cL, _F(0)))
+    R = ((-i1) * cR + sR) * r0
+    L = ((-i1) * cL - sL) * r0
+    return meets, L, R
 
 
 def tile_keep_mask(cache, owner, tx, ty, tile=TILE):
     x0, x1, y0, y1 = cache["bbox"]
     i0, i1, i2 = cache["inv2d"][owner].T
     u, v = cache["mean2d"][owner].T
-    X0 = np.maximum(tx * tile, x0[owner])
-    X1 = np.minimum(tx * tile + tile - 1, x1[owner] - 1)
+    f0, f1, det, sy, ymax, r0 = tile_geom(i0, i1, i2)
     Y0 = np.maximum(ty * tile, y0[owner])
     Y1 = np.minimum(ty * tile + tile - 1, y1[owner] - 1)
-    return tile_min_maha(i0, i1, i2, u, v, X0, X1, Y0, Y1) <= CULL_MARGIN
+    meets, L, R = tile_row_span(f0, f1, det, sy, ymax, r0, v, Y0, Y1)
+    uf = np.asarray(u, dtype=np.float64).astype(_F)
+    ax = np.maximum(tx * tile, x0[owner]).astype(_F) - uf
+    bx = np.minimum(tx * tile + tile - 1, x1[owner] - 1).astype(_F) - uf
+    return meets & (ax <= R) & (bx >= L)

@@ -118,28 +118,32 @@ __device__ __forceinline__ void write_record(int i, double ux, double uy, double
                                              float* __restrict__ geom,
                                              uint64_t* __restrict__ tile_mask) {
   bbox[i] = make_int4(x0, x1, y0, y1);
-  const float fi0 = __double2float_rn(i0), fi2 = __double2float_rn(i2);
-  float gl[kGeom] = {__double2float_rn(ux), __double2float_rn(uy), fi0,
-                     __double2float_rn(i1), fi2, __frcp_rn(fi0), __frcp_rn(fi2), 0.0f};
+  float gl[kGeom];
+  make_geom(ux, uy, i0, i1, i2, gl);
   float* gm = geom + (int64_t)i * kGeom;
 #pragma unroll
   for (int c = 0; c < kGeom; ++c) gm[c] = gl[c];
   int nt = 0;
   uint64_t mask = 0;
   if (x1 > x0 && y1 > y0) {
-    // tiles of the bbox that the maha <= 64 ellipse actually reaches; the
-    // first 64 (row-major in the bbox tile rectangle) are also recorded as a
-    // bit mask so the binning does not repeat the test
+    // tiles of the bbox that the maha <= 64 ellipse actually reaches (one
+    // x-interval per tile row); the first 64 (row-major in the bbox tile
+    // rectangle) are also recorded as a bit mask for the binning
     const int4 bb = make_int4(x0, x1, y0, y1);
     const int tx0 = x0 / kTile, tx1 = (x1 - 1) / kTile + 1;
     const int ty0 = y0 / kTile, ty1 = (y1 - 1) / kTile + 1;
-    int j = 0;
-    for (int ty = ty0; ty < ty1; ++ty)
-      for (int tx = tx0; tx < tx1; ++tx, ++j) {
-        const bool keep = tile_keeps(gl, tx, ty, bb);
-        nt += keep;
-        if (keep && j < 64) mask |= 1ull << j;
+    const int w = tx1 - tx0;
+    for (int ty = ty0; ty < ty1; ++ty) {
+      float L, R;
+      if (!row_span(gl, ty, bb, L, R)) continue;
+      const int j0 = (ty - ty0) * w - tx0;
+      for (int tx = tx0; tx < tx1; ++tx) {
+        if (!col_meets(gl, tx, bb, L, R)) continue;
+        ++nt;
+        const int j = j0 + tx;
+        if (j < 64) mask |= 1ull << j;
       }
+    }
   }
   tile_mask[i] = mask;
   n_tiles[i] = nt;

@@ -83,42 +83,73 @@ __device__ __forceinline__ void quat_to_rot(const double q[4], double r[3][3]) {
   r[2][2] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(y, y))));
 }
 
-// Exact ellipse-vs-tile test (a-4 refinement): minimum over the continuous
-// rectangle [X0, X1] x [Y0, Y1] of pixel centres of m = i0 dx^2 + 2 i1 dx dy +
-// i2 dy^2.  fp32 with every operation explicitly rounded (no FMA
-// contraction), the same sequence as oracle/splat_oracle.py tile_min_maha in
-// numpy float32, so keep/drop decisions (and therefore tile keys) are
-// bit-identical to it.  The margin keeps tiles whose minimum is within
-// 2^-10 relative of 64 (those pixels blend nothing: maha > 64).
+// Exact ellipse-vs-tile test (a-4 refinement).  A tile row (pixel-centre
+// rows [Y0, Y1], clipped to the bbox) meets the ellipse m <= M (m = i0 dx^2
+// + 2 i1 dx dy + i2 dy^2, M = kCullMargin) in an x-interval [L, R]: the right
+// end is max over the row of (-i1 dy + sqrt(i0 M - det dy^2)) / i0, reached at
+// dy = -sy clamped into the row (sy = i1 sqrt(M / (i2 det)), the ellipse's
+// rightmost point), the left end symmetric at +sy; rows beyond |dy| <= ymax =
+// sqrt(M i0 / det) miss it.  A tile is kept iff its pixel-centre columns
+// [X0, X1] meet [L, R].  Per-splat constants come from fp64 (rounded once);
+// the row/tile arithmetic is fp32 with every operation explicitly rounded (no
+// FMA contraction), the sequence of oracle/splat_oracle.py tile_row_span in
+// numpy float32, so keep / drop decisions (and tile keys) are bit-identical
+// to it.  M = 64.0625 keeps a 1e-3 relative margin over the maha <= 64 cut
+// (pixels beyond it blend nothing), far above the fp32 rounding.
 constexpr float kCullMargin = 64.0625f;
-constexpr int kGeom = 8;  // floats per splat: u, v, i0, i1, i2, 1/i0, 1/i2, pad
+constexpr double kCullMarginD = 64.0625;
+constexpr int kGeom = 8;  // floats per splat: u, v, i0, i1, det, sy, ymax, 1/i0
 
 __device__ __forceinline__ float fmr(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float far_(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ float fsr(float a, float b) { return __fsub_rn(a, b); }
 
-__device__ __forceinline__ float quad_form(float i0, float i1, float i2, float dx, float dy) {
-  return far_(far_(fmr(fmr(i0, dx), dx), fmr(fmr(fmr(2.0f, i1), dx), dy)), fmr(fmr(i2, dy), dy));
-}
-
 __device__ __forceinline__ float clampf(float x, float lo, float hi) {
   return fminf(fmaxf(x, lo), hi);
 }
 
-// geom = (u, v, i0, i1, i2, 1/i0, 1/i2) fp32; bb = pixel bbox (x0, x1, y0, y1)
-__device__ __forceinline__ bool tile_keeps(const float* geom, int tx, int ty, int4 bb) {
-  const float u = geom[0], v = geom[1], i0 = geom[2], i1 = geom[3], i2 = geom[4];
-  const float r0 = geom[5], r2 = geom[6];
-  const float ax = fsr((float)max(tx * SS_TILE, bb.x), u);
-  const float bx = fsr((float)min(tx * SS_TILE + SS_TILE - 1, bb.y - 1), u);
-  const float ay = fsr((float)max(ty * SS_TILE, bb.z), v);
-  const float by = fsr((float)min(ty * SS_TILE + SS_TILE - 1, bb.w - 1), v);
-  if (ax <= 0.0f && bx >= 0.0f && ay <= 0.0f && by >= 0.0f) return true;
-  float best = quad_form(i0, i1, i2, ax, clampf(fmr(-fmr(i1, ax), r2), ay, by));
-  best = fminf(best, quad_form(i0, i1, i2, bx, clampf(fmr(-fmr(i1, bx), r2), ay, by)));
-  best = fminf(best, quad_form(i0, i1, i2, clampf(fmr(-fmr(i1, ay), r0), ax, bx), ay));
-  best = fminf(best, quad_form(i0, i1, i2, clampf(fmr(-fmr(i1, by), r0), ax, bx), by));
-  return best <= kCullMargin;
+// geom of a splat from its fp64 centre and conic
+__device__ __forceinline__ void make_geom(double ux, double uy, double i0, double i1, double i2,
+                                          float* g) {
+  const double det = __dsub_rn(__dmul_rn(i0, i2), __dmul_rn(i1, i1));
+  const double sy = __dmul_rn(i1, __dsqrt_rn(__ddiv_rn(kCullMarginD, __dmul_rn(i2, det))));
+  const double ymax = __dsqrt_rn(__ddiv_rn(__dmul_rn(kCullMarginD, i0), det));
+  const float fi0 = __double2float_rn(i0);
+  g[0] = __double2float_rn(ux);
+  g[1] = __double2float_rn(uy);
+  g[2] = fi0;
+  g[3] = __double2float_rn(i1);
+  g[4] = __double2float_rn(det);
+  g[5] = __double2float_rn(sy);
+  g[6] = __double2float_rn(ymax);
+  g[7] = __frcp_rn(fi0);
+}
+
+// x-interval [L, R] (relative to u) of the ellipse within tile row ty;
+// false when the row misses the ellipse.  bb = pixel bbox (x0, x1, y0, y1).
+__device__ __forceinline__ bool row_span(const float* g, int ty, int4 bb, float& L, float& R) {
+  const float v = g[1], i0 = g[2], i1 = g[3], det = g[4], sy = g[5], ymax = g[6], r0 = g[7];
+  const float lo = fmaxf(fsr((float)max(ty * SS_TILE, bb.z), v), -ymax);
+  const float hi = fminf(fsr((float)min(ty * SS_TILE + SS_TILE - 1, bb.w - 1), v), ymax);
+  if (lo > hi) return false;
+  const float m0 = fmr(i0, kCullMargin);
+  const float cR = clampf(-sy, lo, hi), cL = clampf(sy, lo, hi);
+  const float sR = __fsqrt_rn(fmaxf(fsr(m0, fmr(fmr(det, cR), cR)), 0.0f));
+  const float sL = __fsqrt_rn(fmaxf(fsr(m0, fmr(fmr(det, cL), cL)), 0.0f));
+  R = fmr(far_(fmr(-i1, cR), sR), r0);
+  L = fmr(fsr(fmr(-i1, cL), sL), r0);
+  return true;
+}
+
+__device__ __forceinline__ bool col_meets(const float* g, int tx, int4 bb, float L, float R) {
+  const float ax = fsr((float)max(tx * SS_TILE, bb.x), g[0]);
+  const float bx = fsr((float)min(tx * SS_TILE + SS_TILE - 1, bb.y - 1), g[0]);
+  return ax <= R && bx >= L;
+}
+
+__device__ __forceinline__ bool tile_keeps(const float* g, int tx, int ty, int4 bb) {
+  float L, R;
+  return row_span(g, ty, bb, L, R) && col_meets(g, tx, bb, L, R);
 }
 
 // Philox4x32-10 counter-based generator (Salmon et al., SC'11).
