@@ -44,27 +44,6 @@ __device__ __forceinline__ float gt_value(const uint8_t* gt_u8, const float* lut
   return gt_u8 ? lut[gt_u8[idx]] : gt_f32[idx];
 }
 
-// Loads the (42 x 42) halo region of channel ch of x and y (zero outside
-// the image) into padded (42 x kLP) tiles.
-__device__ __forceinline__ void load_region(const float* __restrict__ pred,
-                                            const uint8_t* __restrict__ gt_u8,
-                                            const float* s_lut, const float* __restrict__ gt_f32,
-                                            int W, int H, int x0, int y0, int ch, float* s_x,
-                                            float* s_y) {
-  for (int idx = threadIdx.x; idx < kLR * kLR; idx += blockDim.x) {
-    const int r = idx / kLR, q = idx % kLR;
-    const int gy = y0 - kHalo + r, gx = x0 - kHalo + q;
-    float xv = 0.f, yv = 0.f;
-    if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-      const int64_t e = ((int64_t)gy * W + gx) * 3 + ch;
-      xv = pred[e];
-      yv = gt_u8 ? s_lut[gt_u8[e]] : gt_f32[e];
-    }
-    s_x[r * kLP + q] = xv;
-    s_y[r * kLP + q] = yv;
-  }
-}
-
 struct LossArgs {
   const float* pred;
   const uint8_t* gt_u8;
@@ -75,118 +54,197 @@ struct LossArgs {
   double* partials;   // 2 per block
 };
 
-// Vertical blur of NQ quantities: out[q][r][c] = sum_t w_t src_q(r + t, c) for
-// r in [0, 32), c in [0, 42), from a (42 x kLP) source; quantities are
-// derived from the loaded sources by `load` (e.g. x, y, x*x, x*y, y*y).
-template <int NQ, typename Load>
-__device__ __forceinline__ void vblur(float (*out)[kLT][kLP], Load load) {
+constexpr int kWarpsL = kLossThreads / 32;
+
+// Separable 11-tap blur of one packed pair (A) and one scalar (B) quantity.
+// Vertical pass: task = (column c of the 42-wide region, 8 output rows);
+// out rows [r0, r0 + 8) from input rows [r0, r0 + 18).
+template <typename Load>
+__device__ __forceinline__ void vblur_pair(f2 (*outA)[kLP], float (*outB)[kLP], Load load) {
   for (int task = threadIdx.x; task < kLR * (kLT / kVR); task += kLossThreads) {
     const int c = task % kLR, r0 = (task / kLR) * kVR;
-    float acc[NQ][kVR];
+    f2 accA[kVR];
+    float accB[kVR];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q)
+    for (int i = 0; i < kVR; ++i) {
+      accA[i] = bc(0.f);
+      accB[i] = 0.f;
+    }
 #pragma unroll
-      for (int i = 0; i < kVR; ++i) acc[q][i] = 0.f;
-#pragma unroll
-    for (int s = 0; s < kVR + 10; ++s) {
-      float v[NQ];
-      load(r0 + s, c, v);
+    for (int sidx = 0; sidx < kVR + 10; ++sidx) {
+      f2 va;
+      float vb;
+      load(r0 + sidx, c, va, vb);
 #pragma unroll
       for (int i = 0; i < kVR; ++i) {
-        const int t = s - i;
+        const int t = sidx - i;
         if (t >= 0 && t <= 10) {
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) acc[q][i] = fmaf(win(t), v[q], acc[q][i]);
+          accA[i] = fma2(bc(win(t)), va, accA[i]);
+          accB[i] = fmaf(win(t), vb, accB[i]);
         }
       }
     }
 #pragma unroll
-    for (int q = 0; q < NQ; ++q)
-#pragma unroll
-      for (int i = 0; i < kVR; ++i) out[q][r0 + i][c] = acc[q][i];
+    for (int i = 0; i < kVR; ++i) {
+      outA[r0 + i][c] = accA[i];
+      outB[r0 + i][c] = accB[i];
+    }
   }
 }
 
-// Horizontal blur: res[q][i] = sum_t w_t v[q][r][c0 + i + t], i in [0, kHC)
-template <int NQ>
-__device__ __forceinline__ void hblur(const float (*v)[kLT][kLP], int r, int c0,
-                                      float res[NQ][kHC]) {
+// Horizontal pass: res[i] = sum_t w_t v[r][c0 + i + t], i in [0, kHC)
+__device__ __forceinline__ void hblur_pair(const f2 (*vA)[kLP], const float (*vB)[kLP], int r,
+                                           int c0, f2 resA[kHC], float resB[kHC]) {
 #pragma unroll
-  for (int q = 0; q < NQ; ++q)
+  for (int i = 0; i < kHC; ++i) {
+    resA[i] = bc(0.f);
+    resB[i] = 0.f;
+  }
 #pragma unroll
-    for (int i = 0; i < kHC; ++i) res[q][i] = 0.f;
+  for (int sidx = 0; sidx < kHC + 10; ++sidx) {
+    const f2 a = vA[r][c0 + sidx];
+    const float b = vB[r][c0 + sidx];
 #pragma unroll
-  for (int s = 0; s < kHC + 10; ++s) {
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const float x = v[q][r][c0 + s];
-#pragma unroll
-      for (int i = 0; i < kHC; ++i) {
-        const int t = s - i;
-        if (t >= 0 && t <= 10) res[q][i] = fmaf(win(t), x, res[q][i]);
+    for (int i = 0; i < kHC; ++i) {
+      const int t = sidx - i;
+      if (t >= 0 && t <= 10) {
+        resA[i] = fma2(bc(win(t)), a, resA[i]);
+        resB[i] = fmaf(win(t), b, resB[i]);
       }
     }
   }
 }
 
-// grid (tiles_x, tiles_y, 3): one CTA per 32x32 tile and channel
+// grid (tiles_x, tiles_y, 3): one CTA per 32x32 tile and channel.  The five
+// blurred moments run as two packed pairs, (x, y) and (xx, yy), plus xy.
 __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
-  __shared__ float s_x[kLR * kLP];
-  __shared__ float s_y[kLR * kLP];
-  __shared__ float s_v[5][kLT][kLP];
+  __shared__ f2 s_xy[kLR][kLP];        // (x, y) with the 5-px halo
+  __shared__ f2 s_v2[2][kLT][kLP];     // vertical pass: (mu_x, mu_y), (m_xx, m_yy)
+  __shared__ float s_v1[kLT][kLP];     // vertical pass: m_xy
   __shared__ float s_lut[256];
-  __shared__ double s_red[2][kLossThreads / 32];
+  __shared__ double s_red[2][kWarpsL];
   const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT, ch = blockIdx.z;
   const int W = a.width, H = a.height;
   const int64_t plane = (int64_t)W * H;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (a.gt_u8)
     for (int i = threadIdx.x; i < 256; i += kLossThreads) s_lut[i] = a.lut[i];
   __syncthreads();
-  load_region(a.pred, a.gt_u8, s_lut, a.gt_f32, W, H, x0, y0, ch, s_x, s_y);
+  // region rows by warp, columns by lane; every load of the thread is issued
+  // before the first use (one memory round trip instead of one per row)
+  constexpr int kRW = (kLR + kWarpsL - 1) / kWarpsL;  // rows per warp
+  float xv[kRW][2];
+  float yf[kRW][2];
+  int yb[kRW][2];
+#pragma unroll
+  for (int k = 0; k < kRW; ++k) {
+    const int r = warp + kWarpsL * k;
+    const int gy = y0 - kHalo + r;
+    const int64_t rowbase = ((int64_t)gy * W + (x0 - kHalo)) * 3 + ch;
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int q = lane + 32 * m;
+      const int gx = x0 - kHalo + q;
+      const bool in = r < kLR && q < kLR && gy >= 0 && gy < H && gx >= 0 && gx < W;
+      const int64_t e = rowbase + 3 * q;
+      xv[k][m] = in ? a.pred[e] : 0.f;
+      if (a.gt_u8) {
+        yb[k][m] = in ? (int)a.gt_u8[e] : -1;
+        yf[k][m] = 0.f;
+      } else {
+        yb[k][m] = 0;
+        yf[k][m] = in ? a.gt_f32[e] : 0.f;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kRW; ++k) {
+    const int r = warp + kWarpsL * k;
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int q = lane + 32 * m;
+      if (r < kLR && q < kLR) {
+        const float y = a.gt_u8 ? (yb[k][m] >= 0 ? s_lut[yb[k][m]] : 0.f) : yf[k][m];
+        s_xy[r][q] = pk2(xv[k][m], y);
+      }
+    }
+  }
   __syncthreads();
-  // vertical pass (axis 0, loss.py:31) of x, y, xx, xy, yy
-  vblur<5>(s_v, [&](int r, int c, float* v) {
-    const float xv = s_x[r * kLP + c], yv = s_y[r * kLP + c];
-    v[0] = xv;
-    v[1] = yv;
-    v[2] = xv * xv;
-    v[3] = xv * yv;
-    v[4] = yv * yv;
+  // vertical pass (axis 0, loss.py:31) of (x, y), (xx, yy), xy
+  f2 (*v2a)[kLP] = s_v2[0];
+  vblur_pair(v2a, s_v1, [&](int r, int c, f2& va, float& vb) {
+    const f2 p = s_xy[r][c];
+    va = p;
+    vb = lo2(p) * hi2(p);
   });
+  __syncthreads();
+  (void)v2a;
+  // (xx, yy) pair: a second vertical pass over the squares
+  for (int task = threadIdx.x; task < kLR * (kLT / kVR); task += kLossThreads) {
+    const int c = task % kLR, r0 = (task / kLR) * kVR;
+    f2 acc[kVR];
+#pragma unroll
+    for (int i = 0; i < kVR; ++i) acc[i] = bc(0.f);
+#pragma unroll
+    for (int sidx = 0; sidx < kVR + 10; ++sidx) {
+      const f2 p = s_xy[r0 + sidx][c];
+      const f2 sq = mul2(p, p);
+#pragma unroll
+      for (int i = 0; i < kVR; ++i) {
+        const int t = sidx - i;
+        if (t >= 0 && t <= 10) acc[i] = fma2(bc(win(t)), sq, acc[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kVR; ++i) s_v2[1][r0 + i][c] = acc[i];
+  }
   __syncthreads();
   // horizontal pass (axis 1, loss.py:32) + SSIM terms (loss.py:39-59)
   double l1 = 0.0, ss = 0.0;
   {
     const int r = threadIdx.x / (kLT / kHC), c0 = (threadIdx.x % (kLT / kHC)) * kHC;
-    float m[5][kHC];
-    hblur<5>(s_v, r, c0, m);
+    f2 mu[kHC], sq[kHC];
+    float mxy[kHC];
+    hblur_pair(s_v2[0], s_v1, r, c0, mu, mxy);
+#pragma unroll
+    for (int i = 0; i < kHC; ++i) sq[i] = bc(0.f);
+#pragma unroll
+    for (int sidx = 0; sidx < kHC + 10; ++sidx) {
+      const f2 v = s_v2[1][r][c0 + sidx];
+#pragma unroll
+      for (int i = 0; i < kHC; ++i) {
+        const int t = sidx - i;
+        if (t >= 0 && t <= 10) sq[i] = fma2(bc(win(t)), v, sq[i]);
+      }
+    }
     const int gy = y0 + r;
 #pragma unroll
     for (int i = 0; i < kHC; ++i) {
       const int gx = x0 + c0 + i;
       if (gy >= H || gx >= W) continue;
-      const float mu_x = m[0][i], mu_y = m[1][i], mxx = m[2][i], mxy = m[3][i], myy = m[4][i];
+      const float mu_x = lo2(mu[i]), mu_y = hi2(mu[i]), mxx = lo2(sq[i]), myy = hi2(sq[i]);
+      const float mxyv = mxy[i];
       const float C1 = 1e-4f, C2 = 9e-4f;
       const float sig_x = mxx - mu_x * mu_x;
       const float sig_y = myy - mu_y * mu_y;
-      const float sig_xy = mxy - mu_x * mu_y;
+      const float sig_xy = mxyv - mu_x * mu_y;
       const float a1 = 2.f * mu_x * mu_y + C1;
       const float a2 = 2.f * sig_xy + C2;
       const float b1 = mu_x * mu_x + mu_y * mu_y + C1;
       const float b2 = sig_x + sig_y + C2;
       const float inv_b2 = 1.f / b2;
       const float inv_den = inv_b2 / b1;  // 1 / (b1 b2)
-      const float s = (a1 * a2) * inv_den;
-      const float ds_dmu = (2.f * mu_y * (a2 - a1) - 2.f * mu_x * s * (b2 - b1)) * inv_den;
-      const float ds_dmxx = -s * inv_b2;
+      const float sv = (a1 * a2) * inv_den;
+      const float ds_dmu = (2.f * mu_y * (a2 - a1) - 2.f * mu_x * sv * (b2 - b1)) * inv_den;
+      const float ds_dmxx = -sv * inv_b2;
       const float ds_dmxy = 2.f * a1 * inv_den;
       const int64_t pix = (int64_t)gy * W + gx;
       a.maps[(0 * 3 + ch) * plane + pix] = ds_dmu;
       a.maps[(1 * 3 + ch) * plane + pix] = ds_dmxx;
       a.maps[(2 * 3 + ch) * plane + pix] = ds_dmxy;
-      ss += (double)s;
-      const int off = (r + kHalo) * kLP + (c0 + i + kHalo);
-      l1 += (double)fabsf(s_x[off] - s_y[off]);
+      ss += (double)sv;
+      const f2 p = s_xy[r + kHalo][c0 + i + kHalo];
+      l1 += (double)fabsf(lo2(p) - hi2(p));
     }
   }
   // block reduction of the two sums (fixed order -> deterministic)
@@ -195,14 +253,14 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
     l1 += __shfl_xor_sync(0xffffffffu, l1, o);
     ss += __shfl_xor_sync(0xffffffffu, ss, o);
   }
-  if ((threadIdx.x & 31) == 0) {
-    s_red[0][threadIdx.x >> 5] = l1;
-    s_red[1][threadIdx.x >> 5] = ss;
+  if (lane == 0) {
+    s_red[0][warp] = l1;
+    s_red[1][warp] = ss;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     double t0 = 0.0, t1 = 0.0;
-    for (int i = 0; i < kLossThreads / 32; ++i) {
+    for (int i = 0; i < kWarpsL; ++i) {
       t0 += s_red[0][i];
       t1 += s_red[1][i];
     }
@@ -212,10 +270,13 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
   }
 }
 
+// pass 2: blur of the partial maps as the pair (ds/dmu, ds/dmxx) + ds/dmxy
 __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, float w_ssim,
                                                                  float* __restrict__ dimg) {
-  __shared__ float s_m[3][kLR][kLP];
-  __shared__ float s_v[3][kLT][kLP];
+  __shared__ f2 s_m2[kLR][kLP];
+  __shared__ float s_m1[kLR][kLP];
+  __shared__ f2 s_v2[kLT][kLP];
+  __shared__ float s_v1[kLT][kLP];
   __shared__ float s_lut[256];
   if (a.gt_u8)
     for (int i = threadIdx.x; i < 256; i += kLossThreads) s_lut[i] = a.lut[i];
@@ -223,24 +284,49 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, floa
   const int W = a.width, H = a.height;
   const int64_t plane = (int64_t)W * H;
   const float inv_n = 1.0f / (float)((double)plane * 3.0);
-  for (int idx = threadIdx.x; idx < kLR * kLR; idx += kLossThreads) {
-    const int r = idx / kLR, q = idx % kLR;
-    const int gy = y0 - kHalo + r, gx = x0 - kHalo + q;
-    const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-    const int64_t pix = (int64_t)gy * W + gx;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* m0 = a.maps + (0 * 3 + ch) * plane;
+  const float* m1 = a.maps + (1 * 3 + ch) * plane;
+  const float* m2 = a.maps + (2 * 3 + ch) * plane;
+  constexpr int kRW = (kLR + kWarpsL - 1) / kWarpsL;  // rows per warp
+  float u[kRW][2][3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) s_m[k][r][q] = in ? a.maps[(k * 3 + ch) * plane + pix] : 0.f;
+  for (int k = 0; k < kRW; ++k) {
+    const int r = warp + kWarpsL * k;
+    const int gy = y0 - kHalo + r;
+    const int64_t rowbase = (int64_t)gy * W + (x0 - kHalo);
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int q = lane + 32 * m;
+      const int gx = x0 - kHalo + q;
+      const bool in = r < kLR && q < kLR && gy >= 0 && gy < H && gx >= 0 && gx < W;
+      u[k][m][0] = in ? m0[rowbase + q] : 0.f;
+      u[k][m][1] = in ? m1[rowbase + q] : 0.f;
+      u[k][m][2] = in ? m2[rowbase + q] : 0.f;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kRW; ++k) {
+    const int r = warp + kWarpsL * k;
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int q = lane + 32 * m;
+      if (r < kLR && q < kLR) {
+        s_m2[r][q] = pk2(u[k][m][0], u[k][m][1]);
+        s_m1[r][q] = u[k][m][2];
+      }
+    }
   }
   __syncthreads();
-  vblur<3>(s_v, [&](int r, int c, float* v) {
-    v[0] = s_m[0][r][c];
-    v[1] = s_m[1][r][c];
-    v[2] = s_m[2][r][c];
+  vblur_pair(s_v2, s_v1, [&](int r, int c, f2& va, float& vb) {
+    va = s_m2[r][c];
+    vb = s_m1[r][c];
   });
   __syncthreads();
   const int r = threadIdx.x / (kLT / kHC), c0 = (threadIdx.x % (kLT / kHC)) * kHC;
-  float bl[3][kHC];
-  hblur<3>(s_v, r, c0, bl);
+  f2 bl2[kHC];
+  float bl1[kHC];
+  hblur_pair(s_v2, s_v1, r, c0, bl2, bl1);
   const int gy = y0 + r;
 #pragma unroll
   for (int i = 0; i < kHC; ++i) {
@@ -249,7 +335,7 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, floa
     const int64_t e = ((int64_t)gy * W + gx) * 3 + ch;
     const float x = a.pred[e];
     const float y = gt_value(a.gt_u8, s_lut, a.gt_f32, e);
-    const float grad = (bl[0][i] + 2.f * x * bl[1][i] + y * bl[2][i]) * inv_n;
+    const float grad = (lo2(bl2[i]) + 2.f * x * hi2(bl2[i]) + y * bl1[i]) * inv_n;
     const float d = x - y;
     const float sgn = (d > 0.f) ? 1.f : ((d < 0.f) ? -1.f : 0.f);
     dimg[e] = (1.f - w_ssim) * sgn * inv_n - w_ssim * grad;

@@ -152,6 +152,60 @@ __device__ __forceinline__ bool tile_keeps(const float* g, int tx, int ty, int4 
   return row_span(g, ty, bb, L, R) && col_meets(g, tx, bb, L, R);
 }
 
+// Packed fp32 pairs (Blackwell FFMA2 / FMUL2 / FADD2, PTX *.f32x2): two fp32
+// values share one 64-bit register pair and one instruction issue (raster:
+// a lane's pixels 2p / 2p + 1; SSIM: two blurred quantities).  A scalar
+// operand broadcast with bc() folds into the instruction.
+typedef unsigned long long f2;
+
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo2(f2 r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  (void)b;
+  return a;
+}
+__device__ __forceinline__ float hi2(f2 r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  (void)a;
+  return b;
+}
+__device__ __forceinline__ f2 bc(float s) { return pk2(s, s); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// in-place accumulator forms (the result stays in the accumulator's registers)
+__device__ __forceinline__ void fma2_acc(f2& c, f2 a, f2 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void sub2_acc(f2& c, f2 a) {
+  asm("sub.rn.f32x2 %0, %0, %1;" : "+l"(c) : "l"(a));
+}
+__device__ __forceinline__ void mul2_acc(f2& c, f2 a) {
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(c) : "l"(a));
+}
 // Philox4x32-10 counter-based generator (Salmon et al., SC'11).
 struct Philox4 {
   uint32_t v[4];
