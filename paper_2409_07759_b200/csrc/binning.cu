@@ -20,15 +20,30 @@ __global__ void iota_kernel(int32_t* v, int32_t n) {
   if (i < n) v[i] = i;
 }
 
+// 24-bit prefix of a depth key (3 radix passes): the high word of a positive
+// fp64 z is (exponent << 20 | top mantissa bits); z >= 0.01 > 2^-7 puts the
+// exponent at >= 1016, so (high - 1016 << 20) >> 1 covers z < 2^14 in 24
+// bits, monotone.  Larger z clamp to the top value and culled keys
+// (UINT64_MAX) get 0xFFFFFF: equal prefixes are re-sorted on the full keys.
+constexpr uint32_t kCulled24 = 0xFFFFFFu;
+
+__device__ __forceinline__ uint32_t depth_prefix24(uint64_t k) {
+  if (k == ~0ull) return kCulled24;
+  const uint32_t hi = (uint32_t)(k >> 32), base = 1016u << 20;
+  if (hi < base) return 0u;
+  const uint32_t d = (hi - base) >> 1;
+  return d < kCulled24 - 1 ? d : kCulled24 - 1;
+}
+
 __global__ void high_keys_kernel(const uint64_t* __restrict__ key64, int32_t n,
                                  uint32_t* __restrict__ hi, int32_t* __restrict__ vals) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  hi[i] = (uint32_t)(key64[i] >> 32);
+  hi[i] = depth_prefix24(key64[i]);
   vals[i] = i;
 }
 
-// After a stable sort on the high 32 bits, each run of equal high keys is
+// After a stable sort on the 24-bit prefixes, each run of equal prefixes is
 // re-sorted by (full 64-bit key, index).  Runs of <= 32 (the usual case: a
 // few splats per 2^-20 relative depth) take a per-thread insertion sort; longer
 // runs are queued for long_runs_kernel (one CTA per run, bitonic sort of
@@ -45,6 +60,7 @@ __global__ void fix_runs_kernel(const uint32_t* __restrict__ hi_sorted,
   const uint32_t h = hi_sorted[p];
   if (p > 0 && hi_sorted[p - 1] == h) return;          // not a run start
   if (p + 1 >= n || hi_sorted[p + 1] != h) return;      // singleton run
+  if (h == kCulled24) return;  // culled: equal full keys, already in index order
   int q = p + 1;
   while (q < n && hi_sorted[q] == h) ++q;
   if (q - p > kShortRun) {
@@ -549,7 +565,7 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
   if (n == 0) return SS_OK;
   if (ws_bytes < ss_binning_workspace_bytes(n, 1, 1))
     return set_error(SS_ERR_WORKSPACE, "ss_depth_order: workspace too small");
-  // stable radix sort of the high 32 key bits (4 passes instead of 8), then a
+  // stable radix sort of 24-bit key prefixes (3 passes instead of 8), then a
   // fix-up of equal-high-key runs on the exact 64-bit keys: the result is the
   // stable 64-bit order, i.e. np.lexsort((src, z)) (raster.py:153)
   char* w = (char*)ws;
@@ -566,7 +582,7 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
   cub::DoubleBuffer<uint32_t> dk(hi_a, hi_b);
   cub::DoubleBuffer<int32_t> dv(vals_in, order);
   size_t tmp_bytes = tb;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(w, tmp_bytes, dk, dv, n, 0, 32, stream);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(w, tmp_bytes, dk, dv, n, 0, 24, stream);
   if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_depth_order: %s", cudaGetErrorString(e));
   if (dv.Current() != order)
     cudaMemcpyAsync(order, dv.Current(), nn * 4, cudaMemcpyDeviceToDevice, stream);

@@ -221,7 +221,9 @@ __global__ void records2d_kernel(const double* __restrict__ mean2d, const double
   const int4 b = bbox_in[i];
   const int x0 = max(b.x, 0), x1 = min(b.y, width), y0 = max(b.z, 0), y1 = min(b.w, height);
   write_record(i, mean2d[2 * i], mean2d[2 * i + 1], inv2d[3 * i], inv2d[3 * i + 1], inv2d[3 * i + 2],
-               x0, max(x0, x1), y0, max(y0, y1), alpha[i], color + 3 * i, (uint64_t)rank[i], rec_a,
+               x0, max(x0, x1), y0, max(y0, y1), alpha[i], color + 3 * i,
+               // rank as a positive double key (same form as fp64 z bits)
+               (uint64_t)__double_as_longlong(1.0 + (double)rank[i] * 0x1p-22), rec_a,
                rec_b, rec_c, depth_key, bbox, n_tiles, geom, tile_mask);
 }
 
