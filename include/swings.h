@@ -350,6 +350,10 @@ int ss_event_elapsed_ms(void* start, void* end, float* ms);
  * dst[i] = (mean, quat, exp(log_scale), sigmoid(logit), color) of src[i]. */
 int ss_to_direct(const double* src, double* dst, int64_t n, ss_stream_t stream);
 
+/* Display frame: n float32 linear values -> uint8 sRGB with write_png's
+ * rounding (raster.py:411-425), evaluated in fp64. */
+int ss_to_srgb_u8(const float* img, int64_t n, uint8_t* out, ss_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

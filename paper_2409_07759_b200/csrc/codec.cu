@@ -196,3 +196,22 @@ extern "C" int ss_decode_records(const uint8_t* data, int64_t n, int32_t profile
   decode_kernel<<<grid_for(n, 128), 128, 0, stream>>>(data, n, profile, rows);
   return check_launch("ss_decode_records");
 }
+
+// Display conversion of a rendered frame: write_png's quantisation
+// (raster.py:411-425: clip, sRGB transfer, rint(255 v)) evaluated in fp64 per
+// channel value, float32 linear in, uint8 out.
+__global__ void srgb_u8_kernel(const float* __restrict__ img, int64_t n, uint8_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x = (double)img[i];
+  x = x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x);
+  const double y = x <= 0.0031308 ? 12.92 * x : 1.055 * pow(x, 1.0 / 2.4) - 0.055;
+  out[i] = (uint8_t)rint(y * 255.0);
+}
+
+extern "C" int ss_to_srgb_u8(const float* img, int64_t n, uint8_t* out, cudaStream_t stream) {
+  if (n < 0) return set_error(SS_ERR_INVALID, "ss_to_srgb_u8: n < 0");
+  if (n == 0) return SS_OK;
+  srgb_u8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(img, n, out);
+  return check_launch("ss_to_srgb_u8");
+}

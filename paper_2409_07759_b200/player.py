@@ -40,11 +40,24 @@ class UpdateEvent:
     payload: DecodedSlice
 
 
-@dataclass
 class _Slot:
-    arrays: GaussianArrays
-    valid: np.ndarray
-    lifespan: Lifespan
+    """One slot's splats.  Slots filled from wire bytes on the GPU keep only
+    the device rows; the host GaussianArrays (API compatibility:
+    active_arrays, uploads) are materialised on first access."""
+
+    def __init__(self, arrays: Optional[GaussianArrays], valid: np.ndarray, lifespan: Lifespan,
+                 make_arrays=None):
+        self._arrays = arrays
+        self._make = make_arrays
+        self.valid = valid
+        self.lifespan = lifespan
+
+    @property
+    def arrays(self) -> GaussianArrays:
+        if self._arrays is None:
+            self._arrays = self._make()
+            self._make = None
+        return self._arrays
 
 
 class _DeviceSlots:
@@ -81,7 +94,9 @@ class _DeviceSlots:
         from .engine import Store
 
         L = self.L
-        self.blk_map[: len(order)].copy_(self.torch.tensor(order, dtype=self.torch.int32))
+        # pinned staging: a pageable copy would block the host on the stream
+        order_h = self.torch.tensor(order, dtype=self.torch.int32).pin_memory()
+        self.blk_map[: len(order)].copy_(order_h, non_blocking=True)
         L.check(L.lib().ss_compact_active(L.ptr(self.start), L.ptr(self.expire), 0,
                                           self.swin * self.sl, L.ptr(self.blk_map), self.sl, frame,
                                           L.ptr(self.active_rows), L.ptr(self.counts),
@@ -167,19 +182,36 @@ class PlayerBuffer:
         lifespan = Lifespan(t, t, t + params.swin_size)
         slot = slice_slot(t, self.swin_size)
         dev = self.to_device()
-        host = GaussianArrays.from_rows(rows.cpu().numpy()) if header.kept_count else \
-            GaussianArrays.empty()
-        pad = params.slice_size - header.kept_count
+        kept = header.kept_count
+        pad = params.slice_size - kept
         valid = np.zeros(params.slice_size, dtype=bool)
-        valid[: header.kept_count] = True
-        if pad:
+        valid[:kept] = True
+
+        def host_arrays():
             from .codec import decode_records
 
-            host = GaussianArrays.concat([host, decode_records(
-                b"\x00" * (pad * profile.bytes_per_record), profile, pad)])
+            host = GaussianArrays.from_rows(rows.cpu().numpy()) if kept else GaussianArrays.empty()
+            if pad:
+                host = GaussianArrays.concat([host, decode_records(
+                    b"\x00" * (pad * profile.bytes_per_record), profile, pad)])
+            return host
+
         with self._lock:
-            self.slots[slot] = _Slot(host, valid, lifespan)
-            dev.set_slot(slot, rows, header.kept_count, lifespan)
+            self.slots[slot] = _Slot(None, valid, lifespan, host_arrays)
+            dev.set_slot(slot, rows, kept, lifespan)
+
+    def render_device_u8(self, camera: Camera, frame: Optional[int] = None, out=None):
+        """(H, W, 3) uint8 sRGB CUDA frame (write_png's quantisation) for display."""
+        import torch
+
+        from . import _lib as L
+
+        img = self.render_device(camera, frame)
+        if out is None:
+            out = torch.empty(img.shape, dtype=torch.uint8, device=img.device)
+        L.check(L.lib().ss_to_srgb_u8(L.ptr(img), img.numel(), L.ptr(out), L.stream_ptr()),
+                "to_srgb_u8")
+        return out
 
     def render_device(self, camera: Camera, frame: Optional[int] = None):
         """(H, W, 3) float32 CUDA image of `frame` (default: the buffer's frame)."""

@@ -112,3 +112,40 @@ def test_player_apply_bytes_decodes_on_gpu():
     assert np.array_equal(ia, ib)
     with pytest.raises(player.ProtocolError):
         a.apply(player.UpdateEvent(4, 0, gens[-1]))
+
+
+def test_player_u8_display_frame_and_lazy_host_slots():
+    """render_device_u8 == write_png's quantisation (raster.to_u8) of the same
+    frame; slots filled from wire bytes materialise their host arrays on
+    demand with the decoded rows."""
+    import paper_2409_07759_b200 as P
+    from paper_2409_07759_b200 import codec as C
+    from paper_2409_07759_b200 import player, raster
+    d, gens = _golden_generations(P)
+    frame = int(d["frame"])
+    swin = 3
+    prof = C.PROFILES[1]
+    params = P.StreamParams(swin_size=3, num_gs=90, fps=30.0, bytes_per_gaussian=30, total_frames=6)
+    cam = P.Camera(*[int(x) for x in d["cam_wh"]], *d["cam_f"], d["cam_R"], d["cam_T"])
+    b = player.PlayerBuffer(gens[:swin], swin)
+    applied = []
+    for g in gens[swin:]:
+        t = g.header.target_frame
+        if t > frame:
+            continue
+        kept = g.gaussians.take(np.nonzero(g.valid)[0])
+        blob = C.pack_slice(kept, g.lifespan, prof, swin)
+        b.apply_bytes(blob, prof, params)
+        applied.append((t % swin, blob))
+    img = b.render_device(cam, frame).double().cpu().numpy()
+    u8 = b.render_device_u8(cam, frame).cpu().numpy()
+    ref = raster.to_u8(img)
+    assert u8.dtype == np.uint8 and u8.shape == ref.shape
+    diff = np.abs(u8.astype(int) - ref.astype(int))
+    assert diff.max() <= 1 and (diff == 0).mean() >= 0.9999
+    for slot, blob in applied:
+        hdr = C.SliceHeader.from_bytes(blob)
+        host = b.slots[slot].arrays
+        ref_rows = C.decode_records(blob[C.HEADER_SIZE:C.HEADER_SIZE + hdr.kept_count * 30], prof,
+                                    hdr.kept_count)
+        assert np.array_equal(host.take(np.arange(hdr.kept_count)).rows(), ref_rows.rows())
