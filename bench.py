@@ -275,6 +275,30 @@ class LossReadback:
         self._read()
 
 
+def snapshot_state(state):
+    """What train_swin changes on the window being benchmarked: the device
+    store and Adam moments, per-generation step counters, the sampling RNG
+    and the global iteration (Philox counter).  Restoring it replays the
+    same views on the same model states."""
+    dev = state.device
+    return {"t": [t.clone() for t in (dev.opt, dev.m, dev.v)],
+            "gens": [(g.adam_t, g.windows_trained) for g in state.slices],
+            "rng": state.rng.bit_generator.state, "iteration": state.iteration}
+
+
+def restore_state(state, snap):
+    import torch
+
+    dev = state.device
+    for dst, src in zip((dev.opt, dev.m, dev.v), snap["t"]):
+        dst.copy_(src)
+    for g, (t, w) in zip(state.slices, snap["gens"]):
+        g.adam_t, g.windows_trained = t, w
+    state.rng.bit_generator.state = snap["rng"]
+    state.iteration = snap["iteration"]
+    torch.cuda.synchronize()
+
+
 def time_steps(state, ds, window, steps, dp, progress=None):
     import torch
 
@@ -736,12 +760,15 @@ def main():
         return
     # raster kernel times come from CUDA events recorded by the native driver
     # on the launch stream around every raster launch INSIDE the timed region
+    snap = snapshot_state(state)  # e2e and K_used replay the same trajectory
     state.device.pipe.enable_timing(True)
     with ClockSampler(local) as clocks:
         ms = time_steps(state, ds, window, args.steps, dp)
     kms = state.device.pipe.kernel_ms()
     state.device.pipe.enable_timing(False)
-    # K_used needs per-view host reads: measured over the next steps (untimed)
+    # K_used needs per-view host reads: measured over the first timed views
+    # replayed from the snapshot (untimed)
+    restore_state(state, snap)
     _, k_used, k_pairs, n_act = roofline_pass(state, ds, window, min(args.steps, 10))
     views_per_s = world * args.steps / (ms / 1e3)
     out = {
@@ -762,8 +789,10 @@ def main():
         feed = HostFeed(ds, window, c["views"])
         rb = LossReadback(state.device)
         train.train_swin(window[0], window[1], state, feed, iterations=2, progress=rb)
+        rb.flush()
         feed.h2d_bytes = 0
         rb.d2h_bytes = 0
+        restore_state(state, snap)  # the same views and model states as `value`
         ms_e2e = time_steps(state, feed, window, args.steps, dp, progress=rb)
         out["e2e"] = {"value": world * args.steps / (ms_e2e / 1e3), "unit": "views/s",
                       "h2d_bytes_per_step": feed.h2d_bytes // args.steps,
@@ -783,7 +812,8 @@ def main():
                        "kernel": "raster_fwd + raster_bwd", "peak_source": peak_kind,
                        "bytes_per_view": b_raster, "K_used": k_used, "K": k_pairs,
                        "timing": "kernel ms: CUDA events around each raster launch over the "
-                                 "timed steps; K_used: the 10 steps that follow",
+                                 "timed steps; K_used: the first 10 of those steps replayed "
+                                 "from a snapshot",
                        "active_splats": n_act, "pixels": P,
                        "ms_per_view": {"raster_fwd": kms.get("raster_fwd", 0) / nview,
                                        "raster_bwd": kms.get("raster_bwd", 0) / nview}}

@@ -19,6 +19,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--e2e", action="store_true",
+                    help="the bench's e2e arm: ground truth from pinned host memory + loss readback")
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -27,10 +29,16 @@ def main():
     from paper_2409_07759_b200 import train
 
     c, scene, ds, state, window = bench.build_workload(a.config, None, "gt")
-    train.train_swin(window[0], window[1], state, ds, iterations=5)
+    progress = None
+    if a.e2e:
+        ds = bench.HostFeed(ds, window, c["views"])
+        progress = bench.LossReadback(state.device)
+    train.train_swin(window[0], window[1], state, ds, iterations=5, progress=progress)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        train.train_swin(window[0], window[1], state, ds, iterations=a.steps)
+        train.train_swin(window[0], window[1], state, ds, iterations=a.steps, progress=progress)
+        if progress is not None:
+            progress.flush()
         torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     spans = sorted((e.time_range.start, e.time_range.end, e.name) for e in evs)
