@@ -68,6 +68,20 @@ def load_traffic(kernels):
         return None
 
 
+def load_issue(kernels):
+    """SM issue-slot utilisation (percent of active cycles) of the given
+    kernels from the same committed ncu capture: the bound that applies to the
+    rasterizer (it is instruction-issue bound, not HBM bound)."""
+    files = sorted((ROOT / "profiles").glob("r*_traffic.json"))
+    if not files:
+        return None
+    d = json.loads(files[-1].read_text())
+    try:
+        return {k: d[k]["issue_active_pct"] for k in kernels}
+    except KeyError:
+        return None
+
+
 def load_peaks():
     if PEAKS.exists():
         d = json.loads(PEAKS.read_text())
@@ -807,6 +821,9 @@ def main():
     out["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                        "frac": achieved / peak,
                        "traffic": load_traffic(["raster_fwd", "raster_bwd"]),
+                       "issue_active_pct": load_issue(["raster_fwd", "raster_bwd"]),
+                       "issue_note": "ncu smsp__issue_active (profiles/r*_traffic.json): the "
+                                     "raster kernels are issue-bound; HBM frac is low by design",
                        "traffic_source": "ncu --set full dram__bytes_read+write per launch "
                                          "(profiles/r*_traffic.json, config 3)",
                        "kernel": "raster_fwd + raster_bwd", "peak_source": peak_kind,
