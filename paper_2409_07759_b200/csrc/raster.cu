@@ -38,6 +38,9 @@
 namespace ss {
 
 constexpr int kWarps = 4;  // warps per CTA
+#ifndef SS_BWD_MINB
+#define SS_BWD_MINB 8
+#endif
 constexpr float kKappa = -0.72134752044448170368f;  // -log2(e) / 2
 constexpr float kInvKappa = -1.38629436111989061883f;  // 1 / kappa = -2 ln 2
 constexpr float kMahaKappa = kMahaMax * kKappa;       // 64 kappa
@@ -281,7 +284,7 @@ __device__ __forceinline__ int64_t emit_position(const DetArgs& d, int g, int tx
 }
 
 template <int STRIP, bool DET, bool BB = false>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
     raster_bwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
                       const float4* __restrict__ rec_a, const float4* __restrict__ rec_b,
                       const float* __restrict__ rec_c, int width, int height, int tiles_x,
