@@ -156,56 +156,23 @@ __device__ __forceinline__ bool tile_keeps(const float* g, int tx, int ty, int4 
 // values share one 64-bit register pair and one instruction issue (raster:
 // a lane's pixels 2p / 2p + 1; SSIM: two blurred quantities).  A scalar
 // operand broadcast with bc() folds into the instruction.
-typedef unsigned long long f2;
+typedef float2 f2;
 
-__device__ __forceinline__ f2 pk2(float lo, float hi) {
-  f2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ float lo2(f2 r) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-  (void)b;
-  return a;
-}
-__device__ __forceinline__ float hi2(f2 r) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-  (void)a;
-  return b;
-}
-__device__ __forceinline__ f2 bc(float s) { return pk2(s, s); }
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
-  f2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
-  f2 d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2 add2(f2 a, f2 b) {
-  f2 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
-  f2 d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-// in-place accumulator forms (the result stays in the accumulator's registers)
-__device__ __forceinline__ void fma2_acc(f2& c, f2 a, f2 b) {
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
-}
-__device__ __forceinline__ void sub2_acc(f2& c, f2 a) {
-  asm("sub.rn.f32x2 %0, %0, %1;" : "+l"(c) : "l"(a));
-}
-__device__ __forceinline__ void mul2_acc(f2& c, f2 a) {
-  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(c) : "l"(a));
-}
+// CUDA's sm_100 float2 intrinsics (FFMA2 / FMUL2 / FADD2); values stay in
+// ordinary register pairs, so the compiler allocates them in place.
+__device__ __forceinline__ f2 pk2(float lo, float hi) { return make_float2(lo, hi); }
+__device__ __forceinline__ float lo2(f2 r) { return r.x; }
+__device__ __forceinline__ float hi2(f2 r) { return r.y; }
+__device__ __forceinline__ f2 bc(float s) { return make_float2(s, s); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ f2 add2(f2 a, f2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+// in-place accumulator forms
+__device__ __forceinline__ void fma2_acc(f2& c, f2 a, f2 b) { c = __ffma2_rn(a, b, c); }
+__device__ __forceinline__ void sub2_acc(f2& c, f2 a) { c = sub2(c, a); }
+__device__ __forceinline__ void mul2_acc(f2& c, f2 a) { c = __fmul2_rn(c, a); }
+
 // Philox4x32-10 counter-based generator (Salmon et al., SC'11).
 struct Philox4 {
   uint32_t v[4];
