@@ -160,7 +160,6 @@ __global__ void __launch_bounds__(kWarps * 32)
     stage_load(st, lane, base + lane, rg.y, vals, rec_a, rec_b, rec_c);
     __syncwarp();
     const int cnt = min(32, rg.y - base);
-#pragma unroll 1
     for (int j = 0; j < cnt; ++j) {
       const float4 a = st.a[j];
       const float4 b = st.b[j];
