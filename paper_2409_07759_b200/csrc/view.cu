@@ -82,8 +82,16 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   // K = sum of the per-splat tile counts, read back early: the host waits on
   // it (to size the binning) while the GPU runs the depth sort and offsets.
   // It is parked in offsets[n], which ss_tile_offsets rewrites with K.
-  static int32_t* k_pinned = nullptr;
-  static cudaEvent_t k_event = nullptr;
+  // per host thread and device (views may render from several threads, e.g.
+  // a trainer and a player; an event belongs to the device it was made on)
+  constexpr int kMaxDev = 64;
+  thread_local int32_t* k_pinned_tab[kMaxDev] = {};
+  thread_local cudaEvent_t k_event_tab[kMaxDev] = {};
+  int devid = 0;
+  if (cudaGetDevice(&devid) != cudaSuccess || devid < 0 || devid >= kMaxDev)
+    return check_launch("ss_render_fwd: device");
+  int32_t*& k_pinned = k_pinned_tab[devid];
+  cudaEvent_t& k_event = k_event_tab[devid];
   if (!k_pinned) {
     if (cudaMallocHost(&k_pinned, sizeof(int32_t)) != cudaSuccess ||
         cudaEventCreateWithFlags(&k_event, cudaEventDisableTiming) != cudaSuccess)
