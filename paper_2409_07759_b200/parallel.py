@@ -27,6 +27,10 @@ class DataParallel:
     def allreduce_grads(self, grads) -> None:
         if self.world_size == 1:
             return
+        if self.average and self.dist.get_backend(self.group) == "nccl":
+            # NCCL averages in the collective (no separate scaling pass)
+            self.dist.all_reduce(grads, op=self.dist.ReduceOp.AVG, group=self.group)
+            return
         self.dist.all_reduce(grads, op=self.dist.ReduceOp.SUM, group=self.group)
         if self.average:
             grads.mul_(1.0 / self.world_size)
