@@ -109,6 +109,7 @@ class DeviceModel:
         self.row_expire = torch.zeros(n_rows_all, dtype=torch.int32, device=dev)
         self.blk_map = torch.zeros(self.n_blocks, dtype=torch.int32, device=dev)
         self.active_rows = torch.empty(n_rows_all, dtype=torch.int32, device=dev)
+        self._active_cache = {}  # frame -> (rows, n, n_opt), valid while lifespans hold
         self.counts = torch.zeros(2, dtype=torch.int32, device=dev)
         lib = L.lib()
         self.ws_compact = torch.empty(int(lib.ss_compact_workspace_bytes(n_rows_all)),
@@ -133,6 +134,7 @@ class DeviceModel:
         self.dirty = True
 
     def sync_lifespans(self):
+        self._active_cache = {}
         sl, n_opt = self.sl, self.num_gs
         for i, gen in enumerate(self.state.slices):
             self.row_start[i * sl:(i + 1) * sl].fill_(gen.lifespan.start)
@@ -190,6 +192,11 @@ class DeviceModel:
         state, sl = self.state, self.sl
         if self.dirty:
             self.sync_lifespans()
+        hit = self._active_cache.get(frame)
+        if hit is not None:
+            # lifespans unchanged since this frame was compacted (the cache is
+            # dropped whenever they change): same rows, no kernel launches
+            return hit
         live = lambda ls: ls.start <= frame < ls.expire  # noqa: E731
         n_opt = sl * sum(live(g.lifespan) for g in state.slices)
         n_mat = sl * sum(live(m.lifespan) for m in state.matured)
@@ -199,7 +206,12 @@ class DeviceModel:
                                       L.ptr(self.active_rows), L.ptr(self.counts),
                                       L.ptr(self.ws_compact), self.ws_compact.numel(),
                                       L.stream_ptr()), "compact_active")
-        return self.active_rows, n_opt + n_mat, n_opt
+        n = n_opt + n_mat
+        rows = self.active_rows[: max(n, 1)].clone()
+        if len(self._active_cache) >= 64:
+            self._active_cache.pop(next(iter(self._active_cache)))
+        self._active_cache[frame] = (rows, n, n_opt)
+        return rows, n, n_opt
 
     # ------------------------------------------------------------------ step
     def train_step(self, draws, rank, dataset, it):
@@ -216,7 +228,7 @@ class DeviceModel:
 
         stepped = stepped_generations(state.slices, frames)
         self._gen_table(stepped)
-        _, n, n_opt_here = self.compact(frame)
+        rows, n, n_opt_here = self.compact(frame)
         self.grads.zero_()
         cam = dataset.cameras[view]
         # ground truth may still be in flight on a copy stream: only the loss
@@ -227,7 +239,7 @@ class DeviceModel:
         else:
             gt, gt_ready = dataset.device_frame(frame, view), None
         self.pipe.deterministic = state.deterministic
-        img = self.pipe.forward(self.store, self.active_rows, n, cam)
+        img = self.pipe.forward(self.store, rows, n, cam)
         if gt_ready is not None:
             torch.cuda.current_stream().wait_event(gt_ready)
         dimg, sums = self.lossbuf.run(img, cam.height, cam.width, gt_u8=gt, lut=self.lut,
