@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kWarps * 32)
         }
         any |= valid[2 * p] | valid[2 * p + 1];
       }
-      (void)any;
+      if (!__any_sync(0xffffffffu, any)) continue;
       // branch-free over the strip: invalid pixels get alpha' = 0, which
       // leaves C and T untouched
 #pragma unroll
