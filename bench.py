@@ -720,6 +720,7 @@ def main():
                     help="after warm-up run N steps between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off); prints no JSON")
     ap.add_argument("--strip", type=int, default=0, help="raster pixels per lane (2/4/8); 0 = library default")
+    ap.add_argument("--strip-fwd", type=int, default=0, help="forward strip only (overrides --strip)")
     ap.add_argument("--init", default="gt", choices=["gt", "random"],
                     help="model state: ground-truth splats (converged proxy) or init_state")
     args = ap.parse_args()
@@ -757,6 +758,11 @@ def main():
         from paper_2409_07759_b200 import _lib
 
         _lib.check(_lib.lib().ss_set_raster_strip(args.strip), "set_raster_strip")
+    if args.strip_fwd:
+        from paper_2409_07759_b200 import _lib
+
+        bwd = args.strip or 4
+        _lib.check(_lib.lib().ss_set_raster_strips(args.strip_fwd, bwd), "set_raster_strips")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     world = 1 if dp is None else dp.world_size

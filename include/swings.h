@@ -218,6 +218,9 @@ int ss_raster_bwd_deterministic(const int32_t* ranges, const int32_t* vals, cons
 /* Tuning knob: pixels per lane in the raster kernels (2, 4 or 8); a warp
  * covers 16 x (2 strip) pixels, i.e. 8 / strip warps per tile.  Default 4. */
 int ss_set_raster_strip(int32_t strip);
+/* The same knob set separately for the forward and the backward (the pixel
+ * state passes between them per pixel, independent of the mapping). */
+int ss_set_raster_strips(int32_t strip_fwd, int32_t strip_bwd);
 
 /* ---- a-6 blend backward: _kernels.py:56-130.  Accumulates into g2d
  * (n x 12 floats: the 9 basis sums t dx, t dy, t dx^2, t dx dy, t dy^2, t,

@@ -81,6 +81,7 @@ _SIGNATURES = {
     "ss_raster_fwd": ([P, P, P, P, P, I32, I32, P, P, P, P, P], c_int),
     "ss_raster_bwd": ([P, P, P, P, P, I32, I32, P, P, P, P, P, P], c_int),
     "ss_set_raster_strip": ([I32], c_int),
+    "ss_set_raster_strips": ([I32, I32], c_int),
     "ss_set_binning": ([I32], c_int),
     "ss_get_binning": ([], c_int),
     "ss_bin_tiles_workspace_bytes": ([I64, I32], c_size_t),

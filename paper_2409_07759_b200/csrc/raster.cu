@@ -471,7 +471,8 @@ __global__ void g2d_reduce_kernel(const float* __restrict__ partial,
   for (int c = 0; c < 9; ++c) dst[c] = acc[c];
 }
 
-static int g_strip = 4;
+static int g_strip = 4;       // backward strip
+static int g_strip_fwd = 4;   // forward strip
 
 }  // namespace ss
 
@@ -481,6 +482,16 @@ extern "C" int ss_set_raster_strip(int32_t strip) {
   if (strip != 2 && strip != 4 && strip != 8)
     return set_error(SS_ERR_INVALID, "ss_set_raster_strip: strip must be 2, 4 or 8");
   g_strip = strip;
+  g_strip_fwd = strip;
+  return SS_OK;
+}
+
+extern "C" int ss_set_raster_strips(int32_t strip_fwd, int32_t strip_bwd) {
+  const auto ok = [](int s) { return s == 2 || s == 4 || s == 8; };
+  if (!ok(strip_fwd) || !ok(strip_bwd))
+    return set_error(SS_ERR_INVALID, "ss_set_raster_strips: strips must be 2, 4 or 8");
+  g_strip_fwd = strip_fwd;
+  g_strip = strip_bwd;
   return SS_OK;
 }
 
@@ -491,14 +502,14 @@ extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const v
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_raster_fwd: bad size");
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
-  const int wpt = kTile / (2 * g_strip);
+  const int wpt = kTile / (2 * g_strip_fwd);
   const int blocks = (n_tiles * wpt + kWarps - 1) / kWarps;
 #define SS_FWD(S)                                                                             \
   raster_fwd_kernel<S><<<blocks, kWarps * 32, 0, stream>>>(                                   \
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
       height, tiles_x, n_tiles, tile_order, img, t_final, n_contrib)
-  if (g_strip == 8) SS_FWD(8);
-  else if (g_strip == 4) SS_FWD(4);
+  if (g_strip_fwd == 8) SS_FWD(8);
+  else if (g_strip_fwd == 4) SS_FWD(4);
   else SS_FWD(2);
 #undef SS_FWD
   return check_launch("ss_raster_fwd");
