@@ -47,7 +47,7 @@ __global__ void high_keys_kernel(const uint64_t* __restrict__ key64, int32_t n,
 // re-sorted by (full 64-bit key, index).  Runs of <= 32 (the usual case: a
 // few splats per 2^-20 relative depth) take a per-thread insertion sort; longer
 // runs are queued for long_runs_kernel (one CTA per run, bitonic sort of
-// (low 32 key bits, position in run) -- positions keep it stable).
+// (64-bit key, position in run) -- positions keep it stable).
 constexpr int kShortRun = 32;
 constexpr int kSmemRun = 8192;
 
@@ -82,16 +82,20 @@ __global__ void fix_runs_kernel(const uint32_t* __restrict__ hi_sorted,
   }
 }
 
-// Bitonic sort of n2 (power of two) 64-bit keys in `a` by one CTA.
-__device__ void cta_bitonic(uint64_t* a, int n2) {
+// Bitonic sort of n2 (power of two) (key, position) pairs by one CTA,
+// lexicographic: the full 64-bit depth key, then the position in the run
+// (runs come out of the stable prefix sort in index order, so position
+// order is index order).
+__device__ void cta_bitonic(ulonglong2* a, int n2) {
   for (int size = 2; size <= n2; size <<= 1)
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
         const int lo = 2 * i - (i & (stride - 1));
         const int hi = lo + stride;
         const bool asc = (lo & size) == 0;
-        const uint64_t x = a[lo], y = a[hi];
-        if ((x > y) == asc) {
+        const ulonglong2 x = a[lo], y = a[hi];
+        const bool gt = x.x > y.x || (x.x == y.x && x.y > y.y);
+        if (gt == asc) {
           a[lo] = y;
           a[hi] = x;
         }
@@ -104,21 +108,23 @@ __global__ void __launch_bounds__(1024) long_runs_kernel(const uint64_t* __restr
                                                          int32_t* __restrict__ order,
                                                          const int2* __restrict__ long_runs,
                                                          const int32_t* __restrict__ n_long,
-                                                         uint64_t* __restrict__ scratch,
+                                                         ulonglong2* __restrict__ scratch,
                                                          int32_t* __restrict__ tmp) {
-  extern __shared__ uint64_t s_keys[];
+  extern __shared__ ulonglong2 s_pairs[];
   for (int r = blockIdx.x; r < *n_long; r += gridDim.x) {
     const int2 run = long_runs[r];
     const int L = run.y - run.x;
     int n2 = 1;
     while (n2 < L) n2 <<= 1;
-    // long runs use a private slice of the scratch buffer at the run's offset
-    uint64_t* a = n2 <= kSmemRun ? s_keys : scratch + 2 * (int64_t)run.x;
+    // beyond shared memory: a private slice of the scratch buffer at the
+    // run's offset (n2 <= 2 L, so slices of disjoint runs do not overlap)
+    ulonglong2* a = n2 <= kSmemRun ? s_pairs : scratch + 2 * (int64_t)run.x;
     for (int i = threadIdx.x; i < n2; i += blockDim.x)
-      a[i] = i < L ? (((uint64_t)(uint32_t)key64[order[run.x + i]]) << 32) | (uint32_t)i : ~0ull;
+      a[i] = i < L ? make_ulonglong2(key64[order[run.x + i]], (unsigned long long)i)
+                   : make_ulonglong2(~0ull, ~0ull);
     __syncthreads();
     cta_bitonic(a, n2);
-    for (int i = threadIdx.x; i < L; i += blockDim.x) tmp[run.x + i] = order[run.x + (int)(a[i] & 0xffffffffu)];
+    for (int i = threadIdx.x; i < L; i += blockDim.x) tmp[run.x + i] = order[run.x + (int)a[i].y];
     __syncthreads();
     for (int i = threadIdx.x; i < L; i += blockDim.x) order[run.x + i] = tmp[run.x + i];
     __syncthreads();
@@ -554,7 +560,8 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 extern "C" size_t ss_binning_workspace_bytes(int32_t n, int64_t max_pairs, int32_t n_tiles) {
   (void)n_tiles;
   size_t nn = (size_t)(n > 0 ? n : 1);
-  // [cub temp | n+1 int32 | n u64 | n u64 | n int32 | 4n u64 (long-run bitonic scratch)]
+  // [cub temp | n+1 int32 | n u64 | n u64 | n int32 | 4n u64 (long-run bitonic scratch:
+  //  16-byte pairs, a run of L at offset 2 run.x pairs, next_pow2(L) <= 2 L)]
   return align256(cub_bytes(n, max_pairs)) + align256((nn + 1) * 4) + 2 * align256(nn * 8) +
          align256(nn * 4) + align256(4 * nn * 8) + 1024;
 }
@@ -597,12 +604,12 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(long_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemRun * 8);
+                         kSmemRun * 16);
     attr = true;
   }
-  long_runs_kernel<<<64, 1024, kSmemRun * 8, stream>>>(depth_key, order, long_runs, scratch32,
-                                                        (uint64_t*)((char*)vals_in + align256(nn * 4)),
-                                                        vals_in);
+  long_runs_kernel<<<64, 1024, kSmemRun * 16, stream>>>(
+      depth_key, order, long_runs, scratch32,
+      (ulonglong2*)((char*)vals_in + align256(nn * 4)), vals_in);
   return check_launch("ss_depth_order");
 }
 

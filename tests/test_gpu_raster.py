@@ -306,9 +306,11 @@ def test_deterministic_backward_bit_identical(ss):
 
 
 def test_depth_order_exact_on_adversarial_keys():
-    """ss_depth_order (32-bit high-key radix sort + run fix-up) equals the
+    """ss_depth_order (24-bit key-prefix radix sort + run fix-up) equals the
     stable 64-bit order, i.e. np.lexsort((index, z)) (raster.py:153): depths
-    sharing their high 32 bits, exact ties, culled keys, long runs."""
+    sharing their high 32 bits, exact ties, culled keys, long runs, runs whose
+    keys share the prefix but not the high word, and far depths that clamp to
+    one prefix."""
     import torch
     from paper_2409_07759_b200 import _lib as L
     rng = np.random.default_rng(0)
@@ -317,7 +319,12 @@ def test_depth_order_exact_on_adversarial_keys():
     z[:50_000] = 2.5 + rng.integers(0, 1000, 50_000) * 2.0 ** -44   # same high bits
     z[50_000:60_000] = 2.75                                          # exact ties
     z[60_000:61_000] = 2.75 + np.arange(1000)[::-1] * 2.0 ** -50     # long reversed run
+    z[61_000:63_000] = rng.uniform(2.0 ** 14, 2.0 ** 20, 2000)             # clamped prefix
     keys = z.view(np.uint64).copy()
+    # same 24-bit prefix, high words h and h + 1 (the prefix drops their last bit)
+    h = (np.array([2.9]).view(np.uint64)[0] >> np.uint64(32)) & ~np.uint64(1)
+    hi = h + rng.integers(0, 2, 3000).astype(np.uint64)
+    keys[63_000:66_000] = (hi << np.uint64(32)) | rng.integers(0, 2 ** 32, 3000).astype(np.uint64)
     keys[rng.choice(n, 5000, replace=False)] = np.uint64(0xFFFFFFFFFFFFFFFF)  # culled
     perm = rng.permutation(n)
     keys = keys[perm]
