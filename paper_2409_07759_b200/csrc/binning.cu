@@ -20,47 +20,91 @@ __global__ void iota_kernel(int32_t* v, int32_t n) {
   if (i < n) v[i] = i;
 }
 
-// 24-bit prefix of a depth key (3 radix passes): the high word of a positive
-// fp64 z is (exponent << 20 | top mantissa bits); z >= 0.01 > 2^-7 puts the
-// exponent at >= 1016, so (high - 1016 << 20) >> 1 covers z < 2^14 in 24
-// bits, monotone.  Larger z clamp to the top value and culled keys
-// (UINT64_MAX) get 0xFFFFFF: equal prefixes are re-sorted on the full keys.
-constexpr uint32_t kCulled24 = 0xFFFFFFu;
+// Depth order by buckets (no radix sort): the kept keys' range [kmin, kmax]
+// is cut into NB = 4 n buckets, b(k) = floor((k - kmin) / (kmax - kmin) *
+// (NB - 1)) in fp64 (monotone in k; a bucket holds ~0.25 keys on average);
+// culled keys (UINT64_MAX) go to bucket NB.  Keys are scattered to their
+// bucket's slots by atomics (order inside a bucket arbitrary), then every
+// bucket with more than one key is sorted on (64-bit key, index) -- the
+// result is np.lexsort((index, z)) (raster.py:153) on the kept prefix.
+constexpr int kBucketsPerKey = 4;
 
-__device__ __forceinline__ uint32_t depth_prefix24(uint64_t k) {
-  if (k == ~0ull) return kCulled24;
-  const uint32_t hi = (uint32_t)(k >> 32), base = 1016u << 20;
-  if (hi < base) return 0u;
-  const uint32_t d = (hi - base) >> 1;
-  return d < kCulled24 - 1 ? d : kCulled24 - 1;
+__device__ __forceinline__ uint32_t depth_bucket(uint64_t k, uint64_t kmin, uint64_t kmax,
+                                                 uint32_t nb) {
+  if (k == ~0ull) return nb;
+  const double span = (double)(kmax - kmin);
+  const double f = span > 0.0 ? (double)(k - kmin) / span : 0.0;
+  const uint32_t b = (uint32_t)(f * (double)(nb - 1));
+  return b < nb - 1 ? b : nb - 1;
 }
 
-__global__ void high_keys_kernel(const uint64_t* __restrict__ key64, int32_t n,
-                                 uint32_t* __restrict__ hi, int32_t* __restrict__ vals) {
+// zero the histogram and reduce the kept keys' range (range[0] = ~kmin,
+// range[1] = kmax, both max-reduced from 0)
+__global__ void depth_range_kernel(const uint64_t* __restrict__ key64, int32_t n,
+                                   unsigned long long* __restrict__ range,
+                                   int32_t* __restrict__ hist, int32_t nb_total) {
+  const int stride = gridDim.x * blockDim.x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = tid; i < nb_total; i += stride) hist[i] = 0;
+  unsigned long long inv_min = 0ull, mx = 0ull;
+  for (int i = tid; i < n; i += stride) {
+    const uint64_t k = key64[i];
+    if (k != ~0ull) {
+      inv_min = inv_min > ~k ? inv_min : ~k;
+      mx = mx > k ? mx : k;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, inv_min, o);
+    const unsigned long long b = __shfl_xor_sync(0xffffffffu, mx, o);
+    inv_min = inv_min > a ? inv_min : a;
+    mx = mx > b ? mx : b;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&range[0], inv_min);
+    atomicMax(&range[1], mx);
+  }
+}
+
+__global__ void depth_hist_kernel(const uint64_t* __restrict__ key64, int32_t n,
+                                  const unsigned long long* __restrict__ range, uint32_t nb,
+                                  int32_t* __restrict__ hist) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  hi[i] = depth_prefix24(key64[i]);
-  vals[i] = i;
+  atomicAdd(&hist[depth_bucket(key64[i], ~range[0], range[1], nb)], 1);
 }
 
-// After a stable sort on the 24-bit prefixes, each run of equal prefixes is
-// re-sorted by (full 64-bit key, index).  Runs of <= 32 (the usual case: a
+__global__ void depth_scatter_kernel(const uint64_t* __restrict__ key64, int32_t n,
+                                     const unsigned long long* __restrict__ range, uint32_t nb,
+                                     int32_t* __restrict__ cursor, int32_t* __restrict__ order,
+                                     uint32_t* __restrict__ bucket_of) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t b = depth_bucket(key64[i], ~range[0], range[1], nb);
+  const int32_t pos = atomicAdd(&cursor[b], 1);
+  order[pos] = i;
+  bucket_of[pos] = b;
+}
+
+// Each bucket (a run of equal bucket ids) is sorted by (full 64-bit key,
+// index).  Runs of <= 32 (the usual case: a
 // few splats per 2^-20 relative depth) take a per-thread insertion sort; longer
 // runs are queued for long_runs_kernel (one CTA per run, bitonic sort of
-// (64-bit key, position in run) -- positions keep it stable).
+// (64-bit key, index) pairs).
 constexpr int kShortRun = 32;
 constexpr int kSmemRun = 8192;
 
 __global__ void fix_runs_kernel(const uint32_t* __restrict__ hi_sorted,
                                 const uint64_t* __restrict__ key64, int32_t n,
                                 int32_t* __restrict__ order, int2* __restrict__ long_runs,
-                                int32_t* __restrict__ n_long) {
+                                int32_t* __restrict__ n_long, uint32_t culled) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const uint32_t h = hi_sorted[p];
   if (p > 0 && hi_sorted[p - 1] == h) return;          // not a run start
   if (p + 1 >= n || hi_sorted[p + 1] != h) return;      // singleton run
-  if (h == kCulled24) return;  // culled: equal full keys, already in index order
+  if (h == culled) return;  // culled splats: no place in the blend order
   int q = p + 1;
   while (q < n && hi_sorted[q] == h) ++q;
   if (q - p > kShortRun) {
@@ -82,10 +126,8 @@ __global__ void fix_runs_kernel(const uint32_t* __restrict__ hi_sorted,
   }
 }
 
-// Bitonic sort of n2 (power of two) (key, position) pairs by one CTA,
-// lexicographic: the full 64-bit depth key, then the position in the run
-// (runs come out of the stable prefix sort in index order, so position
-// order is index order).
+// Bitonic sort of n2 (power of two) (64-bit depth key, element index) pairs
+// by one CTA, lexicographic.
 __device__ void cta_bitonic(ulonglong2* a, int n2) {
   for (int size = 2; size <= n2; size <<= 1)
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -108,8 +150,7 @@ __global__ void __launch_bounds__(1024) long_runs_kernel(const uint64_t* __restr
                                                          int32_t* __restrict__ order,
                                                          const int2* __restrict__ long_runs,
                                                          const int32_t* __restrict__ n_long,
-                                                         ulonglong2* __restrict__ scratch,
-                                                         int32_t* __restrict__ tmp) {
+                                                         ulonglong2* __restrict__ scratch) {
   extern __shared__ ulonglong2 s_pairs[];
   for (int r = blockIdx.x; r < *n_long; r += gridDim.x) {
     const int2 run = long_runs[r];
@@ -119,14 +160,14 @@ __global__ void __launch_bounds__(1024) long_runs_kernel(const uint64_t* __restr
     // beyond shared memory: a private slice of the scratch buffer at the
     // run's offset (n2 <= 2 L, so slices of disjoint runs do not overlap)
     ulonglong2* a = n2 <= kSmemRun ? s_pairs : scratch + 2 * (int64_t)run.x;
-    for (int i = threadIdx.x; i < n2; i += blockDim.x)
-      a[i] = i < L ? make_ulonglong2(key64[order[run.x + i]], (unsigned long long)i)
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+      const int32_t v = i < L ? order[run.x + i] : 0;
+      a[i] = i < L ? make_ulonglong2(key64[v], (unsigned long long)v)
                    : make_ulonglong2(~0ull, ~0ull);
+    }
     __syncthreads();
     cta_bitonic(a, n2);
-    for (int i = threadIdx.x; i < L; i += blockDim.x) tmp[run.x + i] = order[run.x + (int)a[i].y];
-    __syncthreads();
-    for (int i = threadIdx.x; i < L; i += blockDim.x) order[run.x + i] = tmp[run.x + i];
+    for (int i = threadIdx.x; i < L; i += blockDim.x) order[run.x + i] = (int32_t)a[i].y;
     __syncthreads();
   }
 }
@@ -551,8 +592,12 @@ static size_t cub_bytes(int32_t n, int64_t max_pairs) {
   cub::DoubleBuffer<int32_t> pv(nullptr, nullptr);
   cub::DeviceRadixSort::SortPairs(nullptr, b, pk, pv, (int)(max_pairs > 0 ? max_pairs : 1), 0, 16);
   cub::DeviceScan::ExclusiveSum(nullptr, c, (int32_t*)nullptr, (int32_t*)nullptr, n + 1);
+  size_t d = 0;  // depth-order bucket scan (kBucketsPerKey n + 1 counts)
+  cub::DeviceScan::ExclusiveSum(nullptr, d, (int32_t*)nullptr, (int32_t*)nullptr,
+                                kBucketsPerKey * (n > 0 ? n : 1) + 1);
   size_t m = a > b ? a : b;
-  return m > c ? m : c;
+  m = m > c ? m : c;
+  return m > d ? m : d;
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -572,44 +617,43 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
   if (n == 0) return SS_OK;
   if (ws_bytes < ss_binning_workspace_bytes(n, 1, 1))
     return set_error(SS_ERR_WORKSPACE, "ss_depth_order: workspace too small");
-  // stable radix sort of 24-bit key prefixes (3 passes instead of 8), then a
-  // fix-up of equal-high-key runs on the exact 64-bit keys: the result is the
-  // stable 64-bit order, i.e. np.lexsort((src, z)) (raster.py:153)
+  // workspace regions (ss_binning_workspace_bytes): [cub | n+1 int32 | n u64 | n u64 | n int32 |
+  // 4n u64]; here: scratch32 = [n_long, pad, range (2 u64)], u64a = bucket ids (n u32) + long
+  // run list, the 4n u64 region = histogram / cursors (NB + 1 int32), later long-run scratch
   char* w = (char*)ws;
   const size_t nn = (size_t)n;
   const size_t tb = align256(cub_bytes(n, 1));
-  // workspace regions (see ss_binning_workspace_bytes): [cub | n+1 int32 | 2 x n u64 | n int32 | ...]
   int32_t* scratch32 = (int32_t*)(w + tb);
+  unsigned long long* range = (unsigned long long*)(scratch32 + 2);
   uint64_t* u64a = (uint64_t*)((char*)scratch32 + align256((nn + 1) * 4));
   uint64_t* u64b = (uint64_t*)((char*)u64a + align256(nn * 8));
   int32_t* vals_in = (int32_t*)((char*)u64b + align256(nn * 8));
-  uint32_t* hi_a = (uint32_t*)u64a;
-  uint32_t* hi_b = hi_a + nn;  // both high-key buffers fit in region u64a
-  high_keys_kernel<<<grid_for(n, 256), 256, 0, stream>>>(depth_key, n, hi_a, vals_in);
-  cub::DoubleBuffer<uint32_t> dk(hi_a, hi_b);
-  cub::DoubleBuffer<int32_t> dv(vals_in, order);
+  int32_t* big = (int32_t*)((char*)vals_in + align256(nn * 4));
+  uint32_t* bucket_of = (uint32_t*)u64a;
+  int2* long_runs = (int2*)((char*)u64a + align256(nn * 4));
+  const uint32_t nb = (uint32_t)(kBucketsPerKey * nn);
+  int32_t* hist = big;  // nb + 1 counts, scanned in place into the bucket cursors
+  cudaMemsetAsync(scratch32, 0, 2 * sizeof(int32_t) + 2 * sizeof(unsigned long long), stream);
+  depth_range_kernel<<<min(296, (n + 255) / 256), 256, 0, stream>>>(depth_key, n, range, hist,
+                                                                      (int32_t)nb + 1);
+  depth_hist_kernel<<<grid_for(n, 256), 256, 0, stream>>>(depth_key, n, range, nb, hist);
   size_t tmp_bytes = tb;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(w, tmp_bytes, dk, dv, n, 0, 24, stream);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(w, tmp_bytes, hist, hist, (int)nb + 1, stream);
   if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_depth_order: %s", cudaGetErrorString(e));
-  if (dv.Current() != order)
-    cudaMemcpyAsync(order, dv.Current(), nn * 4, cudaMemcpyDeviceToDevice, stream);
-  // long-run list in region u64b (int2 per potential run start), its count in scratch32[0]
-  int2* long_runs = (int2*)u64b;
-  cudaMemsetAsync(scratch32, 0, sizeof(int32_t), stream);
-  fix_runs_kernel<<<grid_for(n, 256), 256, 0, stream>>>(dk.Current(), depth_key, n, order,
-                                                         long_runs, scratch32);
-  // long runs: a run of length L >= 33 sorts in place via the vals_in region
-  // (tmp) and, beyond kSmemRun, the u64 region after it (scratch, 2x run.x
-  // offset keeps runs disjoint: next_pow2(L) <= 2 L)
+  depth_scatter_kernel<<<grid_for(n, 256), 256, 0, stream>>>(depth_key, n, range, nb, hist, order,
+                                                             bucket_of);
+  fix_runs_kernel<<<grid_for(n, 256), 256, 0, stream>>>(bucket_of, depth_key, n, order, long_runs,
+                                                         scratch32, nb);
+  // long runs: a run of length L >= 33 sorts in shared memory, or beyond
+  // kSmemRun in the 4n u64 region (a run of L at offset 2 run.x pairs)
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(long_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSmemRun * 16);
     attr = true;
   }
-  long_runs_kernel<<<64, 1024, kSmemRun * 16, stream>>>(
-      depth_key, order, long_runs, scratch32,
-      (ulonglong2*)((char*)vals_in + align256(nn * 4)), vals_in);
+  long_runs_kernel<<<64, 1024, kSmemRun * 16, stream>>>(depth_key, order, long_runs, scratch32,
+                                                         (ulonglong2*)big);
   return check_launch("ss_depth_order");
 }
 
