@@ -16,6 +16,8 @@
 namespace ss {
 
 __global__ void iota_kernel(int32_t* v, int32_t n) {
+  pdl_wait();
+  pdl_trigger();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = i;
 }
@@ -43,6 +45,8 @@ __device__ __forceinline__ uint32_t depth_bucket(uint64_t k, uint64_t kmin, uint
 __global__ void depth_range_kernel(const uint64_t* __restrict__ key64, int32_t n,
                                    unsigned long long* __restrict__ range,
                                    int32_t* __restrict__ hist, int32_t nb_total) {
+  pdl_wait();
+  pdl_trigger();
   const int stride = gridDim.x * blockDim.x;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   for (int i = tid; i < nb_total; i += stride) hist[i] = 0;
@@ -70,6 +74,8 @@ __global__ void depth_range_kernel(const uint64_t* __restrict__ key64, int32_t n
 __global__ void depth_hist_kernel(const uint64_t* __restrict__ key64, int32_t n,
                                   const unsigned long long* __restrict__ range, uint32_t nb,
                                   int32_t* __restrict__ hist) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   atomicAdd(&hist[depth_bucket(key64[i], ~range[0], range[1], nb)], 1);
@@ -79,6 +85,8 @@ __global__ void depth_scatter_kernel(const uint64_t* __restrict__ key64, int32_t
                                      const unsigned long long* __restrict__ range, uint32_t nb,
                                      int32_t* __restrict__ cursor, int32_t* __restrict__ order,
                                      uint32_t* __restrict__ bucket_of) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t b = depth_bucket(key64[i], ~range[0], range[1], nb);
@@ -99,6 +107,8 @@ __global__ void fix_runs_kernel(const uint32_t* __restrict__ hi_sorted,
                                 const uint64_t* __restrict__ key64, int32_t n,
                                 int32_t* __restrict__ order, int2* __restrict__ long_runs,
                                 int32_t* __restrict__ n_long, uint32_t culled) {
+  pdl_wait();
+  pdl_trigger();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const uint32_t h = hi_sorted[p];
@@ -151,6 +161,8 @@ __global__ void __launch_bounds__(1024) long_runs_kernel(const uint64_t* __restr
                                                          const int2* __restrict__ long_runs,
                                                          const int32_t* __restrict__ n_long,
                                                          ulonglong2* __restrict__ scratch) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ ulonglong2 s_pairs[];
   for (int r = blockIdx.x; r < *n_long; r += gridDim.x) {
     const int2 run = long_runs[r];
@@ -175,6 +187,8 @@ __global__ void __launch_bounds__(1024) long_runs_kernel(const uint64_t* __restr
 __global__ void gather_counts_kernel(const int32_t* __restrict__ order,
                                      const int32_t* __restrict__ n_tiles, int32_t n,
                                      int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) out[k] = n_tiles[order[k]];
   if (k == n) out[k] = 0;
@@ -189,6 +203,8 @@ __global__ void emit_pairs_kernel(const int32_t* __restrict__ order,
                                   const uint64_t* __restrict__ tile_mask, int32_t n,
                                   int32_t tiles_x, uint32_t* __restrict__ keys,
                                   int32_t* __restrict__ vals) {
+  pdl_wait();
+  pdl_trigger();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   int32_t off = offsets[k];
@@ -225,6 +241,8 @@ __global__ void emit_pairs_kernel(const int32_t* __restrict__ order,
 
 __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int64_t n_pairs,
                                    int2* __restrict__ ranges) {
+  pdl_wait();
+  pdl_trigger();
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
   const uint32_t t = keys[p];
@@ -234,6 +252,8 @@ __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int64_t n_
 
 __global__ void tile_len_kernel(const int2* __restrict__ ranges, int n_tiles,
                                 int32_t* __restrict__ len, int32_t* __restrict__ ids) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_tiles) return;
   const int2 r = ranges[t];
@@ -263,6 +283,8 @@ constexpr int kBinWarps = kBinThreads / 32;
 // splats is as short as one of far, small splats.
 __global__ void bin_bounds_kernel(const int32_t* __restrict__ offsets, int32_t n, int32_t n_chunks,
                                   int32_t* __restrict__ bounds) {
+  pdl_wait();
+  pdl_trigger();
   // warp per boundary, 32-ary search: first k with offsets[k] >= target
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (c > n_chunks) return;
@@ -323,6 +345,8 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
     const uint64_t* __restrict__ tile_mask, const int32_t* __restrict__ bounds, int32_t n_tiles,
     int32_t tiles_x, uint16_t* __restrict__ keys, int32_t* __restrict__ vals,
     int32_t* __restrict__ counts) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ int32_t s_hist[];
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_hist[t] = 0;
   __syncthreads();
@@ -434,6 +458,8 @@ __global__ void __launch_bounds__(kBinThreads) bin_col_scan_kernel(int32_t* __re
                                                                    int32_t n_chunks,
                                                                    int32_t n_tiles,
                                                                    int32_t* __restrict__ totals) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t s_part[kBinWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = blockIdx.x * 32 + lane;
@@ -471,6 +497,8 @@ __global__ void __launch_bounds__(1024) bin_tile_scan_kernel(const int32_t* __re
                                                              int32_t n_tiles,
                                                              int32_t* __restrict__ start,
                                                              int2* __restrict__ ranges) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t s_warp[32];
   extern __shared__ int32_t s_tot[];  // totals staged by coalesced loads
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_tot[t] = totals[t];
@@ -523,6 +551,8 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(
     const uint16_t* __restrict__ keys, const int32_t* __restrict__ vals, int32_t n_tiles,
     const int32_t* __restrict__ base, const int32_t* __restrict__ start,
     int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char s_dyn[];
   unsigned long long* s_wc = reinterpret_cast<unsigned long long*>(s_dyn);  // n_tiles
   int32_t* s_cur = reinterpret_cast<int32_t*>(s_wc + n_tiles);              // n_tiles
@@ -634,15 +664,15 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
   const uint32_t nb = (uint32_t)(kBucketsPerKey * nn);
   int32_t* hist = big;  // nb + 1 counts, scanned in place into the bucket cursors
   cudaMemsetAsync(scratch32, 0, 2 * sizeof(int32_t) + 2 * sizeof(unsigned long long), stream);
-  depth_range_kernel<<<min(296, (n + 255) / 256), 256, 0, stream>>>(depth_key, n, range, hist,
+  launch_k(depth_range_kernel, min(296, (n + 255) / 256), 256, 0, stream, depth_key, n, range, hist,
                                                                       (int32_t)nb + 1);
-  depth_hist_kernel<<<grid_for(n, 256), 256, 0, stream>>>(depth_key, n, range, nb, hist);
+  launch_k(depth_hist_kernel, grid_for(n, 256), 256, 0, stream, depth_key, n, range, nb, hist);
   size_t tmp_bytes = tb;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(w, tmp_bytes, hist, hist, (int)nb + 1, stream);
   if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_depth_order: %s", cudaGetErrorString(e));
-  depth_scatter_kernel<<<grid_for(n, 256), 256, 0, stream>>>(depth_key, n, range, nb, hist, order,
+  launch_k(depth_scatter_kernel, grid_for(n, 256), 256, 0, stream, depth_key, n, range, nb, hist, order,
                                                              bucket_of);
-  fix_runs_kernel<<<grid_for(n, 256), 256, 0, stream>>>(bucket_of, depth_key, n, order, long_runs,
+  launch_k(fix_runs_kernel, grid_for(n, 256), 256, 0, stream, bucket_of, depth_key, n, order, long_runs,
                                                          scratch32, nb);
   // long runs: a run of length L >= 33 sorts in shared memory, or beyond
   // kSmemRun in the 4n u64 region (a run of L at offset 2 run.x pairs)
@@ -652,7 +682,7 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
                          kSmemRun * 16);
     attr = true;
   }
-  long_runs_kernel<<<64, 1024, kSmemRun * 16, stream>>>(depth_key, order, long_runs, scratch32,
+  launch_k(long_runs_kernel, 64, 1024, kSmemRun * 16, stream, depth_key, order, long_runs, scratch32,
                                                          (ulonglong2*)big);
   return check_launch("ss_depth_order");
 }
@@ -665,7 +695,7 @@ extern "C" int ss_tile_offsets(const int32_t* order, const int32_t* n_tiles, int
   char* w = (char*)ws;
   size_t tb = align256(cub_bytes(n, 1));
   int32_t* cnt = (int32_t*)(w + tb);
-  gather_counts_kernel<<<grid_for(n + 1, 256), 256, 0, stream>>>(order, n_tiles, n, cnt);
+  launch_k(gather_counts_kernel, grid_for(n + 1, 256), 256, 0, stream, order, n_tiles, n, cnt);
   size_t tmp_bytes = tb;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(w, tmp_bytes, cnt, offsets, n + 1, stream);
   if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_tile_offsets: %s", cudaGetErrorString(e));
@@ -678,7 +708,7 @@ extern "C" int ss_emit_tile_pairs(const int32_t* order, const int32_t* offsets,
                                   uint32_t* keys, int32_t* vals, cudaStream_t stream) {
   if (n < 0 || tiles_x <= 0) return set_error(SS_ERR_INVALID, "ss_emit_tile_pairs: bad sizes");
   if (n == 0) return SS_OK;
-  emit_pairs_kernel<<<grid_for(n, 128), 128, 0, stream>>>(
+  launch_k(emit_pairs_kernel, grid_for(n, 128), 128, 0, stream, 
       order, offsets, (const int4*)bbox, geom, tile_mask, n, tiles_x, keys, vals);
   return check_launch("ss_emit_tile_pairs");
 }
@@ -754,13 +784,13 @@ extern "C" int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const 
                          (int)smem_scatter);
     attr_scatter = smem_scatter;
   }
-  bin_bounds_kernel<<<(32 * (C + 1) + 127) / 128, 128, 0, stream>>>(offsets, n, C, bounds);
-  bin_emit_kernel<<<C, kBinThreads, smem, stream>>>(order, offsets, (const int4*)bbox, geom,
+  launch_k(bin_bounds_kernel, (32 * (C + 1) + 127) / 128, 128, 0, stream, offsets, n, C, bounds);
+  launch_k(bin_emit_kernel, C, kBinThreads, smem, stream, order, offsets, (const int4*)bbox, geom,
                                                     tile_mask, bounds, n_tiles, tiles_x, keys,
                                                     vals, counts);
-  bin_col_scan_kernel<<<(n_tiles + 31) / 32, kBinThreads, 0, stream>>>(counts, C, n_tiles, totals);
-  bin_tile_scan_kernel<<<1, 1024, (size_t)n_tiles * 4, stream>>>(totals, n_tiles, start, (int2*)ranges);
-  bin_scatter_kernel<<<C, kBinThreads, smem_scatter, stream>>>(offsets, bounds, keys, vals,
+  launch_k(bin_col_scan_kernel, (n_tiles + 31) / 32, kBinThreads, 0, stream, counts, C, n_tiles, totals);
+  launch_k(bin_tile_scan_kernel, 1, 1024, (size_t)n_tiles * 4, stream, totals, n_tiles, start, (int2*)ranges);
+  launch_k(bin_scatter_kernel, C, kBinThreads, smem_scatter, stream, offsets, bounds, keys, vals,
                                                                n_tiles, counts, start, vals_out);
   return check_launch("ss_bin_tiles");
 }
@@ -791,7 +821,7 @@ extern "C" int ss_tile_ranges(const uint32_t* sorted_keys, int64_t n_pairs, int3
   if (n_pairs < 0 || n_tiles <= 0) return set_error(SS_ERR_INVALID, "ss_tile_ranges: bad sizes");
   cudaMemsetAsync(ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, stream);
   if (n_pairs > 0)
-    tile_ranges_kernel<<<grid_for(n_pairs, 256), 256, 0, stream>>>(sorted_keys, n_pairs,
+    launch_k(tile_ranges_kernel, grid_for(n_pairs, 256), 256, 0, stream, sorted_keys, n_pairs,
                                                                     (int2*)ranges);
   return check_launch("ss_tile_ranges");
 }
@@ -813,6 +843,8 @@ __device__ __forceinline__ int len_bucket(int len) {
 __global__ void __launch_bounds__(1024) tile_order_bucket_kernel(const int2* __restrict__ ranges,
                                                                  int n_tiles,
                                                                  int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int hist[kBuckets];
   __shared__ int cursor[kBuckets];
   for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
@@ -853,7 +885,7 @@ extern "C" int ss_tile_order(const int32_t* ranges, int32_t n_tiles, int32_t* ti
                              void* ws, size_t ws_bytes, cudaStream_t stream) {
   if (n_tiles <= 0) return set_error(SS_ERR_INVALID, "ss_tile_order: n_tiles <= 0");
   if (n_tiles <= kOrderMax) {
-    tile_order_bucket_kernel<<<1, 1024, 0, stream>>>((const int2*)ranges, n_tiles, tile_order);
+    launch_k(tile_order_bucket_kernel, 1, 1024, 0, stream, (const int2*)ranges, n_tiles, tile_order);
     return check_launch("ss_tile_order");
   }
   if (ws_bytes < ss_tile_order_workspace_bytes(n_tiles))
@@ -864,7 +896,7 @@ extern "C" int ss_tile_order(const int32_t* ranges, int32_t n_tiles, int32_t* ti
   int32_t* len = (int32_t*)(w + tb);
   int32_t* len_out = (int32_t*)((char*)len + align256(nn * 4));
   int32_t* ids = (int32_t*)((char*)len_out + align256(nn * 4));
-  tile_len_kernel<<<grid_for(n_tiles, 256), 256, 0, stream>>>((const int2*)ranges, n_tiles, len,
+  launch_k(tile_len_kernel, grid_for(n_tiles, 256), 256, 0, stream, (const int2*)ranges, n_tiles, len,
                                                                ids);
   size_t tmp = tb;
   cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(w, tmp, len, len_out, ids, tile_order,

@@ -107,6 +107,8 @@ __device__ void quantize_rot_u8(const double q[4], uint8_t out[4]) {
 
 __global__ void encode_kernel(const double* __restrict__ rows, int64_t n, int profile,
                               uint8_t* __restrict__ out, int32_t* __restrict__ bad) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double* r = rows + i * SS_ROW;
@@ -135,6 +137,8 @@ __global__ void encode_kernel(const double* __restrict__ rows, int64_t n, int pr
 // codec.py:235-266
 __global__ void decode_kernel(const uint8_t* __restrict__ data, int64_t n, int profile,
                               double* __restrict__ rows) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double* r = rows + i * SS_ROW;
@@ -184,7 +188,7 @@ extern "C" int ss_encode_records(const double* rows, int64_t n, int32_t profile,
   if (n < 0 || (profile != 0 && profile != 1))
     return set_error(SS_ERR_INVALID, "ss_encode_records: bad arguments");
   if (n == 0) return SS_OK;
-  encode_kernel<<<grid_for(n, 128), 128, 0, stream>>>(rows, n, profile, out, bad);
+  launch_k(encode_kernel, grid_for(n, 128), 128, 0, stream, rows, n, profile, out, bad);
   return check_launch("ss_encode_records");
 }
 
@@ -193,7 +197,7 @@ extern "C" int ss_decode_records(const uint8_t* data, int64_t n, int32_t profile
   if (n < 0 || (profile != 0 && profile != 1))
     return set_error(SS_ERR_INVALID, "ss_decode_records: bad arguments");
   if (n == 0) return SS_OK;
-  decode_kernel<<<grid_for(n, 128), 128, 0, stream>>>(data, n, profile, rows);
+  launch_k(decode_kernel, grid_for(n, 128), 128, 0, stream, data, n, profile, rows);
   return check_launch("ss_decode_records");
 }
 
@@ -201,6 +205,8 @@ extern "C" int ss_decode_records(const uint8_t* data, int64_t n, int32_t profile
 // (raster.py:411-425: clip, sRGB transfer, rint(255 v)) evaluated in fp64 per
 // channel value, float32 linear in, uint8 out.
 __global__ void srgb_u8_kernel(const float* __restrict__ img, int64_t n, uint8_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double x = (double)img[i];
@@ -212,6 +218,6 @@ __global__ void srgb_u8_kernel(const float* __restrict__ img, int64_t n, uint8_t
 extern "C" int ss_to_srgb_u8(const float* img, int64_t n, uint8_t* out, cudaStream_t stream) {
   if (n < 0) return set_error(SS_ERR_INVALID, "ss_to_srgb_u8: n < 0");
   if (n == 0) return SS_OK;
-  srgb_u8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(img, n, out);
+  launch_k(srgb_u8_kernel, (unsigned)((n + 255) / 256), 256, 0, stream, img, n, out);
   return check_launch("ss_to_srgb_u8");
 }

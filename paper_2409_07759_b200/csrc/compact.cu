@@ -41,6 +41,8 @@ __device__ __forceinline__ int32_t cand_row(const CandMap& m, int64_t c) {
 }
 
 __global__ void compact_count(CandMap m, int32_t* block_counts) {
+  pdl_wait();
+  pdl_trigger();
   int64_t base = (int64_t)blockIdx.x * kCompactTile;
   int cnt = 0;
 #pragma unroll
@@ -59,6 +61,8 @@ __global__ void compact_count(CandMap m, int32_t* block_counts) {
 
 // Single block: exclusive scan of block counts in place (n_blocks <= any).
 __global__ void compact_scan(int32_t* block_counts, int n_blocks, int32_t* total) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_carry;
   __shared__ int s_warp[32];
   if (threadIdx.x == 0) s_carry = 0;
@@ -97,6 +101,8 @@ __global__ void compact_scan(int32_t* block_counts, int n_blocks, int32_t* total
 
 __global__ void compact_scatter(CandMap m, const int32_t* block_offsets, int32_t* out_rows,
                                 int32_t* out_counts, const int32_t* total) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_warp[kCompactBlock / 32];
   __shared__ int s_base;
   int64_t base = (int64_t)blockIdx.x * kCompactTile;
@@ -155,8 +161,8 @@ extern "C" int ss_compact_active(const int32_t* row_start, const int32_t* row_ex
   int nb = grid_for(n_cand, kCompactTile);
   int32_t* counts = (int32_t*)ws;
   int32_t* total = counts + nb;
-  compact_count<<<nb, kCompactBlock, 0, stream>>>(m, counts);
-  compact_scan<<<1, 1024, 0, stream>>>(counts, nb, total);
-  compact_scatter<<<nb, kCompactBlock, 0, stream>>>(m, counts, out_rows, out_counts, total);
+  launch_k(compact_count, nb, kCompactBlock, 0, stream, m, counts);
+  launch_k(compact_scan, 1, 1024, 0, stream, counts, nb, total);
+  launch_k(compact_scatter, nb, kCompactBlock, 0, stream, m, counts, out_rows, out_counts, total);
   return check_launch("ss_compact_active");
 }

@@ -118,6 +118,8 @@ __device__ __forceinline__ void hblur_pair(const f2 (*vA)[kLP], const float (*vB
 // grid (tiles_x, tiles_y, 3): one CTA per 32x32 tile and channel.  The five
 // blurred moments run as two packed pairs, (x, y) and (xx, yy), plus xy.
 __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ f2 s_xy[kLR][kLP];        // (x, y) with the 5-px halo
   __shared__ f2 s_v2[2][kLT][kLP];     // vertical pass: (mu_x, mu_y), (m_xx, m_yy)
   __shared__ float s_v1[kLT][kLP];     // vertical pass: m_xy
@@ -273,6 +275,8 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
 // pass 2: blur of the partial maps as the pair (ds/dmu, ds/dmxx) + ds/dmxy
 __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, float w_ssim,
                                                                  float* __restrict__ dimg) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ f2 s_m2[kLR][kLP];
   __shared__ float s_m1[kLR][kLP];
   __shared__ f2 s_v2[kLT][kLP];
@@ -344,6 +348,8 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, floa
 
 __global__ void loss_reduce_kernel(const double* __restrict__ partials, int n_blocks,
                                    double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double s[2][32];
   double t0 = 0.0, t1 = 0.0;
   for (int i = threadIdx.x; i < n_blocks; i += blockDim.x) {
@@ -394,8 +400,8 @@ extern "C" int ss_loss_l1_ssim(const float* pred, const uint8_t* gt_u8, const fl
   const size_t plane = (size_t)width * height;
   LossArgs a{pred, gt_u8, lut, gt_f32, width, height, (float*)ws,
              (double*)((char*)ws + ((9 * plane * sizeof(float) + 255) & ~(size_t)255))};
-  ssim_fwd_kernel<<<grid, kLossThreads, 0, stream>>>(a);
-  ssim_bwd_kernel<<<grid, kLossThreads, 0, stream>>>(a, (float)ssim_weight, dimg);
-  loss_reduce_kernel<<<1, 1024, 0, stream>>>(a.partials, grid.x * grid.y * grid.z, out_sums);
+  launch_k(ssim_fwd_kernel, grid, kLossThreads, 0, stream, a);
+  launch_k(ssim_bwd_kernel, grid, kLossThreads, 0, stream, a, (float)ssim_weight, dimg);
+  launch_k(loss_reduce_kernel, 1, 1024, 0, stream, a.partials, grid.x * grid.y * grid.z, out_sums);
   return check_launch("ss_loss_l1_ssim");
 }

@@ -77,6 +77,8 @@ __global__ void __launch_bounds__(128, 5) adam_sgld_kernel(double* __restrict__ 
                                  double* __restrict__ m, double* __restrict__ v, int64_t n_rows,
                                  int32_t rows_per_gen, const ss_gen_step* __restrict__ gens,
                                  HyperK h, const double* __restrict__ eta) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_rows) return;
   const ss_gen_step gs = gens[r / rows_per_gen];
@@ -156,6 +158,7 @@ __global__ void __launch_bounds__(128, 5) adam_sgld_kernel(double* __restrict__ 
 __global__ void sgld_kernel(double* __restrict__ opt, int64_t n_rows, int32_t rows_per_gen,
                             const ss_gen_step* __restrict__ gens, HyperK h,
                             const double* __restrict__ eta) {
+  pdl_wait();
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_rows) return;
   if (!gens[r / rows_per_gen].active) return;
@@ -182,6 +185,8 @@ __global__ void reloc_flags_kernel(const double* __restrict__ opt, int64_t n_row
                                    int32_t rows_per_gen, const ss_gen_step* __restrict__ gens,
                                    double threshold, uint8_t* __restrict__ dead,
                                    uint8_t* __restrict__ alive, int32_t* __restrict__ hits) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_rows) return;
   hits[r] = 0;
@@ -199,6 +204,8 @@ __global__ void reloc_probs_kernel(const double* __restrict__ opt,
                                    const int32_t* __restrict__ alive_rows,
                                    const int32_t* __restrict__ counts, int64_t n_rows,
                                    double* __restrict__ alpha_alive) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n_rows) return;
   const int n_alive = counts[1];
@@ -207,6 +214,8 @@ __global__ void reloc_probs_kernel(const double* __restrict__ opt,
 
 __global__ void reloc_div_kernel(double* __restrict__ p, int64_t n_rows,
                                  const double* __restrict__ total) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n_rows) return;
   p[k] = p[k] / *total;
@@ -221,6 +230,8 @@ __global__ void reloc_targets_kernel(const double* __restrict__ cdf,
                                      uint32_t k1, uint32_t c0, uint32_t c1,
                                      int32_t* __restrict__ target, int32_t* __restrict__ hits,
                                      int64_t n_rows) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int n_dead = counts[0], n_alive = counts[1];
   if (k >= n_dead || n_alive == 0) return;
@@ -255,6 +266,8 @@ __global__ void reloc_clones_kernel(double* __restrict__ opt, double* __restrict
                                     const int32_t* __restrict__ target,
                                     const int32_t* __restrict__ hits,
                                     const int32_t* __restrict__ counts) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= counts[0] || counts[1] == 0) return;
   const int32_t d = dead_rows[k], t = target[k];
@@ -282,6 +295,8 @@ __global__ void reloc_clones_kernel(double* __restrict__ opt, double* __restrict
 __global__ void reloc_targets_update_kernel(double* __restrict__ opt, double* __restrict__ m,
                                             double* __restrict__ v,
                                             const int32_t* __restrict__ hits, int64_t n_rows) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_rows) return;
   const int n = hits[r];
@@ -352,6 +367,8 @@ static RelocWs carve(void* base, int64_t n) {
 }
 
 __global__ void iota32_kernel(int32_t* v, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = (int32_t)i;
 }
@@ -367,7 +384,7 @@ extern "C" int ss_adam_sgld_step(double* opt, const float* grads, double* adam_m
   if (n_rows < 0 || rows_per_gen <= 0 || !hyper)
     return set_error(SS_ERR_INVALID, "ss_adam_sgld_step: bad arguments");
   if (n_rows == 0) return SS_OK;
-  adam_sgld_kernel<<<grid_for(n_rows, 128), 128, 0, stream>>>(
+  launch_k(adam_sgld_kernel, grid_for(n_rows, 128), 128, 0, stream, 
       opt, grads, adam_m, adam_v, n_rows, rows_per_gen, gens, to_hyper(hyper), eta);
   return check_launch("ss_adam_sgld_step");
 }
@@ -377,7 +394,7 @@ extern "C" int ss_sgld(double* opt, int64_t n_rows, int32_t rows_per_gen, const 
   if (n_rows < 0 || rows_per_gen <= 0 || !hyper)
     return set_error(SS_ERR_INVALID, "ss_sgld: bad arguments");
   if (n_rows == 0) return SS_OK;
-  sgld_kernel<<<grid_for(n_rows, 128), 128, 0, stream>>>(opt, n_rows, rows_per_gen, gens,
+  launch_k(sgld_kernel, grid_for(n_rows, 128), 128, 0, stream, opt, n_rows, rows_per_gen, gens,
                                                           to_hyper(hyper), eta);
   return check_launch("ss_sgld");
 }
@@ -400,9 +417,9 @@ extern "C" int ss_relocate(double* opt, double* adam_m, double* adam_v, int64_t 
   RelocWs w = carve(base, n_rows);
   const int nb = grid_for(n_rows, 256);
   const int n = (int)n_rows;
-  reloc_flags_kernel<<<nb, 256, 0, stream>>>(opt, n_rows, rows_per_gen, gens, threshold,
+  launch_k(reloc_flags_kernel, nb, 256, 0, stream, opt, n_rows, rows_per_gen, gens, threshold,
                                              w.dead_flag, w.alive_flag, w.hits);
-  iota32_kernel<<<nb, 256, 0, stream>>>(w.row_ids, n_rows);
+  launch_k(iota32_kernel, nb, 256, 0, stream, w.row_ids, n_rows);
   size_t cb = w.cub_bytes;
   cudaError_t e = cub::DeviceSelect::Flagged(w.cub, cb, w.row_ids, w.dead_flag, w.dead_rows,
                                              out_counts, n, stream);
@@ -412,20 +429,20 @@ extern "C" int ss_relocate(double* opt, double* adam_m, double* adam_v, int64_t 
                                    out_counts + 1, n, stream);
   if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_relocate: %s", cudaGetErrorString(e));
   // p = alpha[alive] / sum(alpha[alive]); cdf = cumsum(p)  (train.py:293-294)
-  reloc_probs_kernel<<<nb, 256, 0, stream>>>(opt, w.alive_rows, out_counts, n_rows, w.p);
+  launch_k(reloc_probs_kernel, nb, 256, 0, stream, opt, w.alive_rows, out_counts, n_rows, w.p);
   cb = w.cub_bytes;
   e = cub::DeviceReduce::Sum(w.cub, cb, w.p, w.total, n, stream);
   if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_relocate: %s", cudaGetErrorString(e));
-  reloc_div_kernel<<<nb, 256, 0, stream>>>(w.p, n_rows, w.total);
+  launch_k(reloc_div_kernel, nb, 256, 0, stream, w.p, n_rows, w.total);
   cb = w.cub_bytes;
   e = cub::DeviceScan::InclusiveSum(w.cub, cb, w.p, w.cdf, n, stream);
   if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_relocate: %s", cudaGetErrorString(e));
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   const uint32_t c0 = (uint32_t)counter, c1 = (uint32_t)(counter >> 32);
-  reloc_targets_kernel<<<nb, 256, 0, stream>>>(w.cdf, w.alive_rows, out_counts, uniforms, k0, k1,
+  launch_k(reloc_targets_kernel, nb, 256, 0, stream, w.cdf, w.alive_rows, out_counts, uniforms, k0, k1,
                                                c0, c1, w.target, w.hits, n_rows);
-  reloc_clones_kernel<<<nb, 256, 0, stream>>>(opt, adam_m, adam_v, w.dead_rows, w.target, w.hits,
+  launch_k(reloc_clones_kernel, nb, 256, 0, stream, opt, adam_m, adam_v, w.dead_rows, w.target, w.hits,
                                               out_counts);
-  reloc_targets_update_kernel<<<nb, 256, 0, stream>>>(opt, adam_m, adam_v, w.hits, n_rows);
+  launch_k(reloc_targets_update_kernel, nb, 256, 0, stream, opt, adam_m, adam_v, w.hits, n_rows);
   return check_launch("ss_relocate");
 }

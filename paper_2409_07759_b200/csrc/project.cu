@@ -173,6 +173,7 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
                                    uint64_t* __restrict__ depth_key, int4* __restrict__ bbox,
                                    int32_t* __restrict__ n_tiles, float* __restrict__ geom,
                                    uint64_t* __restrict__ tile_mask) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int32_t row = rows ? rows[i] : i;
@@ -212,6 +213,7 @@ __global__ void records2d_kernel(const double* __restrict__ mean2d, const double
                                  uint64_t* __restrict__ depth_key, int4* __restrict__ bbox,
                                  int32_t* __restrict__ n_tiles, float* __restrict__ geom,
                                  uint64_t* __restrict__ tile_mask) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (rank[i] < 0) {
@@ -235,6 +237,8 @@ __global__ void basis_to_2d_kernel(const float* __restrict__ g2d, const double* 
                                    int32_t n, double* __restrict__ g_mean2d,
                                    double* __restrict__ g_inv2d, double* __restrict__ g_alpha,
                                    double* __restrict__ g_color) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || key[i] == ~0ull) return;
   const float* w = g2d + (int64_t)i * SS_G2D_ROW;
@@ -256,6 +260,7 @@ __global__ void project_bwd_kernel(StoreView store, const int32_t* __restrict__ 
                                    const uint64_t* __restrict__ depth_key,
                                    const uint8_t* __restrict__ mask, int64_t trainable_rows,
                                    float* __restrict__ grads) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (depth_key[i] == ~0ull) return;  // culled
@@ -370,6 +375,8 @@ __global__ void project_bwd_kernel(StoreView store, const int32_t* __restrict__ 
 
 __global__ void to_direct_kernel(const double* __restrict__ src, double* __restrict__ dst,
                                  int64_t n) {
+  pdl_wait();
+  pdl_trigger();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double* s = src + i * SS_ROW;
@@ -396,7 +403,7 @@ extern "C" int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_
     return set_error(SS_ERR_INVALID, "ss_project_fwd: bad camera");
   if (n == 0) return SS_OK;
   StoreView sv{store->opt, store->n_opt, store->mat};
-  project_fwd_kernel<<<grid_for(n, 128), 128, 0, stream>>>(
+  launch_k(project_fwd_kernel, grid_for(n, 128), 128, 0, stream, 
       sv, rows, n, to_camk(cam), (float4*)rec_a, (float4*)rec_b, rec_c, depth_key, (int4*)bbox,
       n_tiles, geom, tile_mask);
   return check_launch("ss_project_fwd");
@@ -409,7 +416,7 @@ extern "C" int ss_records_2d(const ss_splats2d* sp, int32_t width, int32_t heigh
   if (!sp || sp->n < 0 || width <= 0 || height <= 0)
     return set_error(SS_ERR_INVALID, "ss_records_2d: bad arguments");
   if (sp->n == 0) return SS_OK;
-  records2d_kernel<<<grid_for(sp->n, 128), 128, 0, stream>>>(
+  launch_k(records2d_kernel, grid_for(sp->n, 128), 128, 0, stream, 
       sp->mean2d, sp->inv2d, sp->alpha, sp->color, (const int4*)sp->bbox, sp->rank, sp->n, width,
       height, (float4*)rec_a, (float4*)rec_b, rec_c, depth_key, (int4*)bbox, n_tiles, geom,
       tile_mask);
@@ -421,7 +428,7 @@ extern "C" int ss_basis_to_2d(const float* g2d, const ss_splats2d* sp, const voi
                               double* g_alpha, double* g_color, cudaStream_t stream) {
   if (!sp || sp->n < 0) return set_error(SS_ERR_INVALID, "ss_basis_to_2d: bad arguments");
   if (sp->n == 0) return SS_OK;
-  basis_to_2d_kernel<<<grid_for(sp->n, 128), 128, 0, stream>>>(
+  launch_k(basis_to_2d_kernel, grid_for(sp->n, 128), 128, 0, stream, 
       g2d, sp->inv2d, (const float4*)rec_b, depth_key, sp->n, g_mean2d, g_inv2d, g_alpha, g_color);
   return check_launch("ss_basis_to_2d");
 }
@@ -433,7 +440,7 @@ extern "C" int ss_project_bwd(const ss_store* store, const int32_t* rows, int32_
   if (!store || !cam || n < 0) return set_error(SS_ERR_INVALID, "ss_project_bwd: bad arguments");
   if (n == 0) return SS_OK;
   StoreView sv{store->opt, store->n_opt, store->mat};
-  project_bwd_kernel<<<grid_for(n, 128), 128, 0, stream>>>(sv, rows, n, to_camk(cam), g2d,
+  launch_k(project_bwd_kernel, grid_for(n, 128), 128, 0, stream, sv, rows, n, to_camk(cam), g2d,
                                                             depth_key, trainable_mask,
                                                             trainable_rows, grads);
   return check_launch("ss_project_bwd");
@@ -442,6 +449,6 @@ extern "C" int ss_project_bwd(const ss_store* store, const int32_t* rows, int32_
 extern "C" int ss_to_direct(const double* src, double* dst, int64_t n, cudaStream_t stream) {
   if (n < 0) return set_error(SS_ERR_INVALID, "ss_to_direct: n < 0");
   if (n == 0) return SS_OK;
-  to_direct_kernel<<<grid_for(n, 256), 256, 0, stream>>>(src, dst, n);
+  launch_k(to_direct_kernel, grid_for(n, 256), 256, 0, stream, src, dst, n);
   return check_launch("ss_to_direct");
 }

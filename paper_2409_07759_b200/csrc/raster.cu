@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                       int n_tiles, const int32_t* __restrict__ tile_order,
                       float* __restrict__ img, float* __restrict__ t_final,
                       int32_t* __restrict__ n_contrib, const int4* __restrict__ pbox = nullptr) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ WarpStage s_stage[kWarps];
   constexpr int WPT = kTile / (2 * STRIP);  // warps per tile
   constexpr int NP = STRIP / 2;             // pixel pairs per lane
@@ -292,6 +294,8 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
                       const float* __restrict__ dimg, const float* __restrict__ t_final,
                       const int32_t* __restrict__ n_contrib, float* __restrict__ g2d,
                       DetArgs det, const int4* __restrict__ pbox = nullptr) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int64_t s_epos[kWarps][32];
   __shared__ WarpStage s_stage[kWarps];
   constexpr int WPT = kTile / (2 * STRIP);
@@ -447,6 +451,8 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
 }
 
 __global__ void rank_kernel(const int32_t* __restrict__ order, int n, int32_t* __restrict__ rank) {
+  pdl_wait();
+  pdl_trigger();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) rank[order[k]] = k;
 }
@@ -456,6 +462,7 @@ __global__ void g2d_reduce_kernel(const float* __restrict__ partial,
                                   const int32_t* __restrict__ order,
                                   const int32_t* __restrict__ offsets, int n, int wpt,
                                   float* __restrict__ g2d) {
+  pdl_wait();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   float acc[9];
@@ -505,9 +512,9 @@ extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const v
   const int wpt = kTile / (2 * g_strip_fwd);
   const int blocks = (n_tiles * wpt + kWarps - 1) / kWarps;
 #define SS_FWD(S)                                                                             \
-  raster_fwd_kernel<S><<<blocks, kWarps * 32, 0, stream>>>(                                   \
+  launch_k(raster_fwd_kernel<S>, blocks, kWarps * 32, 0, stream,                                    \
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
-      height, tiles_x, n_tiles, tile_order, img, t_final, n_contrib)
+      height, tiles_x, n_tiles, tile_order, img, t_final, n_contrib, nullptr)
   if (g_strip_fwd == 8) SS_FWD(8);
   else if (g_strip_fwd == 4) SS_FWD(4);
   else SS_FWD(2);
@@ -527,9 +534,9 @@ static int raster_bwd_launch(const int32_t* ranges, const int32_t* vals, const v
   const int blocks = (n_tiles * wpt + kWarps - 1) / kWarps;
   DetArgs d = det ? *det : DetArgs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 #define SS_BWD(S, D)                                                                          \
-  raster_bwd_kernel<S, D><<<blocks, kWarps * 32, 0, stream>>>(                                \
+  launch_k(raster_bwd_kernel<S, D>, blocks, kWarps * 32, 0, stream,                                 \
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
-      height, tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d)
+      height, tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d, nullptr)
   if (det) {
     if (g_strip == 8) SS_BWD(8, true);
     else if (g_strip == 4) SS_BWD(4, true);
@@ -560,7 +567,7 @@ int raster_fwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
   const int blocks = (n_tiles * 2 + kWarps - 1) / kWarps;
-  raster_fwd_kernel<4, true><<<blocks, kWarps * 32, 0, stream>>>(
+  launch_k(raster_fwd_kernel<4, true>, blocks, kWarps * 32, 0, stream, 
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
       tiles_x, n_tiles, tile_order, img, t_final, n_contrib, (const int4*)pbox);
   return check_launch("raster_fwd_bbox");
@@ -575,7 +582,7 @@ int raster_bwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_
   const int n_tiles = tiles_x * tiles_y;
   const int blocks = (n_tiles * 2 + kWarps - 1) / kWarps;
   const DetArgs d{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  raster_bwd_kernel<4, false, true><<<blocks, kWarps * 32, 0, stream>>>(
+  launch_k(raster_bwd_kernel<4, false, true>, blocks, kWarps * 32, 0, stream, 
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
       tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d, (const int4*)pbox);
   return check_launch("raster_bwd_bbox");
@@ -592,12 +599,12 @@ extern "C" int ss_raster_bwd_deterministic(
     const int32_t* offsets, const int32_t* bbox, const uint64_t* tile_mask, const float* geom,
     int32_t n, int32_t* rank, float* partial, float* g2d, cudaStream_t stream) {
   if (n <= 0) return SS_OK;
-  rank_kernel<<<grid_for(n, 256), 256, 0, stream>>>(order, n, rank);
+  launch_k(rank_kernel, grid_for(n, 256), 256, 0, stream, order, n, rank);
   DetArgs d{partial, rank, offsets, (const int4*)bbox, tile_mask, geom};
   int rc = raster_bwd_launch(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, dimg,
                              t_final, n_contrib, g2d, &d, stream);
   if (rc) return rc;
-  g2d_reduce_kernel<<<grid_for(n, 128), 128, 0, stream>>>(partial, order, offsets, n,
+  launch_k(g2d_reduce_kernel, grid_for(n, 128), 128, 0, stream, partial, order, offsets, n,
                                                            kTile / (2 * g_strip), g2d);
   return check_launch("ss_raster_bwd_deterministic");
 }

@@ -173,6 +173,35 @@ __device__ __forceinline__ void fma2_acc(f2& c, f2 a, f2 b) { c = __ffma2_rn(a, 
 __device__ __forceinline__ void sub2_acc(f2& c, f2 a) { c = sub2(c, a); }
 __device__ __forceinline__ void mul2_acc(f2& c, f2 a) { c = __fmul2_rn(c, a); }
 
+
+// Programmatic dependent launch (sm_90+): every kernel of the library is
+// launched with programmatic stream serialisation, so its CTAs may be
+// scheduled while the previous kernel in the stream is finishing; each kernel
+// begins with pdl_wait() (griddepcontrol.wait: the previous grid has completed
+// and its writes are visible), so the data dependence is unchanged -- only
+// the launch gap between consecutive kernels is hidden.  pdl_trigger()
+// (griddepcontrol.launch_dependents) lets the next kernel be scheduled early;
+// multi-wave kernels leave it to their exit so waiting dependents do not take
+// SM slots from their later waves.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t stream, Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Philox4x32-10 counter-based generator (Salmon et al., SC'11).
 struct Philox4 {
   uint32_t v[4];

@@ -16,6 +16,8 @@ using namespace ss;
 // one atomic per CTA.
 __global__ void __launch_bounds__(256) sum_kernel(const int32_t* __restrict__ v, int32_t n,
                                                   int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t s_part[8];
   int32_t acc = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -98,7 +100,7 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
       return check_launch("ss_render_fwd: pinned pair count");
   }
   cudaMemsetAsync(v->offsets + n, 0, sizeof(int32_t), stream);
-  sum_kernel<<<min(296, (n + 255) / 256), 256, 0, stream>>>(v->n_tiles, n, v->offsets + n);
+  launch_k(sum_kernel, min(296, (n + 255) / 256), 256, 0, stream, v->n_tiles, n, v->offsets + n);
   if (cudaMemcpyAsync(k_pinned, v->offsets + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream) !=
           cudaSuccess ||
       cudaEventRecord(k_event, stream) != cudaSuccess)

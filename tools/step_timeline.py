@@ -35,7 +35,7 @@ def main():
         progress = bench.LossReadback(state.device)
     train.train_swin(window[0], window[1], state, ds, iterations=5, progress=progress)
     torch.cuda.synchronize()
-    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
         train.train_swin(window[0], window[1], state, ds, iterations=a.steps, progress=progress)
         if progress is not None:
             progress.flush()
