@@ -3,6 +3,11 @@ kernel time by name, GPU busy time vs the step's wall span, i.e. the idle gaps
 that launch overhead and the per-view host sync leave.
 
     python tools/step_timeline.py [--steps 5] [--config 3]
+
+With programmatic dependent launch (every library kernel) a kernel's CTAs
+start early and wait for their predecessor inside the kernel, so per-kernel
+durations here include that wait; the merged busy / idle totals stay valid.
+Per-kernel times: the ncu launch list (profiles/) or bench.py's events.
 """
 
 import argparse
