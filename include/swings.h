@@ -349,6 +349,10 @@ int ss_event_create(void** ev);
 int ss_event_destroy(void* ev);
 int ss_event_elapsed_ms(void* start, void* end, float* ms);
 
+/* Zero fill (a library kernel, launched with programmatic dependent launch
+ * like the others, unlike a driver memset). */
+int ss_memzero(void* ptr, size_t bytes, ss_stream_t stream);
+
 /* Direct-space snapshot of optimizable rows (train.py:155-161 + 474):
  * dst[i] = (mean, quat, exp(log_scale), sigmoid(logit), color) of src[i]. */
 int ss_to_direct(const double* src, double* dst, int64_t n, ss_stream_t stream);

@@ -99,6 +99,7 @@ _SIGNATURES = {
     "ss_relocate": ([P, P, P, I64, I32, P, c_double, P, c_uint64, c_uint64, P, P, c_size_t, P],
                     c_int),
     "ss_to_direct": ([P, P, I64, P], c_int),
+    "ss_memzero": ([P, c_size_t, P], c_int),
     "ss_to_srgb_u8": ([P, I64, P, P], c_int),
     "ss_render_fwd": ([POINTER(SSStore), POINTER(SSCamera), POINTER(SSView), P], c_int),
     "ss_render2d_fwd": ([POINTER(SSSplats2D), I32, I32, POINTER(SSView), P], c_int),

@@ -663,7 +663,7 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
   int2* long_runs = (int2*)((char*)u64a + align256(nn * 4));
   const uint32_t nb = (uint32_t)(kBucketsPerKey * nn);
   int32_t* hist = big;  // nb + 1 counts, scanned in place into the bucket cursors
-  cudaMemsetAsync(scratch32, 0, 2 * sizeof(int32_t) + 2 * sizeof(unsigned long long), stream);
+  memzero(scratch32, 2 * sizeof(int32_t) + 2 * sizeof(unsigned long long), stream);
   launch_k(depth_range_kernel, min(296, (n + 255) / 256), 256, 0, stream, depth_key, n, range, hist,
                                                                       (int32_t)nb + 1);
   launch_k(depth_hist_kernel, grid_for(n, 256), 256, 0, stream, depth_key, n, range, nb, hist);
@@ -762,7 +762,7 @@ extern "C" int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const 
   if (ws_bytes < ss_bin_tiles_workspace_bytes(n_pairs, n_tiles))
     return set_error(SS_ERR_WORKSPACE, "ss_bin_tiles: workspace too small");
   if (n == 0 || n_pairs == 0) {
-    cudaMemsetAsync(ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, stream);
+    memzero(ranges, sizeof(int32_t) * 2 * (size_t)n_tiles, stream);
     return check_launch("ss_bin_tiles");
   }
   const int C = bin_chunks(n_pairs, n_tiles);
@@ -819,7 +819,7 @@ extern "C" int ss_sort_tile_pairs(uint32_t* keys, int32_t* vals, uint32_t* keys_
 extern "C" int ss_tile_ranges(const uint32_t* sorted_keys, int64_t n_pairs, int32_t n_tiles,
                               int32_t* ranges, cudaStream_t stream) {
   if (n_pairs < 0 || n_tiles <= 0) return set_error(SS_ERR_INVALID, "ss_tile_ranges: bad sizes");
-  cudaMemsetAsync(ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, stream);
+  memzero(ranges, sizeof(int32_t) * 2 * (size_t)n_tiles, stream);
   if (n_pairs > 0)
     launch_k(tile_ranges_kernel, grid_for(n_pairs, 256), 256, 0, stream, sorted_keys, n_pairs,
                                                                     (int2*)ranges);

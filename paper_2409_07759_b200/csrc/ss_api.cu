@@ -22,7 +22,38 @@ int check_launch(const char* what) {
   return SS_OK;
 }
 
+// Zero fill launched like every other library kernel (programmatic dependent
+// launch), so it does not break the launch-gap hiding the way a driver
+// memset between two kernels does.  16-byte stores where aligned.
+__global__ void memzero_kernel(unsigned char* __restrict__ p, size_t bytes) {
+  pdl_wait();
+  pdl_trigger();
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t head = (16 - ((uintptr_t)p & 15)) & 15;
+  const size_t h = head < bytes ? head : bytes;
+  for (size_t i = tid; i < h; i += stride) p[i] = 0;
+  const size_t nv = (bytes - h) / 16;
+  uint4* v = reinterpret_cast<uint4*>(p + h);
+  for (size_t i = tid; i < nv; i += stride) v[i] = make_uint4(0, 0, 0, 0);
+  for (size_t i = h + nv * 16 + tid; i < bytes; i += stride) p[i] = 0;
+}
+
+int memzero(void* p, size_t bytes, cudaStream_t stream) {
+  if (bytes == 0) return SS_OK;
+  size_t blocks = (bytes / 16 + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  launch_k(memzero_kernel, (unsigned)blocks, 256, 0, stream, (unsigned char*)p, bytes);
+  return check_launch("memzero");
+}
+
 }  // namespace ss
+
+extern "C" int ss_memzero(void* ptr, size_t bytes, cudaStream_t stream) {
+  if (!ptr && bytes) return ss::set_error(SS_ERR_INVALID, "ss_memzero: null pointer");
+  return ss::memzero(ptr, bytes, stream);
+}
 
 extern "C" const char* ss_last_error(void) { return ss::g_err; }
 

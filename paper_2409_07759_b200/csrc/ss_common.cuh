@@ -242,3 +242,6 @@ int raster_bwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_
                     const int32_t* tile_order, const float* dimg, const float* t_final,
                     const int32_t* n_contrib, float* g2d, const int32_t* pbox,
                     cudaStream_t stream);
+namespace ss {
+int memzero(void* p, size_t bytes, cudaStream_t stream);  // ss_api.cu: PDL zero fill
+}

@@ -68,9 +68,9 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   v->sorted_sel = 0;
   int rc;
   if (n == 0) {
-    cudaMemsetAsync(v->img, 0, sizeof(float) * 3 * (size_t)W * H, stream);
-    cudaMemsetAsync(v->n_contrib, 0, sizeof(int32_t) * (size_t)W * H, stream);
-    cudaMemsetAsync(v->ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, stream);
+    memzero(v->img, sizeof(float) * 3 * (size_t)W * H, stream);
+    memzero(v->n_contrib, sizeof(int32_t) * (size_t)W * H, stream);
+    memzero(v->ranges, sizeof(int32_t) * 2 * (size_t)n_tiles, stream);
     return check_launch("ss_render_fwd");
   }
   size_t need_ws = ss_binning_workspace_bytes(n, v->pair_cap > 0 ? v->pair_cap : 1, n_tiles);
@@ -99,7 +99,7 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
         cudaEventCreateWithFlags(&k_event, cudaEventDisableTiming) != cudaSuccess)
       return check_launch("ss_render_fwd: pinned pair count");
   }
-  cudaMemsetAsync(v->offsets + n, 0, sizeof(int32_t), stream);
+  memzero(v->offsets + n, sizeof(int32_t), stream);
   launch_k(sum_kernel, min(296, (n + 255) / 256), 256, 0, stream, v->n_tiles, n, v->offsets + n);
   if (cudaMemcpyAsync(k_pinned, v->offsets + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream) !=
           cudaSuccess ||
@@ -175,7 +175,7 @@ extern "C" int ss_render2d_bwd(const ss_splats2d* sp, int32_t width, int32_t hei
                                cudaStream_t stream) {
   if (!sp || !v) return set_error(SS_ERR_INVALID, "ss_render2d_bwd: bad args");
   if (v->n == 0 || v->n_pairs == 0) return SS_OK;
-  cudaMemsetAsync(g2d, 0, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
+  memzero(g2d, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
   const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
   int rc = raster_bwd_bbox(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, width, height,
                            v->tile_order, dimg, v->t_final, v->n_contrib, g2d, v->bbox, stream);
@@ -189,7 +189,7 @@ extern "C" int ss_render_bwd(const ss_store* store, const ss_camera* cam, const 
                              int64_t trainable_rows, float* grads, cudaStream_t stream) {
   if (!store || !cam || !v) return set_error(SS_ERR_INVALID, "ss_render_bwd: bad args");
   if (v->n == 0 || v->n_pairs == 0) return SS_OK;
-  cudaMemsetAsync(g2d, 0, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
+  memzero(g2d, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
   const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
   record(v->events[2], stream);
   int rc;

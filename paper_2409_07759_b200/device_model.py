@@ -229,7 +229,7 @@ class DeviceModel:
         stepped = stepped_generations(state.slices, frames)
         self._gen_table(stepped)
         rows, n, n_opt_here = self.compact(frame)
-        self.grads.zero_()
+        L.check(lib.ss_memzero(L.ptr(self.grads), self.grads.numel() * 4, sp), "memzero")
         cam = dataset.cameras[view]
         # ground truth may still be in flight on a copy stream: only the loss
         # waits for it, the projection / binning / raster run meanwhile
