@@ -184,6 +184,121 @@ __global__ void __launch_bounds__(1024) long_runs_kernel(const uint64_t* __restr
   }
 }
 
+// Exclusive scan of N int32 in three library kernels (so the whole chain
+// keeps programmatic dependent launch): per-block sums, one CTA over the
+// block sums, per-block scan + offset.  GATHER: element e < n is
+// in[order[e]] (tile counts in rank order), element n is 0; otherwise in[e].
+// In place (in == out) is fine: each element is read and written by the same
+// thread in the last pass.
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <bool GATHER>
+__device__ __forceinline__ int32_t scan_in(const int32_t* in, const int32_t* order, int n,
+                                           int64_t e) {
+  if (GATHER) return e < n ? in[order[e]] : 0;
+  return in[e];
+}
+
+__device__ __forceinline__ int32_t block_exclusive(int32_t v, int32_t* s_warp, int32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    s_warp[lane] = w;
+  }
+  __syncthreads();
+  total = s_warp[31];
+  const int32_t before = warp > 0 ? s_warp[warp - 1] : 0;
+  return before + inc - v;
+}
+
+template <bool GATHER>
+__global__ void __launch_bounds__(kScanThreads) scan_sums_kernel(const int32_t* __restrict__ in,
+                                                                 const int32_t* __restrict__ order,
+                                                                 int32_t n, int64_t N,
+                                                                 int32_t* __restrict__ sums) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int32_t s_warp[32];
+  const int64_t e0 = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int32_t v = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (e0 + k < N) v += scan_in<GATHER>(in, order, n, e0 + k);
+  int32_t total;
+  block_exclusive(v, s_warp, total);
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_top_kernel(int32_t* __restrict__ sums,
+                                                                int32_t nblocks) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int32_t s_warp[32];
+  // sequential chunks of the block sums, carried across iterations
+  int32_t carry = 0;
+  for (int base = 0; base < nblocks; base += kScanThreads) {
+    const int i = base + threadIdx.x;
+    const int32_t v = i < nblocks ? sums[i] : 0;
+    int32_t total;
+    const int32_t ex = block_exclusive(v, s_warp, total);
+    if (i < nblocks) sums[i] = carry + ex;
+    carry += total;
+    __syncthreads();
+  }
+}
+
+template <bool GATHER>
+__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const int32_t* in,
+                                                                 const int32_t* __restrict__ order,
+                                                                 int32_t n, int64_t N,
+                                                                 const int32_t* __restrict__ sums,
+                                                                 int32_t* out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int32_t s_warp[32];
+  const int64_t e0 = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int32_t x[kScanItems];
+  int32_t v = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    x[k] = e0 + k < N ? scan_in<GATHER>(in, order, n, e0 + k) : 0;
+    v += x[k];
+  }
+  int32_t total;
+  int32_t run = sums[blockIdx.x] + block_exclusive(v, s_warp, total);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (e0 + k < N) out[e0 + k] = run;
+    run += x[k];
+  }
+}
+
+template <bool GATHER>
+static int exclusive_scan(const int32_t* in, const int32_t* order, int32_t n, int64_t N,
+                          int32_t* out, int32_t* block_sums, cudaStream_t stream) {
+  const int nblocks = (int)((N + kScanTile - 1) / kScanTile);
+  launch_k(scan_sums_kernel<GATHER>, nblocks, kScanThreads, 0, stream, in, order, n, N, block_sums);
+  launch_k(scan_top_kernel, 1, kScanThreads, 0, stream, block_sums, nblocks);
+  launch_k(scan_down_kernel<GATHER>, nblocks, kScanThreads, 0, stream, in, order, n, N, block_sums,
+           out);
+  return check_launch("exclusive_scan");
+}
+
 __global__ void gather_counts_kernel(const int32_t* __restrict__ order,
                                      const int32_t* __restrict__ n_tiles, int32_t n,
                                      int32_t* __restrict__ out) {
@@ -667,9 +782,9 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
   launch_k(depth_range_kernel, min(296, (n + 255) / 256), 256, 0, stream, depth_key, n, range, hist,
                                                                       (int32_t)nb + 1);
   launch_k(depth_hist_kernel, grid_for(n, 256), 256, 0, stream, depth_key, n, range, nb, hist);
-  size_t tmp_bytes = tb;
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(w, tmp_bytes, hist, hist, (int)nb + 1, stream);
-  if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_depth_order: %s", cudaGetErrorString(e));
+  // block sums after n_long / pad / range in the scratch32 region
+  int rc = exclusive_scan<false>(hist, nullptr, 0, (int64_t)nb + 1, hist, scratch32 + 8, stream);
+  if (rc) return rc;
   launch_k(depth_scatter_kernel, grid_for(n, 256), 256, 0, stream, depth_key, n, range, nb, hist, order,
                                                              bucket_of);
   launch_k(fix_runs_kernel, grid_for(n, 256), 256, 0, stream, bucket_of, depth_key, n, order, long_runs,
@@ -694,12 +809,9 @@ extern "C" int ss_tile_offsets(const int32_t* order, const int32_t* n_tiles, int
   if (ws_bytes < need) return set_error(SS_ERR_WORKSPACE, "ss_tile_offsets: workspace too small");
   char* w = (char*)ws;
   size_t tb = align256(cub_bytes(n, 1));
-  int32_t* cnt = (int32_t*)(w + tb);
-  launch_k(gather_counts_kernel, grid_for(n + 1, 256), 256, 0, stream, order, n_tiles, n, cnt);
-  size_t tmp_bytes = tb;
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(w, tmp_bytes, cnt, offsets, n + 1, stream);
-  if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_tile_offsets: %s", cudaGetErrorString(e));
-  return check_launch("ss_tile_offsets");
+  int32_t* block_sums = (int32_t*)(w + tb);  // the n+1 int32 scratch region
+  // offsets[k] = sum of the kept-tile counts of ranks < k (gathered on the fly)
+  return exclusive_scan<true>(n_tiles, order, n, (int64_t)n + 1, offsets, block_sums, stream);
 }
 
 extern "C" int ss_emit_tile_pairs(const int32_t* order, const int32_t* offsets,
