@@ -22,7 +22,7 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
-]
+] + os.environ.get("SS_NVCC_EXTRA", "").split()  # developer knob: extra -D for experiments
 
 
 def nvcc() -> str:

@@ -39,11 +39,6 @@ __device__ __forceinline__ constexpr float win(int t) {
                            : 0.26601171493530273f;
 }
 
-__device__ __forceinline__ float gt_value(const uint8_t* gt_u8, const float* lut,
-                                          const float* gt_f32, int64_t idx) {
-  return gt_u8 ? lut[gt_u8[idx]] : gt_f32[idx];
-}
-
 struct LossArgs {
   const float* pred;
   const uint8_t* gt_u8;
@@ -55,6 +50,7 @@ struct LossArgs {
 };
 
 constexpr int kWarpsL = kLossThreads / 32;
+
 
 // Separable 11-tap blur of one packed pair (A) and one scalar (B) quantity.
 // Vertical pass: task = (column c of the 42-wide region, 8 output rows);
@@ -127,36 +123,35 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
   __shared__ double s_red[2][kWarpsL];
   const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT, ch = blockIdx.z;
   const int W = a.width, H = a.height;
-  const int64_t plane = (int64_t)W * H;
+  const int plane = W * H;  // 9 W H < 2^31 (checked on the host): 32-bit offsets
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (a.gt_u8)
     for (int i = threadIdx.x; i < 256; i += kLossThreads) s_lut[i] = a.lut[i];
   __syncthreads();
   // region rows by warp, columns by lane; every load of the thread is issued
-  // before the first use (one memory round trip instead of one per row)
+  // before the first use (one memory round trip instead of one per row).
+  // Offsets are hoisted: row k adds k * 8 rows to one base offset.
   constexpr int kRW = (kLR + kWarpsL - 1) / kWarpsL;  // rows per warp
+  const int gx0 = x0 - kHalo + lane;
+  const bool col_in[2] = {(unsigned)gx0 < (unsigned)W,
+                          lane + 32 < kLR && (unsigned)(gx0 + 32) < (unsigned)W};
+  const int gy0 = y0 - kHalo + warp;
+  const int base = (gy0 * W + gx0) * 3 + ch;
+  const int row_step = kWarpsL * 3 * W;
   float xv[kRW][2];
-  float yf[kRW][2];
-  int yb[kRW][2];
+  uint32_t yv[kRW][2];  // u8: the byte or ~0u (outside); f32: the bits
 #pragma unroll
   for (int k = 0; k < kRW; ++k) {
-    const int r = warp + kWarpsL * k;
-    const int gy = y0 - kHalo + r;
-    const int64_t rowbase = ((int64_t)gy * W + (x0 - kHalo)) * 3 + ch;
+    const bool row_in = warp + kWarpsL * k < kLR && (unsigned)(gy0 + kWarpsL * k) < (unsigned)H;
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
-      const int q = lane + 32 * m;
-      const int gx = x0 - kHalo + q;
-      const bool in = r < kLR && q < kLR && gy >= 0 && gy < H && gx >= 0 && gx < W;
-      const int64_t e = rowbase + 3 * q;
+      const bool in = row_in && col_in[m];
+      const int e = base + k * row_step + 96 * m;
       xv[k][m] = in ? a.pred[e] : 0.f;
-      if (a.gt_u8) {
-        yb[k][m] = in ? (int)a.gt_u8[e] : -1;
-        yf[k][m] = 0.f;
-      } else {
-        yb[k][m] = 0;
-        yf[k][m] = in ? a.gt_f32[e] : 0.f;
-      }
+      if (a.gt_u8)
+        yv[k][m] = in ? (uint32_t)a.gt_u8[e] : ~0u;
+      else
+        yv[k][m] = in ? __float_as_uint(a.gt_f32[e]) : 0u;
     }
   }
 #pragma unroll
@@ -166,7 +161,8 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
     for (int m = 0; m < 2; ++m) {
       const int q = lane + 32 * m;
       if (r < kLR && q < kLR) {
-        const float y = a.gt_u8 ? (yb[k][m] >= 0 ? s_lut[yb[k][m]] : 0.f) : yf[k][m];
+        const uint32_t yr = yv[k][m];
+        const float y = a.gt_u8 ? (yr != ~0u ? s_lut[yr] : 0.f) : __uint_as_float(yr);
         s_xy[r][q] = pk2(xv[k][m], y);
       }
     }
@@ -240,7 +236,7 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
       const float ds_dmu = (2.f * mu_y * (a2 - a1) - 2.f * mu_x * sv * (b2 - b1)) * inv_den;
       const float ds_dmxx = -sv * inv_b2;
       const float ds_dmxy = 2.f * a1 * inv_den;
-      const int64_t pix = (int64_t)gy * W + gx;
+      const int pix = gy * W + gx;
       a.maps[(0 * 3 + ch) * plane + pix] = ds_dmu;
       a.maps[(1 * 3 + ch) * plane + pix] = ds_dmxx;
       a.maps[(2 * 3 + ch) * plane + pix] = ds_dmxy;
@@ -286,38 +282,44 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, floa
     for (int i = threadIdx.x; i < 256; i += kLossThreads) s_lut[i] = a.lut[i];
   const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT, ch = blockIdx.z;
   const int W = a.width, H = a.height;
-  const int64_t plane = (int64_t)W * H;
+  const int plane = W * H;  // 9 W H < 2^31 (checked on the host)
   const float inv_n = 1.0f / (float)((double)plane * 3.0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float* m0 = a.maps + (0 * 3 + ch) * plane;
   const float* m1 = a.maps + (1 * 3 + ch) * plane;
   const float* m2 = a.maps + (2 * 3 + ch) * plane;
   constexpr int kRW = (kLR + kWarpsL - 1) / kWarpsL;  // rows per warp
+  const int gx0 = x0 - kHalo + lane;
+  const bool col_in[2] = {(unsigned)gx0 < (unsigned)W,
+                          lane + 32 < kLR && (unsigned)(gx0 + 32) < (unsigned)W};
+  const int gy0 = y0 - kHalo + warp;
+  const int base = gy0 * W + gx0;
   float u[kRW][2][3];
 #pragma unroll
   for (int k = 0; k < kRW; ++k) {
-    const int r = warp + kWarpsL * k;
-    const int gy = y0 - kHalo + r;
-    const int64_t rowbase = (int64_t)gy * W + (x0 - kHalo);
+    const bool row_in = warp + kWarpsL * k < kLR && (unsigned)(gy0 + kWarpsL * k) < (unsigned)H;
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
-      const int q = lane + 32 * m;
-      const int gx = x0 - kHalo + q;
-      const bool in = r < kLR && q < kLR && gy >= 0 && gy < H && gx >= 0 && gx < W;
-      u[k][m][0] = in ? m0[rowbase + q] : 0.f;
-      u[k][m][1] = in ? m1[rowbase + q] : 0.f;
-      u[k][m][2] = in ? m2[rowbase + q] : 0.f;
+      const bool in = row_in && col_in[m];
+      const int e = base + k * kWarpsL * W + 32 * m;
+      u[k][m][0] = in ? m0[e] : 0.f;
+      u[k][m][1] = in ? m1[e] : 0.f;
+      u[k][m][2] = in ? m2[e] : 0.f;
     }
   }
+  const int r = threadIdx.x / (kLT / kHC), c0 = (threadIdx.x % (kLT / kHC)) * kHC;
+  const int gy = y0 + r;
+  const int eo = (gy * W + x0 + c0) * 3 + ch;
+
 #pragma unroll
   for (int k = 0; k < kRW; ++k) {
-    const int r = warp + kWarpsL * k;
+    const int rr = warp + kWarpsL * k;
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
       const int q = lane + 32 * m;
-      if (r < kLR && q < kLR) {
-        s_m2[r][q] = pk2(u[k][m][0], u[k][m][1]);
-        s_m1[r][q] = u[k][m][2];
+      if (rr < kLR && q < kLR) {
+        s_m2[rr][q] = pk2(u[k][m][0], u[k][m][1]);
+        s_m1[rr][q] = u[k][m][2];
       }
     }
   }
@@ -327,22 +329,31 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, floa
     vb = s_m1[r][c];
   });
   __syncthreads();
-  const int r = threadIdx.x / (kLT / kHC), c0 = (threadIdx.x % (kLT / kHC)) * kHC;
   f2 bl2[kHC];
   float bl1[kHC];
-  hblur_pair(s_v2, s_v1, r, c0, bl2, bl1);
-  const int gy = y0 + r;
+  // the outputs' x and y are loaded only now (loading them with the maps
+  // costs 18 registers and one resident CTA per SM: measured slower)
+  float xo[kHC];
+  uint32_t yo[kHC];
 #pragma unroll
   for (int i = 0; i < kHC; ++i) {
-    const int gx = x0 + c0 + i;
-    if (gy >= H || gx >= W) continue;
-    const int64_t e = ((int64_t)gy * W + gx) * 3 + ch;
-    const float x = a.pred[e];
-    const float y = gt_value(a.gt_u8, s_lut, a.gt_f32, e);
+    const bool in = gy < H && x0 + c0 + i < W;
+    xo[i] = in ? a.pred[eo + 3 * i] : 0.f;
+    if (a.gt_u8)
+      yo[i] = in ? (uint32_t)a.gt_u8[eo + 3 * i] : 0u;
+    else
+      yo[i] = in ? __float_as_uint(a.gt_f32[eo + 3 * i]) : 0u;
+  }
+  hblur_pair(s_v2, s_v1, r, c0, bl2, bl1);
+#pragma unroll
+  for (int i = 0; i < kHC; ++i) {
+    if (gy >= H || x0 + c0 + i >= W) continue;
+    const float x = xo[i];
+    const float y = a.gt_u8 ? s_lut[yo[i]] : __uint_as_float(yo[i]);
     const float grad = (lo2(bl2[i]) + 2.f * x * hi2(bl2[i]) + y * bl1[i]) * inv_n;
     const float d = x - y;
     const float sgn = (d > 0.f) ? 1.f : ((d < 0.f) ? -1.f : 0.f);
-    dimg[e] = (1.f - w_ssim) * sgn * inv_n - w_ssim * grad;
+    dimg[eo + 3 * i] = (1.f - w_ssim) * sgn * inv_n - w_ssim * grad;
   }
 }
 
@@ -393,6 +404,8 @@ extern "C" int ss_loss_l1_ssim(const float* pred, const uint8_t* gt_u8, const fl
                                size_t ws_bytes, cudaStream_t stream) {
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_loss: bad size");
   if (!gt_u8 && !gt_f32) return set_error(SS_ERR_INVALID, "ss_loss: no ground truth");
+  if (9 * (int64_t)width * height >= ((int64_t)1 << 31))
+    return set_error(SS_ERR_INVALID, "ss_loss: frame too large (9 W H must fit 31 bits)");
   if (gt_u8 && !lut) return set_error(SS_ERR_INVALID, "ss_loss: u8 ground truth needs a LUT");
   if (ws_bytes < ss_loss_workspace_bytes(width, height))
     return set_error(SS_ERR_WORKSPACE, "ss_loss: workspace too small");
