@@ -126,6 +126,7 @@ class DeviceModel:
         self.seed = philox_seed(cfg.rng_seed)
         self.store = Store(opt=self.opt, mat=self.mat)
         self.dirty = True
+        self._life_sig = None
         self.last_sums = None
         self.last_counts = (0, 0)
 
@@ -134,6 +135,14 @@ class DeviceModel:
         self.dirty = True
 
     def sync_lifespans(self):
+        sig = (tuple((g.lifespan.start, g.lifespan.expire) for g in self.state.slices),
+               tuple((m.block, m.lifespan.start, m.lifespan.expire) for m in self.state.matured))
+        if sig == self._life_sig:
+            # marked dirty but unchanged (e.g. a train_swin call on the same
+            # window): row tables and compacted frames stay valid
+            self.dirty = False
+            return
+        self._life_sig = sig
         self._active_cache = {}
         sl, n_opt = self.sl, self.num_gs
         for i, gen in enumerate(self.state.slices):

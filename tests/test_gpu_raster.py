@@ -392,6 +392,26 @@ def g_keys():
     return ("mean", "log_scale", "quat", "opacity_logit", "color")
 
 
+def test_wide_frame_chunked_binning(ss):
+    """A 2048x1536 frame (12288 tiles, 2/3 of the chunked binning's shared-
+    memory limit): keys stay bit-exact against the oracle."""
+    P, R = ss
+    from paper_2409_07759_b200 import _lib as L
+    rng = np.random.default_rng(23)
+    n = 4000
+    means = rng.uniform((-1.2, -0.9, 2.0), (1.2, 0.9, 4.0), size=(n, 3))
+    scales = np.exp(rng.uniform(np.log(0.003), np.log(0.03), size=(n, 3)))
+    scales[:20] = rng.uniform(0.2, 0.4, size=(20, 3))
+    arr = P.GaussianArrays(means, random_unit_quats(rng, n), scales, rng.uniform(0.1, 0.9, n),
+                           rng.uniform(0, 1, (n, 3)))
+    from conftest import Cam
+    ocam = Cam(2048, 1536, 1200.0, 1200.0, 1024.0, 768.0, np.eye(3), np.zeros(3))
+    tiles = (2048 // 16) * (1536 // 16)
+    assert 11 * 1024 < tiles <= 18 * 1024
+    assert L.lib().ss_bin_tiles_supported(1 << 20, tiles)
+    _tile_check(P, R, cam_from(P, ocam), arr, ocam)
+
+
 def test_large_frame_uses_pair_sort_fallback(ss):
     """A frame with more 16x16 tiles than the chunked binning's shared-memory
     cursors hold (> 18432) falls back to emit + pair sort automatically; keys
