@@ -57,12 +57,6 @@ __device__ __forceinline__ float rcp(float x) {
   return y;
 }
 
-// (k, k + 1) and (k^2, (k + 1)^2) for pair p (k = 2p)
-__device__ __forceinline__ f2 kpair(int p) { return pk2((float)(2 * p), (float)(2 * p + 1)); }
-__device__ __forceinline__ f2 kkpair(int p) {
-  return pk2((float)(4 * p * p), (float)((2 * p + 1) * (2 * p + 1)));
-}
-
 struct WarpStage {
   float4 a[32];
   float4 b[32];
@@ -111,6 +105,25 @@ __device__ __forceinline__ float strip_exp(const StripQuad& s, int k) {
   if (k == 0) return s.q0;
   if (k == 1) return (s.q0 + s.lin) + s.quad;
   return fmaf((float)(k * k), s.quad, fmaf((float)k, s.lin, s.q0));
+}
+
+// The strip's exponents as packed pairs, by forward differences:
+// e_{k+1} = e_k + d_k, d_k = lin + (2k + 1) quad.  Plain two-register FADDs
+// (no (k, k^2) constant pairs to keep in registers or rematerialise per
+// entry); the rounding differs from the direct form by a few ulp of e.
+template <int NP>
+__device__ __forceinline__ void strip_exps(const StripQuad& s, f2 e[NP]) {
+  float ev[2 * NP];
+  const float q2 = s.quad + s.quad;
+  float d = s.lin + s.quad;
+  ev[0] = s.q0;
+#pragma unroll
+  for (int k = 1; k < 2 * NP; ++k) {
+    ev[k] = ev[k - 1] + d;
+    if (k + 1 < 2 * NP) d += q2;
+  }
+#pragma unroll
+  for (int p = 0; p < NP; ++p) e[p] = pk2(ev[2 * p], ev[2 * p + 1]);
 }
 
 // BB: also apply an explicit per-splat pixel bbox (pbox, x0 x1 y0 y1 half
@@ -171,13 +184,13 @@ __global__ void __launch_bounds__(kWarps * 32)
       // exponents and validity of the whole strip first: a warp skips the
       // entry when none of its pixels is live and inside the maha <= 64 ellipse
       f2 e[NP];
+      strip_exps<NP>(s, e);
       bool valid[STRIP];
       bool any = false;
       int4 q = make_int4(0, 0, 0, 0);
       if (BB) q = __ldg(pbox + st.g[j]);
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
-        e[p] = fma2(kkpair(p), bc(s.quad), fma2(kpair(p), bc(s.lin), bc(s.q0)));
         valid[2 * p] = (lo2(T[p]) >= kTMin) && (lo2(e[p]) >= s.thr);
         valid[2 * p + 1] = (hi2(T[p]) >= kTMin) && (hi2(e[p]) >= s.thr);
         if (BB) {
@@ -367,13 +380,13 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
       const float cb = st.c[j];
       const StripQuad s = strip_quad(a, b, fx, fy0);
       f2 e[NP];
+      strip_exps<NP>(s, e);
       bool valid[STRIP];
       bool any = false;
       int4 q = make_int4(0, 0, 0, 0);
       if (BB) q = __ldg(pbox + st.g[j]);
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
-        e[p] = fma2(kkpair(p), bc(s.quad), fma2(kpair(p), bc(s.lin), bc(s.q0)));
         valid[2 * p] = (pos < last[2 * p]) && (lo2(e[p]) >= s.thr);
         valid[2 * p + 1] = (pos < last[2 * p + 1]) && (hi2(e[p]) >= s.thr);
         if (BB) {
@@ -387,7 +400,7 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
         if (DET && slot_ok) det.partial[(s_epos[warp][j] * WPT + sub) * 9 + slot] = 0.f;
         continue;
       }
-      f2 nsc0, nsc1, nsc2, st0, st1, st2;
+      f2 nsc0, nsc1, nsc2, tp[NP];
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         // branch-free: an invalid pixel has alpha' = 0 (T and Q unchanged)
@@ -395,8 +408,9 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
         const float gl = ex2(lo2(e[p])), gh = ex2(hi2(e[p]));
         const bool vl = valid[2 * p], vh = valid[2 * p + 1];
         const f2 nap = pk2(vl ? fmaxf(-gl, -kAlphaMax) : 0.f, vh ? fmaxf(-gh, -kAlphaMax) : 0.f);
-        // clamped splats pass no alpha/footprint gradient (_kernels.py:120-121)
-        const f2 g = pk2((vl && gl <= kAlphaMax) ? gl : 0.f, (vh && gh <= kAlphaMax) ? gh : 0.f);
+        // clamped splats pass no alpha/footprint gradient (_kernels.py:120-121);
+        // -nap is alpha' = alpha G for a valid unclamped pixel and 0 when invalid
+        const f2 g = pk2(gl <= kAlphaMax ? -lo2(nap) : 0.f, gh <= kAlphaMax ? -hi2(nap) : 0.f);
         const f2 om = add2(bc(1.f), nap);  // 1 - alpha'
         const f2 inv = pk2(rcp(lo2(om)), rcp(hi2(om)));
         const f2 Ta = T[p];
@@ -405,29 +419,33 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
         const f2 dc = fma2(d2[p], bc(cb), fma2(d1[p], bc(b.w), mul2(d0[p], bc(b.z))));
         const f2 dap = mul2(inv, fma2(Ta, dc, nQ[p]));  // T dc - Q / (1 - alpha')
         fma2_acc(nQ[p], nw, dc);
-        const f2 t = mul2(g, dap);
+        tp[p] = mul2(g, dap);
         if (p == 0) {
           nsc0 = mul2(d0[p], nw);
           nsc1 = mul2(d1[p], nw);
           nsc2 = mul2(d2[p], nw);
-          st0 = t;
-          st1 = mul2(kpair(0), t);
-          st2 = mul2(kkpair(0), t);
         } else {
           nsc0 = fma2(d0[p], nw, nsc0);
           nsc1 = fma2(d1[p], nw, nsc1);
           nsc2 = fma2(d2[p], nw, nsc2);
-          st0 = add2(st0, t);
-          st1 = fma2(kpair(p), t, st1);
-          st2 = fma2(kkpair(p), t, st2);
         }
+      }
+      // strip moments sum t, sum t k, sum t k^2 with immediate k, k^2
+      f2 st0 = tp[0];
+#pragma unroll
+      for (int p = 1; p < NP; ++p) st0 = add2(st0, tp[p]);
+      float s_tk = hi2(tp[0]), s_tkk = hi2(tp[0]);
+#pragma unroll
+      for (int k = 2; k < STRIP; ++k) {
+        const float tk = (k & 1) ? hi2(tp[k >> 1]) : lo2(tp[k >> 1]);
+        s_tk = fmaf((float)k, tk, s_tk);
+        s_tkk = fmaf((float)(k * k), tk, s_tkk);
       }
       // strip sums -> the 9 basis sums of the footprint gradient (with
       // dy = dy0 + k):  t dx, t dy, t dx^2, t dx dy, t dy^2, t, colour.  The
       // per-splat constants (the conic, 1/alpha) are applied once per splat
       // in ss_project_bwd, so only lane-dependent factors are formed here.
-      const float s_t = lo2(st0) + hi2(st0), s_tk = lo2(st1) + hi2(st1),
-                  s_tkk = lo2(st2) + hi2(st2);
+      const float s_t = lo2(st0) + hi2(st0);
       const float dx = s.dx, dy0 = s.dy0;
       const float s_dy = fmaf(dy0, s_t, s_tk);                               // sum t dy
       const float s_dyy = fmaf(dy0, fmaf(dy0, s_t, s_tk + s_tk), s_tkk);     // sum t dy^2
