@@ -8,17 +8,30 @@
 // meanwhile); if K exceeds the caller's pair capacity it returns
 // SS_ERR_CAPACITY with K in v->n_pairs and the caller grows the buffers and
 // calls again.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+
 #include "ss_common.cuh"
 
 using namespace ss;
 
-// out[0] += sum of v[0..n) (int32; out zeroed by the caller): grid-stride,
-// one atomic per CTA.
+// K = sum of v[0..n) (int32), grid-stride.  Every CTA parks its partial in
+// partial[block]; the last CTA to finish (done counter) adds the partials in
+// block order (deterministic), writes the total to out and, with a
+// system-scope store, to the host-mapped pinned word the host is polling, and
+// re-arms the counter.  No copy-engine node and no zero fill in the stream.
+constexpr int kSumBlocks = 296;
+
 __global__ void __launch_bounds__(256) sum_kernel(const int32_t* __restrict__ v, int32_t n,
-                                                  int32_t* __restrict__ out) {
+                                                  int32_t* __restrict__ out,
+                                                  int32_t* __restrict__ host_out,
+                                                  int32_t* __restrict__ partial,
+                                                  unsigned int* __restrict__ done) {
   pdl_wait();
   pdl_trigger();
   __shared__ int32_t s_part[8];
+  __shared__ bool s_last;
   int32_t acc = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     acc += v[i];
@@ -28,7 +41,24 @@ __global__ void __launch_bounds__(256) sum_kernel(const int32_t* __restrict__ v,
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < 8; ++w) acc += s_part[w];
-    atomicAdd(out, acc);
+    partial[blockIdx.x] = acc;
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x < 32) {
+    __threadfence();
+    int32_t t = 0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) t += ((volatile int32_t*)partial)[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) {
+      *out = t;
+      *done = 0u;  // re-armed before the host can see K and launch the next view
+      __threadfence();
+      *(volatile int32_t*)host_out = t;
+      __threadfence_system();
+    }
   }
 }
 
@@ -87,29 +117,47 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   // per host thread and device (views may render from several threads, e.g.
   // a trainer and a player; an event belongs to the device it was made on)
   constexpr int kMaxDev = 64;
-  thread_local int32_t* k_pinned_tab[kMaxDev] = {};
-  thread_local cudaEvent_t k_event_tab[kMaxDev] = {};
+  struct KRead {
+    int32_t* host = nullptr;     // pinned, mapped: K lands here
+    int32_t* partial = nullptr;  // device: per-CTA partial sums
+    unsigned int* done = nullptr;
+  };
+  thread_local KRead k_tab[kMaxDev] = {};
   int devid = 0;
   if (cudaGetDevice(&devid) != cudaSuccess || devid < 0 || devid >= kMaxDev)
     return check_launch("ss_render_fwd: device");
-  int32_t*& k_pinned = k_pinned_tab[devid];
-  cudaEvent_t& k_event = k_event_tab[devid];
-  if (!k_pinned) {
-    if (cudaMallocHost(&k_pinned, sizeof(int32_t)) != cudaSuccess ||
-        cudaEventCreateWithFlags(&k_event, cudaEventDisableTiming) != cudaSuccess)
-      return check_launch("ss_render_fwd: pinned pair count");
+  KRead& kr = k_tab[devid];
+  if (!kr.host) {
+    if (cudaHostAlloc(&kr.host, sizeof(int32_t), cudaHostAllocMapped) != cudaSuccess ||
+        cudaMalloc(&kr.partial, kSumBlocks * sizeof(int32_t) + sizeof(unsigned int)) != cudaSuccess ||
+        cudaMemsetAsync(kr.partial, 0, kSumBlocks * sizeof(int32_t) + sizeof(unsigned int),
+                        stream) != cudaSuccess)
+      return check_launch("ss_render_fwd: pair count readback");
+    kr.done = reinterpret_cast<unsigned int*>(kr.partial + kSumBlocks);
   }
-  memzero(v->offsets + n, sizeof(int32_t), stream);
-  launch_k(sum_kernel, min(296, (n + 255) / 256), 256, 0, stream, v->n_tiles, n, v->offsets + n);
-  if (cudaMemcpyAsync(k_pinned, v->offsets + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream) !=
-          cudaSuccess ||
-      cudaEventRecord(k_event, stream) != cudaSuccess)
-    return check_launch("ss_render_fwd: pair count");
+  volatile int32_t* k_poll = kr.host;
+  *k_poll = -1;  // the previous view's K was consumed: re-arm
+  launch_k(sum_kernel, std::max(1, std::min(kSumBlocks, (n + 255) / 256)), 256, 0, stream,
+           (const int32_t*)v->n_tiles, n, v->offsets + n, kr.host, kr.partial, kr.done);
   if ((rc = ss_depth_order(v->depth_key, n, v->order, v->ws, v->ws_bytes, stream))) return rc;
   if ((rc = ss_tile_offsets(v->order, v->n_tiles, n, v->offsets, v->ws, v->ws_bytes, stream)))
     return rc;
-  if (cudaEventSynchronize(k_event) != cudaSuccess) return check_launch("ss_render_fwd: pair count");
-  const int32_t k_host = *k_pinned;
+  // the host polls the mapped word (no event or copy node in the stream);
+  // after 2 s of polling it falls back to draining the stream
+  int32_t k_host = *k_poll;
+  if (k_host < 0) {
+    const auto t0 = std::chrono::steady_clock::now();
+    while ((k_host = *k_poll) < 0) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+        if (cudaStreamSynchronize(stream) != cudaSuccess)
+          return check_launch("ss_render_fwd: pair count");
+        if ((k_host = *k_poll) < 0)
+          return set_error(SS_ERR_CUDA, "ss_render_fwd: pair count never arrived");
+        break;
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   v->n_pairs = k_host;
   if (k_host > v->pair_cap) return set_error(SS_ERR_CAPACITY, "ss_render_fwd: %d pairs > capacity", k_host);
   const int32_t* sv = v->vals;
