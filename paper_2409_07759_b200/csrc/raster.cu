@@ -37,9 +37,16 @@
 
 namespace ss {
 
-constexpr int kWarps = 4;  // warps per CTA
+#ifndef SS_RASTER_WARPS_FWD
+#define SS_RASTER_WARPS_FWD 8
+#endif
+#ifndef SS_RASTER_WARPS_BWD
+#define SS_RASTER_WARPS_BWD 4
+#endif
+constexpr int kWarps = SS_RASTER_WARPS_BWD;     // warps per CTA, backward
+constexpr int kWarpsF = SS_RASTER_WARPS_FWD;    // warps per CTA, forward
 #ifndef SS_BWD_MINB
-#define SS_BWD_MINB 8
+#define SS_BWD_MINB (32 / SS_RASTER_WARPS_BWD)  // 64 registers
 #endif
 constexpr float kKappa = -0.72134752044448170368f;  // -log2(e) / 2
 constexpr float kInvKappa = -1.38629436111989061883f;  // 1 / kappa = -2 ln 2
@@ -131,7 +138,7 @@ __device__ __forceinline__ void strip_exps(const StripQuad& s, f2 e[NP]) {
 // not enclose the maha <= 64 ellipse.  Off for the training path, where the
 // 8-sigma bbox is implied by the maha cut.
 template <int STRIP, bool BB = false>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarpsF * 32)
     raster_fwd_kernel(const int2* __restrict__ ranges, const int32_t* __restrict__ vals,
                       const float4* __restrict__ rec_a, const float4* __restrict__ rec_b,
                       const float* __restrict__ rec_c, int width, int height, int tiles_x,
@@ -140,11 +147,11 @@ __global__ void __launch_bounds__(kWarps * 32)
                       int32_t* __restrict__ n_contrib, const int4* __restrict__ pbox = nullptr) {
   pdl_wait();
   pdl_trigger();
-  __shared__ WarpStage s_stage[kWarps];
+  __shared__ WarpStage s_stage[kWarpsF];
   constexpr int WPT = kTile / (2 * STRIP);  // warps per tile
   constexpr int NP = STRIP / 2;             // pixel pairs per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gwarp = blockIdx.x * kWarps + warp;
+  const int gwarp = blockIdx.x * kWarpsF + warp;
   const int slot_id = gwarp / WPT, sub = gwarp % WPT;
   if (slot_id >= n_tiles) return;
   const int tile = tile_order ? tile_order[slot_id] : slot_id;
@@ -528,9 +535,9 @@ extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const v
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
   const int wpt = kTile / (2 * g_strip_fwd);
-  const int blocks = (n_tiles * wpt + kWarps - 1) / kWarps;
+  const int blocks = (n_tiles * wpt + kWarpsF - 1) / kWarpsF;
 #define SS_FWD(S)                                                                             \
-  launch_k(raster_fwd_kernel<S>, blocks, kWarps * 32, 0, stream,                                    \
+  launch_k(raster_fwd_kernel<S>, blocks, kWarpsF * 32, 0, stream,                                    \
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
       height, tiles_x, n_tiles, tile_order, img, t_final, n_contrib, nullptr)
   if (g_strip_fwd == 8) SS_FWD(8);
@@ -584,8 +591,8 @@ int raster_fwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_
                     const int32_t* pbox, cudaStream_t stream) {
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
-  const int blocks = (n_tiles * 2 + kWarps - 1) / kWarps;
-  launch_k(raster_fwd_kernel<4, true>, blocks, kWarps * 32, 0, stream, 
+  const int blocks = (n_tiles * 2 + kWarpsF - 1) / kWarpsF;
+  launch_k(raster_fwd_kernel<4, true>, blocks, kWarpsF * 32, 0, stream, 
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
       tiles_x, n_tiles, tile_order, img, t_final, n_contrib, (const int4*)pbox);
   return check_launch("raster_fwd_bbox");
