@@ -34,6 +34,13 @@ def test_binding_covers_header():
     assert set(declared()) <= set(_lib.exported_symbols())
 
 
+def test_integration_doc_covers_header():
+    """INTEGRATION.md names every C entry point the header declares."""
+    doc = (ROOT / "INTEGRATION.md").read_text()
+    missing = [n for n in declared() if n not in doc]
+    assert not missing, missing
+
+
 def test_error_reporting_without_gpu():
     """Argument validation happens before any device work."""
     from paper_2409_07759_b200 import _lib
