@@ -82,6 +82,21 @@ def load_issue(kernels):
         return None
 
 
+def load_ncu_throughput(kernels):
+    """SM / L2 / L1 throughput (percent of B200 peak), L2 hit rate and
+    occupancy of the given kernels from the committed ncu capture."""
+    files = sorted((ROOT / "profiles").glob("r*_traffic.json"))
+    if not files:
+        return None
+    d = json.loads(files[-1].read_text())
+    keys = ("sm_throughput_pct", "l2_throughput_pct", "l1_throughput_pct", "l2_hit_rate_pct",
+            "occupancy_pct")
+    try:
+        return {k: {q: d[k].get(q) for q in keys} for k in kernels}
+    except KeyError:
+        return None
+
+
 def load_peaks():
     if PEAKS.exists():
         d = json.loads(PEAKS.read_text())
@@ -840,6 +855,7 @@ def main():
                        "frac": achieved / peak,
                        "traffic": load_traffic(["raster_fwd", "raster_bwd"]),
                        "issue_active_pct": load_issue(["raster_fwd", "raster_bwd"]),
+                       "ncu_throughput": load_ncu_throughput(["raster_fwd", "raster_bwd"]),
                        "issue_note": "ncu smsp__issue_active (profiles/r*_traffic.json): the "
                                      "raster kernels are issue-bound; HBM frac is low by design",
                        "traffic_source": "ncu --set full dram__bytes_read+write per launch "

@@ -28,7 +28,12 @@ PIPES = ["smsp__issue_active.avg.pct_of_peak_sustained_active",
          "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
          "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
          "smsp__inst_executed.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-         "gpu__time_duration.sum"]
+         "gpu__time_duration.sum",
+         "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+         "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+         "l1tex__throughput.avg.pct_of_peak_sustained_active",
+         "lts__t_sector_hit_rate.pct",
+         "sm__warps_active.avg.pct_of_peak_sustained_active"]
 
 
 def raw_metrics(rep):
@@ -68,7 +73,12 @@ def main():
                    "dram_bytes_write": v["dram__bytes_write.sum"],
                    "duration_us": v["gpu__time_duration.sum"],
                    "issue_active_pct": v["smsp__issue_active.avg.pct_of_peak_sustained_active"],
-                   "warp_instructions": v["smsp__inst_executed.sum"]}
+                   "warp_instructions": v["smsp__inst_executed.sum"],
+                   "sm_throughput_pct": v.get("sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+                   "l2_throughput_pct": v.get("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                   "l1_throughput_pct": v.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                   "l2_hit_rate_pct": v.get("lts__t_sector_hit_rate.pct"),
+                   "occupancy_pct": v.get("sm__warps_active.avg.pct_of_peak_sustained_active")}
                for k, v in (("raster_fwd", f), ("raster_bwd", b))}
     traffic["source"] = (f"ncu --set full --clock-control none, config 3 (bench.py --profile-steps 1), "
                          f"round {a.round[1:]}; bytes converted from the raw page's units")
@@ -77,6 +87,11 @@ def main():
     def row(name, v):
         return (f"| {name} | {v[PIPES[0]]:.0f} | {v[PIPES[1]]:.0f} | {v[PIPES[2]]:.0f} | "
                 f"{v[PIPES[3]]:.0f} | {v[PIPES[4]]:.0f} | {v[PIPES[5]] / 1e6:.0f} M |")
+
+    def row2(name, v):
+        g = lambda k: v.get(k, float("nan"))  # noqa: E731
+        return (f"| {name} | {g(PIPES[9]):.0f} | {g(PIPES[10]):.0f} | {g(PIPES[11]):.0f} | "
+                f"{g(PIPES[12]):.0f} | {g(PIPES[13]):.0f} |")
 
     reports = "\n".join(ncu_summary.report(r) for r in [a.raster] + a.extra)
     md = f"""# Round {a.round[1:]} — config 3 profile (DyNeRF-shaped, 300k splats, 1352x1014, B200)
@@ -108,6 +123,15 @@ of active cycles.  Pipe shares (percent of peak, active cycles):
 |---|---|---|---|---|---|---|
 {row("raster_fwd", f)}
 {row("raster_bwd", b)}
+
+Throughput against B200 peak (ncu, percent): SM is busy, the memory
+hierarchy is not -- L2 a few %, DRAM ~1 % (the tile lists' 36-B records are
+re-read from L1/L2, hit rate below).
+
+| kernel | SM throughput | L2 throughput | L1 throughput | L2 hit rate | achieved occupancy |
+|---|---|---|---|---|---|
+{row2("raster_fwd", f)}
+{row2("raster_bwd", b)}
 
 {reports}
 """
