@@ -433,3 +433,48 @@ def test_large_frame_uses_pair_sort_fallback(ss):
     ref = O.blend_forward_tiled(cache, cam.height, cam.width, nthreads=8, bins=bins)
     img = R.render_arrays(cam, arr).pixels
     assert np.abs(img - ref["image"]).max() <= IMG_TOL
+
+
+def test_concurrent_views_from_two_threads(ss):
+    """Two host threads (a trainer and a player, say), each with its own
+    pipeline and stream, render different views at the same time: each view's
+    pair count K arrives through its thread's own mapped word, so images equal
+    the single-threaded renders bit for bit."""
+    import threading
+
+    import torch
+
+    from paper_2409_07759_b200.engine import Store, ViewPipeline, device
+
+    P, R = ss
+    arr = _synth_scene(P, 20_000, 0.03, seed=5)
+    rows = torch.from_numpy(arr.rows()).to(device())
+    store = Store(opt=None, mat=rows)
+    cams = [cam_from(P, arc_camera(i, 8, 320, 240)) for i in range(4)]
+    ref = [ViewPipeline().forward(store, None, len(arr), c).clone() for c in cams]
+    torch.cuda.synchronize()
+    out = [[None] * 4 for _ in range(2)]
+    errors = []
+
+    def worker(t):
+        try:
+            pipe = ViewPipeline()
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(5):
+                    for i, c in enumerate(cams[t::2]):
+                        img = pipe.forward(store, None, len(arr), c, stream=s)
+                        out[t][2 * i + t] = img.clone()
+            s.synchronize()
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=worker, args=(t,)) for t in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=120)
+    assert not errors, errors
+    for t in range(2):
+        for i in range(t, 4, 2):
+            assert torch.equal(out[t][i], ref[i]), (t, i)
