@@ -25,7 +25,8 @@ constexpr int kSumBlocks = 296;
 
 __global__ void __launch_bounds__(256) sum_kernel(const int32_t* __restrict__ v, int32_t n,
                                                   int32_t* __restrict__ out,
-                                                  int32_t* __restrict__ host_out,
+                                                  unsigned long long* __restrict__ host_out,
+                                                  uint32_t seq,
                                                   int32_t* __restrict__ partial,
                                                   unsigned int* __restrict__ done) {
   pdl_wait();
@@ -56,7 +57,9 @@ __global__ void __launch_bounds__(256) sum_kernel(const int32_t* __restrict__ v,
       *out = t;
       *done = 0u;  // re-armed before the host can see K and launch the next view
       __threadfence();
-      *(volatile int32_t*)host_out = t;
+      // one 8-byte store: (view sequence number, K) arrive together
+      *(volatile unsigned long long*)host_out =
+          ((unsigned long long)seq << 32) | (unsigned long long)(uint32_t)t;
       __threadfence_system();
     }
   }
@@ -115,10 +118,11 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   // it (to size the binning) while the GPU runs the depth sort and offsets.
   // It is parked in offsets[n], which ss_tile_offsets rewrites with K.
   // per host thread and device (views may render from several threads, e.g.
-  // a trainer and a player; an event belongs to the device it was made on)
+  // a trainer and a player; the partials and counter live on the device)
   constexpr int kMaxDev = 64;
   struct KRead {
-    int32_t* host = nullptr;     // pinned, mapped: K lands here
+    unsigned long long* host = nullptr;  // pinned, mapped: (seq, K) lands here
+    uint32_t seq = 0;                    // views issued by this thread on this device
     int32_t* partial = nullptr;  // device: per-CTA partial sums
     unsigned int* done = nullptr;
   };
@@ -128,36 +132,42 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
     return check_launch("ss_render_fwd: device");
   KRead& kr = k_tab[devid];
   if (!kr.host) {
-    if (cudaHostAlloc(&kr.host, sizeof(int32_t), cudaHostAllocMapped) != cudaSuccess ||
+    if (cudaHostAlloc(&kr.host, sizeof(unsigned long long), cudaHostAllocMapped) != cudaSuccess ||
         cudaMalloc(&kr.partial, kSumBlocks * sizeof(int32_t) + sizeof(unsigned int)) != cudaSuccess ||
         cudaMemsetAsync(kr.partial, 0, kSumBlocks * sizeof(int32_t) + sizeof(unsigned int),
                         stream) != cudaSuccess)
       return check_launch("ss_render_fwd: pair count readback");
     kr.done = reinterpret_cast<unsigned int*>(kr.partial + kSumBlocks);
+    *(volatile unsigned long long*)kr.host = 0ull;  // no view has sequence number 0
   }
-  volatile int32_t* k_poll = kr.host;
-  *k_poll = -1;  // the previous view's K was consumed: re-arm
+  // the word carries the view's sequence number, so a late write from an
+  // earlier (abandoned) view can never be taken for this view's K
+  volatile unsigned long long* k_poll = kr.host;
+  const uint32_t seq = ++kr.seq;
   launch_k(sum_kernel, std::max(1, std::min(kSumBlocks, (n + 255) / 256)), 256, 0, stream,
-           (const int32_t*)v->n_tiles, n, v->offsets + n, kr.host, kr.partial, kr.done);
+           (const int32_t*)v->n_tiles, n, v->offsets + n, kr.host, seq, kr.partial, kr.done);
   if ((rc = ss_depth_order(v->depth_key, n, v->order, v->ws, v->ws_bytes, stream))) return rc;
   if ((rc = ss_tile_offsets(v->order, v->n_tiles, n, v->offsets, v->ws, v->ws_bytes, stream)))
     return rc;
   // the host polls the mapped word (no event or copy node in the stream);
   // after 2 s of polling it falls back to draining the stream
-  int32_t k_host = *k_poll;
-  if (k_host < 0) {
+  const auto arrived = [&]() { return (uint32_t)(*k_poll >> 32) == seq; };
+  if (!arrived()) {
     const auto t0 = std::chrono::steady_clock::now();
-    while ((k_host = *k_poll) < 0) {
+    while (!arrived()) {
+#if defined(__x86_64__) || defined(__i386__)
+      __builtin_ia32_pause();  // spin politely (SMT sibling, power)
+#endif
       if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
         if (cudaStreamSynchronize(stream) != cudaSuccess)
           return check_launch("ss_render_fwd: pair count");
-        if ((k_host = *k_poll) < 0)
-          return set_error(SS_ERR_CUDA, "ss_render_fwd: pair count never arrived");
+        if (!arrived()) return set_error(SS_ERR_CUDA, "ss_render_fwd: pair count never arrived");
         break;
       }
     }
   }
   std::atomic_thread_fence(std::memory_order_acquire);
+  const int32_t k_host = (int32_t)(uint32_t)*k_poll;
   v->n_pairs = k_host;
   if (k_host > v->pair_cap) return set_error(SS_ERR_CAPACITY, "ss_render_fwd: %d pairs > capacity", k_host);
   const int32_t* sv = v->vals;
