@@ -361,6 +361,19 @@ int ss_to_direct(const double* src, double* dst, int64_t n, ss_stream_t stream);
  * rounding (raster.py:411-425), evaluated in fp64. */
 int ss_to_srgb_u8(const float* img, int64_t n, uint8_t* out, ss_stream_t stream);
 
+/* ---- ABR tail-drop selection (server.py:39-79).
+ * src holds n keys of `kind` at byte `offset` of `stride`-byte records
+ * (wire records: SS_ABR_F32 opacity at 40 / 56 B for profile 0, SS_ABR_U8 at
+ * 16 / 30 B for profile 1; SS_ABR_F64 with stride 8 for an opacity array).
+ * Writes the ascending indices of the kept_n highest keys, ties to the lower
+ * index (the reference's stable argsort of -opacity), to keep_idx[kept_n]
+ * and, when out != NULL, those records' stride bytes in the same order. */
+#define SS_ABR_F32 0
+#define SS_ABR_U8 1
+#define SS_ABR_F64 2
+int ss_abr_select(const void* src, int64_t n, int32_t kind, int32_t stride, int32_t offset,
+                  int64_t kept_n, int32_t* keep_idx, uint8_t* out, ss_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

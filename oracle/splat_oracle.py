@@ -676,3 +676,40 @@ def tile_keep_mask(cache, owner, tx, ty, tile=TILE):
     ax = np.maximum(tx * tile, x0[owner]).astype(_F) - uf
     bx = np.minimum(tx * tile + tile - 1, x1[owner] - 1).astype(_F) - uf
     return meets & (ax <= R) & (bx >= L)
+
+
+# ---------------------------------------------------------------------------
+# §8(f)-4 ABR tail-drop selection (server.py:39-79)
+
+ABR_OPACITY = {0: ("<f4", 40, 56), 1: ("u1", 16, 30)}  # profile -> (dtype, byte offset, record size)
+SLICE_HEADER = 16                                      # codec.py HEADER_SIZE
+
+
+def abr_keep_indices(opacities, fraction):
+    """server.py:39-50: ascending indices of the ceil(fraction n) highest
+    opacities, ties to the lower index (stable argsort of -opacity)."""
+    if not (0.0 < fraction <= 1.0):
+        raise ValueError(f"fraction {fraction} outside (0, 1]")
+    n = len(opacities)
+    kept_n = int(math.ceil(fraction * n))
+    if kept_n >= n:
+        return np.arange(n)
+    ranked = np.argsort(-np.asarray(opacities, dtype=np.float64), kind="stable")
+    return np.sort(ranked[:kept_n])
+
+
+def subsample_records(payload, profile_id, fraction):
+    """server.py:59-79 on the record bytes of one slice: (kept record bytes,
+    kept count).  Opacity is read at the profile's field offset (f32, or u8
+    / 255 for profile 1, as the reference's astype(float64) / 255)."""
+    dt, off, size = ABR_OPACITY[profile_id]
+    payload = np.frombuffer(bytes(payload), dtype=np.uint8)
+    n = len(payload) // size
+    rec = payload.reshape(n, size)
+    opac = np.frombuffer(rec[:, off:off + np.dtype(dt).itemsize].tobytes(), dtype=dt).astype(np.float64)
+    if profile_id == 1:
+        opac = opac / 255.0
+    if fraction >= 1.0:
+        return payload.tobytes(), n
+    keep = abr_keep_indices(opac, fraction)
+    return rec[keep].tobytes(), len(keep)

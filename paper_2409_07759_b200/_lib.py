@@ -18,6 +18,7 @@ SS_ROW = 14
 SS_GRAD_ROW = 14
 SS_G2D_ROW = 12
 SS_TILE = 16
+SS_ABR_F32, SS_ABR_U8, SS_ABR_F64 = 0, 1, 2
 
 
 class SSCamera(Structure):
@@ -114,6 +115,7 @@ _SIGNATURES = {
     "ss_event_elapsed_ms": ([P, P, POINTER(ctypes.c_float)], c_int),
     "ss_encode_records": ([P, I64, I32, P, P, P], c_int),
     "ss_decode_records": ([P, I64, I32, P, P], c_int),
+    "ss_abr_select": ([P, I64, I32, I32, I32, I64, P, P, P], c_int),
 }
 
 _LIB = None

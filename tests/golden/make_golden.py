@@ -342,6 +342,38 @@ def make_codec(ref):
     print("codec: ok")
 
 
+def make_abr(ref):
+    """ABR tail-drop selection (reference server.py:39-79): abr_keep_indices on
+    fp64 opacities with ties, and subsample_slice_bytes on wire slices of both
+    profiles (u8 opacities tie heavily), at several quality fractions."""
+    C = sys.modules["ref_splatstream.codec"]
+    S = sys.modules["ref_splatstream.server"]
+    rng = np.random.default_rng(41)
+    out = {}
+    fractions = np.array([0.013, 0.1, 0.37, 0.5, 0.77, 0.999, 1.0])
+    out["fractions"] = fractions
+    opac = rng.uniform(0, 1, 1001)
+    opac[::7] = 0.25                      # a large tie class
+    opac[5:40:3] = opac[4]                # ties at high opacity
+    opac[100:110] = 0.0
+    out["opac"] = opac
+    for i, q in enumerate(fractions):
+        out[f"keep_{i}"] = S.abr_keep_indices(opac, float(q)).astype(np.int64)
+    n = 613
+    arr = random_arrays(ref, rng, n, opacity_lo=0.0, opacity_hi=1.0)
+    arr.opacities[::5] = 0.5
+    arr.opacities[1:60:4] = arr.opacities[0]
+    for pid in (0, 1):
+        prof = C.PROFILES[pid]
+        blob = C.pack_slice(arr, ref.core.Lifespan(9, 9, 14), prof, swin_size=5)
+        out[f"slice_p{pid}"] = np.frombuffer(blob, dtype=np.uint8)
+        for i, q in enumerate(fractions):
+            out[f"sub_p{pid}_{i}"] = np.frombuffer(S.subsample_slice_bytes(blob, float(q), prof),
+                                                   dtype=np.uint8)
+    np.savez_compressed(OUT / "abr.npz", **out)
+    print("abr: ok")
+
+
 def main():
     ref = load_reference()
     import ref_splatstream.synth  # noqa: F401
@@ -352,6 +384,8 @@ def main():
     make_golden_render(ref)
     import ref_splatstream.codec  # noqa: F401
     make_codec(ref)
+    import ref_splatstream.server  # noqa: F401
+    make_abr(ref)
 
 
 if __name__ == "__main__":

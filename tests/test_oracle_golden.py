@@ -159,3 +159,18 @@ def test_srgb_lut_roundtrip():
     lin = O.linear_from_u8(u8)
     assert np.array_equal(O.u8_from_linear(lin), u8)
     assert lin[0] == 0.0 and lin[255] == 1.0 and np.all(np.diff(lin) > 0)
+
+
+def test_abr_selection_matches_reference():
+    """§8(f)-4: the oracle's abr_keep_indices / wire-level tail drop against
+    the reference's own outputs (server.py:39-79, tests/golden/abr.npz)."""
+    d = load_golden("abr")
+    for i, q in enumerate(d["fractions"]):
+        assert np.array_equal(O.abr_keep_indices(d["opac"], float(q)), d[f"keep_{i}"])
+    for pid in (0, 1):
+        blob = d[f"slice_p{pid}"].tobytes()
+        for i, q in enumerate(d["fractions"]):
+            sub = d[f"sub_p{pid}_{i}"].tobytes()
+            body, kept = O.subsample_records(blob[O.SLICE_HEADER:], pid, float(q))
+            assert body == sub[O.SLICE_HEADER:]
+            assert len(body) == kept * O.ABR_OPACITY[pid][2]
