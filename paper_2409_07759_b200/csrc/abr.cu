@@ -26,20 +26,35 @@ __device__ __forceinline__ uint64_t abr_key(const uint8_t* src, int64_t i, int k
   const uint8_t* p = src + i * stride + offset;
   if (kind == SS_ABR_U8) return (uint64_t)*p;
   if (kind == SS_ABR_F32) {
-    uint32_t u;
-    memcpy(&u, p, 4);
+    uint32_t u = *reinterpret_cast<const uint32_t*>(p);  // 4-aligned (checked on the host)
     if ((u & 0x7fffffffu) == 0u) u = 0u;
     return (uint64_t)((u & 0x80000000u) ? ~u : (u | 0x80000000u));
   }
-  uint64_t u;
-  memcpy(&u, p, 8);
+  uint64_t u = *reinterpret_cast<const uint64_t*>(p);  // 8-aligned (checked on the host)
   if ((u & 0x7fffffffffffffffull) == 0ull) u = 0ull;
   return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
 }
 
+// One record's bytes in the widest words both ends' alignment allows.
+__device__ __forceinline__ void copy_record(uint8_t* dst, const uint8_t* src, int stride,
+                                            int word) {
+  if (word == 8) {
+    for (int b = 0; b < stride; b += 8)
+      *reinterpret_cast<uint64_t*>(dst + b) = *reinterpret_cast<const uint64_t*>(src + b);
+  } else if (word == 4) {
+    for (int b = 0; b < stride; b += 4)
+      *reinterpret_cast<uint32_t*>(dst + b) = *reinterpret_cast<const uint32_t*>(src + b);
+  } else if (word == 2) {
+    for (int b = 0; b < stride; b += 2)
+      *reinterpret_cast<uint16_t*>(dst + b) = *reinterpret_cast<const uint16_t*>(src + b);
+  } else {
+    for (int b = 0; b < stride; ++b) dst[b] = src[b];
+  }
+}
+
 __global__ void __launch_bounds__(kAbrThreads) abr_select_kernel(
     const uint8_t* __restrict__ src, int64_t n, int kind, int stride, int offset, int64_t kept_n,
-    int32_t* __restrict__ keep_idx, uint8_t* __restrict__ out) {
+    int32_t* __restrict__ keep_idx, uint8_t* __restrict__ out, int word) {
   pdl_wait();
   pdl_trigger();
   using Scan = cub::BlockScan<int, kAbrThreads>;
@@ -96,8 +111,7 @@ __global__ void __launch_bounds__(kAbrThreads) abr_select_kernel(
     if (keep) {
       const int64_t o = kept_before + pos;
       keep_idx[o] = (int32_t)i;
-      if (out)
-        for (int b = 0; b < stride; ++b) out[o * stride + b] = src[i * stride + b];
+      if (out) copy_record(out + o * stride, src + i * stride, stride, word);
     }
     eq_before += eq_total;
     kept_before += kept_total;
@@ -114,10 +128,15 @@ extern "C" int ss_abr_select(const void* src, int64_t n, int32_t kind, int32_t s
   const int key_bytes = kind == SS_ABR_U8 ? 1 : (kind == SS_ABR_F32 ? 4 : 8);
   if (n < 0 || n > 0x7fffffffll || kept_n < 0 || kept_n > n || !src ||
       (kind != SS_ABR_U8 && kind != SS_ABR_F32 && kind != SS_ABR_F64) || offset < 0 ||
-      stride < offset + key_bytes || (kept_n > 0 && !keep_idx))
+      stride < offset + key_bytes || (kept_n > 0 && !keep_idx) ||
+      (offset % key_bytes) || (stride % key_bytes) || ((uintptr_t)src % key_bytes))
     return set_error(SS_ERR_INVALID, "ss_abr_select: bad arguments");
   if (n == 0 || kept_n == 0) return SS_OK;
+  // copy width: the largest of 8 / 4 / 2 / 1 dividing the stride and both base addresses
+  int word = 8;
+  while (word > 1 && ((stride % word) || ((uintptr_t)src % word) || (out && (uintptr_t)out % word)))
+    word >>= 1;
   launch_k(abr_select_kernel, 1, kAbrThreads, 0, stream, (const uint8_t*)src, n, (int)kind,
-           (int)stride, (int)offset, kept_n, keep_idx, out);
+           (int)stride, (int)offset, kept_n, keep_idx, out, word);
   return check_launch("ss_abr_select");
 }
