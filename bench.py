@@ -544,6 +544,13 @@ def run_render_only(args, dp):
             buf.render_device(cams[(start + i * world + rank) % len(cams)], 0)
 
     frames(args.warmup)
+    if args.profile_steps:
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        frames(args.profile_steps)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        return {"profiled_frames": args.profile_steps}
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clocks:
         if dp is not None:
             dp.barrier()

@@ -77,8 +77,13 @@ __global__ void depth_hist_kernel(const uint64_t* __restrict__ key64, int32_t n,
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  atomicAdd(&hist[depth_bucket(key64[i], ~range[0], range[1], nb)], 1);
+  const uint64_t k = i < n ? key64[i] : 0ull;
+  // culled keys all land in bucket nb: one atomic per warp for them (off-view
+  // splats are most of a novel view's store), one per key otherwise
+  const bool culled = i < n && k == ~0ull;
+  const uint32_t cm = __ballot_sync(0xffffffffu, culled);
+  if (culled && (threadIdx.x & 31) == __ffs(cm) - 1) atomicAdd(&hist[nb], __popc(cm));
+  if (i < n && !culled) atomicAdd(&hist[depth_bucket(k, ~range[0], range[1], nb)], 1);
 }
 
 __global__ void depth_scatter_kernel(const uint64_t* __restrict__ key64, int32_t n,
@@ -88,9 +93,18 @@ __global__ void depth_scatter_kernel(const uint64_t* __restrict__ key64, int32_t
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t k = i < n ? key64[i] : 0ull;
+  const bool culled = i < n && k == ~0ull;
+  // culled keys: one warp-aggregated atomic on bucket nb (their order inside
+  // the trailing culled run is free)
+  const uint32_t cm = __ballot_sync(0xffffffffu, culled);
+  int32_t cbase = 0;
+  const int lane = threadIdx.x & 31;
+  if (cm && lane == __ffs(cm) - 1) cbase = atomicAdd(&cursor[nb], __popc(cm));
+  cbase = __shfl_sync(0xffffffffu, cbase, cm ? __ffs(cm) - 1 : 0);
   if (i >= n) return;
-  const uint32_t b = depth_bucket(key64[i], ~range[0], range[1], nb);
-  const int32_t pos = atomicAdd(&cursor[b], 1);
+  const uint32_t b = culled ? nb : depth_bucket(k, ~range[0], range[1], nb);
+  const int32_t pos = culled ? cbase + __popc(cm & ((1u << lane) - 1u)) : atomicAdd(&cursor[b], 1);
   order[pos] = i;
   bucket_of[pos] = b;
 }
@@ -836,8 +850,13 @@ extern "C" int ss_set_binning(int32_t mode) {
 extern "C" int ss_get_binning(void) { return g_binning; }
 
 // Chunks: a whole number of scatter waves (resident CTAs on 148 SMs), each
-// chunk at most ~16k pairs (bounds balance them by pairs), at most 4096.
-constexpr int kBinPairsPerChunk = 16384;
+// chunk at most ~32k pairs (bounds balance them by pairs), at most 4096.  At
+// large K (config 5: 1M splats, 1920x1080) fewer, longer chunks keep the
+// (chunks x tiles) histogram small: 32k measured best (16k / 64k slower).
+#ifndef SS_BIN_PAIRS_PER_CHUNK
+#define SS_BIN_PAIRS_PER_CHUNK 32768
+#endif
+constexpr int kBinPairsPerChunk = SS_BIN_PAIRS_PER_CHUNK;
 constexpr int kBinChunksCap = 4096;
 constexpr int kBinMaxTiles = 18 * 1024;  // 12 bytes of shared memory per tile in the scatter
 
