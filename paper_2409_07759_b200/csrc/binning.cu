@@ -622,13 +622,25 @@ __global__ void __launch_bounds__(kBinThreads) bin_col_scan_kernel(int32_t* __re
 }
 
 // One CTA: exclusive scan of the tile totals -> start[t], ranges[t].
+constexpr int kOrderMax = 1 << 20;
+constexpr int kBuckets = 128;
+
+__device__ __forceinline__ int len_bucket(int len) {
+  // 4 * log2(len + 1) without a log: exponent and the top two mantissa bits
+  const float f = (float)(len + 1);
+  const int b = ((__float_as_int(f) >> 21) - (127 << 2));  // 4 * floor-ish(log2)
+  return kBuckets - 1 - min(max(b, 0), kBuckets - 1);
+}
+
 __global__ void __launch_bounds__(1024) bin_tile_scan_kernel(const int32_t* __restrict__ totals,
                                                              int32_t n_tiles,
                                                              int32_t* __restrict__ start,
-                                                             int2* __restrict__ ranges) {
+                                                             int2* __restrict__ ranges,
+                                                             int32_t* __restrict__ tile_order) {
   pdl_wait();
   pdl_trigger();
   __shared__ int32_t s_warp[32];
+  __shared__ int s_hist[kBuckets];
   extern __shared__ int32_t s_tot[];  // totals staged by coalesced loads
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_tot[t] = totals[t];
   __syncthreads();
@@ -662,11 +674,31 @@ __global__ void __launch_bounds__(1024) bin_tile_scan_kernel(const int32_t* __re
     run += c;
   }
   __syncthreads();
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) s_hist[i] = 0;
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
     const int32_t a = s_tot[t];
+    const int32_t len = totals[t];
     start[t] = a;
-    ranges[t] = make_int2(a, a + totals[t]);
+    ranges[t] = make_int2(a, a + len);
+    s_tot[t] = len;  // this thread's own entries only: no race with the scan reads above
   }
+  if (!tile_order) return;
+  // the raster launch order (ss_tile_order's counting sort by list-length
+  // bucket, longest first) from the totals already in shared memory
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&s_hist[len_bucket(s_tot[t])], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < kBuckets; ++b) {
+      const int c = s_hist[b];
+      s_hist[b] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
+    tile_order[atomicAdd(&s_hist[len_bucket(s_tot[t])], 1)] = t;
 }
 
 // Stable scatter of one chunk: waves of 256 pairs in emit order, one per
@@ -884,6 +916,17 @@ extern "C" int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const 
                             int64_t n_pairs, int32_t tiles_x, int32_t tiles_y, uint16_t* keys,
                             int32_t* vals, int32_t* vals_out, int32_t* ranges, void* ws,
                             size_t ws_bytes, cudaStream_t stream) {
+  return bin_tiles_with_order(order, offsets, bbox, geom, tile_mask, n, n_pairs, tiles_x, tiles_y,
+                              keys, vals, vals_out, ranges, nullptr, ws, ws_bytes, stream);
+}
+
+// ss_bin_tiles that also writes the raster launch order (ss_tile_order's
+// result) from its tile scan when tile_order != NULL.
+int bin_tiles_with_order(const int32_t* order, const int32_t* offsets, const int32_t* bbox,
+                         const float* geom, const uint64_t* tile_mask, int32_t n,
+                         int64_t n_pairs, int32_t tiles_x, int32_t tiles_y, uint16_t* keys,
+                         int32_t* vals, int32_t* vals_out, int32_t* ranges, int32_t* tile_order,
+                         void* ws, size_t ws_bytes, cudaStream_t stream) {
   const int n_tiles = tiles_x * tiles_y;
   if (n < 0 || tiles_x <= 0 || tiles_y <= 0 || n_pairs < 0)
     return set_error(SS_ERR_INVALID, "ss_bin_tiles: bad sizes");
@@ -920,7 +963,8 @@ extern "C" int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const 
                                                     tile_mask, bounds, n_tiles, tiles_x, keys,
                                                     vals, counts);
   launch_k(bin_col_scan_kernel, (n_tiles + 31) / 32, kBinThreads, 0, stream, counts, C, n_tiles, totals);
-  launch_k(bin_tile_scan_kernel, 1, 1024, (size_t)n_tiles * 4, stream, totals, n_tiles, start, (int2*)ranges);
+  launch_k(bin_tile_scan_kernel, 1, 1024, (size_t)n_tiles * 4, stream, totals, n_tiles, start,
+           (int2*)ranges, tile_order);
   launch_k(bin_scatter_kernel, C, kBinThreads, smem_scatter, stream, offsets, bounds, keys, vals,
                                                                n_tiles, counts, start, vals_out);
   return check_launch("ss_bin_tiles");
@@ -961,16 +1005,6 @@ extern "C" int ss_tile_ranges(const uint32_t* sorted_keys, int64_t n_pairs, int3
 // length bucket (4 buckets per octave, longest first).  Only the launch
 // order depends on it (each tile's work is independent), so ties within a
 // bucket need no fixed order.
-constexpr int kOrderMax = 1 << 20;
-constexpr int kBuckets = 128;
-
-__device__ __forceinline__ int len_bucket(int len) {
-  // 4 * log2(len + 1) without a log: exponent and the top two mantissa bits
-  const float f = (float)(len + 1);
-  const int b = ((__float_as_int(f) >> 21) - (127 << 2));  // 4 * floor-ish(log2)
-  return kBuckets - 1 - min(max(b, 0), kBuckets - 1);
-}
-
 __global__ void __launch_bounds__(1024) tile_order_bucket_kernel(const int2* __restrict__ ranges,
                                                                  int n_tiles,
                                                                  int32_t* __restrict__ out) {

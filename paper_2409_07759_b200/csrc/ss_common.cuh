@@ -242,6 +242,12 @@ int raster_bwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_
                     const int32_t* tile_order, const float* dimg, const float* t_final,
                     const int32_t* n_contrib, float* g2d, const int32_t* pbox,
                     cudaStream_t stream);
+// binning.cu: ss_bin_tiles + the raster launch order from the same tile scan
+int bin_tiles_with_order(const int32_t* order, const int32_t* offsets, const int32_t* bbox,
+                         const float* geom, const uint64_t* tile_mask, int32_t n,
+                         int64_t n_pairs, int32_t tiles_x, int32_t tiles_y, uint16_t* keys,
+                         int32_t* vals, int32_t* vals_out, int32_t* ranges, int32_t* tile_order,
+                         void* ws, size_t ws_bytes, cudaStream_t stream);
 namespace ss {
 int memzero(void* p, size_t bytes, cudaStream_t stream);  // ss_api.cu: PDL zero fill
 }

@@ -171,16 +171,19 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   v->n_pairs = k_host;
   if (k_host > v->pair_cap) return set_error(SS_ERR_CAPACITY, "ss_render_fwd: %d pairs > capacity", k_host);
   const int32_t* sv = v->vals;
+  bool tile_order_done = false;  // the chunked binning's tile scan writes it
   if (ss_get_binning() == 0 && ss_bin_tiles_supported(k_host, n_tiles)) {
     const size_t need_bin = ss_bin_tiles_workspace_bytes(k_host, n_tiles);
     if (v->ws_bytes < need_bin) {
       v->ws_needed = need_bin;
       return set_error(SS_ERR_WORKSPACE, "ss_render_fwd: workspace %zu < %zu", v->ws_bytes, need_bin);
     }
-    if ((rc = ss_bin_tiles(v->order, v->offsets, v->bbox, v->geom, v->tile_mask, n, k_host,
-                           tiles_x, tiles_y, (uint16_t*)v->keys, v->vals, v->vals_alt, v->ranges,
-                           v->ws, v->ws_bytes, stream)))
+    if ((rc = bin_tiles_with_order(v->order, v->offsets, v->bbox, v->geom, v->tile_mask, n,
+                                   k_host, tiles_x, tiles_y, (uint16_t*)v->keys, v->vals,
+                                   v->vals_alt, v->ranges, v->tile_order, v->ws, v->ws_bytes,
+                                   stream)))
       return rc;
+    tile_order_done = true;
     v->sorted_sel = 1;
     sv = v->vals_alt;
   } else {
@@ -196,7 +199,9 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
     if ((rc = ss_tile_ranges(sel ? v->keys_alt : v->keys, k_host, n_tiles, v->ranges, stream)))
       return rc;
   }
-  if ((rc = ss_tile_order(v->ranges, n_tiles, v->tile_order, v->ws, v->ws_bytes, stream))) return rc;
+  if (!tile_order_done &&
+      (rc = ss_tile_order(v->ranges, n_tiles, v->tile_order, v->ws, v->ws_bytes, stream)))
+    return rc;
   record(v->events[0], stream);
   if (pbox)
     rc = raster_fwd_bbox(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,
