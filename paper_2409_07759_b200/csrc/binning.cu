@@ -921,7 +921,8 @@ extern "C" int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const 
 }
 
 // ss_bin_tiles that also writes the raster launch order (ss_tile_order's
-// result) from its tile scan when tile_order != NULL.
+// result) from its tile scan when tile_order != NULL -- except with no pairs
+// (n == 0 or n_pairs == 0), where only the empty ranges are written.
 int bin_tiles_with_order(const int32_t* order, const int32_t* offsets, const int32_t* bbox,
                          const float* geom, const uint64_t* tile_mask, int32_t n,
                          int64_t n_pairs, int32_t tiles_x, int32_t tiles_y, uint16_t* keys,

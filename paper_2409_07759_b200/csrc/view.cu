@@ -183,7 +183,7 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
                                    v->vals_alt, v->ranges, v->tile_order, v->ws, v->ws_bytes,
                                    stream)))
       return rc;
-    tile_order_done = true;
+    tile_order_done = n > 0 && k_host > 0;  // (no pairs: the scan is skipped)
     v->sorted_sel = 1;
     sv = v->vals_alt;
   } else {
