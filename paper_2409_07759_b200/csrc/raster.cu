@@ -49,7 +49,6 @@ constexpr int kWarpsF = SS_RASTER_WARPS_FWD;    // warps per CTA, forward
 #define SS_BWD_MINB (32 / SS_RASTER_WARPS_BWD)  // 64 registers
 #endif
 constexpr float kKappa = -0.72134752044448170368f;  // -log2(e) / 2
-constexpr float kInvKappa = -1.38629436111989061883f;  // 1 / kappa = -2 ln 2
 constexpr float kMahaKappa = kMahaMax * kKappa;       // 64 kappa
 
 __device__ __forceinline__ float ex2(float x) {
