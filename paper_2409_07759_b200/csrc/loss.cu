@@ -168,33 +168,38 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
     }
   }
   __syncthreads();
-  // vertical pass (axis 0, loss.py:31) of (x, y), (xx, yy), xy
-  f2 (*v2a)[kLP] = s_v2[0];
-  vblur_pair(v2a, s_v1, [&](int r, int c, f2& va, float& vb) {
-    const f2 p = s_xy[r][c];
-    va = p;
-    vb = lo2(p) * hi2(p);
-  });
-  __syncthreads();
-  (void)v2a;
-  // (xx, yy) pair: a second vertical pass over the squares
+  // vertical pass (axis 0, loss.py:31) of (x, y), xy and (xx, yy) in one
+  // sweep over the region's columns
   for (int task = threadIdx.x; task < kLR * (kLT / kVR); task += kLossThreads) {
     const int c = task % kLR, r0 = (task / kLR) * kVR;
-    f2 acc[kVR];
+    f2 accA[kVR], accC[kVR];
+    float accB[kVR];
 #pragma unroll
-    for (int i = 0; i < kVR; ++i) acc[i] = bc(0.f);
+    for (int i = 0; i < kVR; ++i) {
+      accA[i] = accC[i] = bc(0.f);
+      accB[i] = 0.f;
+    }
 #pragma unroll
     for (int sidx = 0; sidx < kVR + 10; ++sidx) {
       const f2 p = s_xy[r0 + sidx][c];
+      const float xy = lo2(p) * hi2(p);
       const f2 sq = mul2(p, p);
 #pragma unroll
       for (int i = 0; i < kVR; ++i) {
         const int t = sidx - i;
-        if (t >= 0 && t <= 10) acc[i] = fma2(bc(win(t)), sq, acc[i]);
+        if (t >= 0 && t <= 10) {
+          accA[i] = fma2(bc(win(t)), p, accA[i]);
+          accB[i] = fmaf(win(t), xy, accB[i]);
+          accC[i] = fma2(bc(win(t)), sq, accC[i]);
+        }
       }
     }
 #pragma unroll
-    for (int i = 0; i < kVR; ++i) s_v2[1][r0 + i][c] = acc[i];
+    for (int i = 0; i < kVR; ++i) {
+      s_v2[0][r0 + i][c] = accA[i];
+      s_v1[r0 + i][c] = accB[i];
+      s_v2[1][r0 + i][c] = accC[i];
+    }
   }
   __syncthreads();
   // horizontal pass (axis 1, loss.py:32) + SSIM terms (loss.py:39-59)
