@@ -76,14 +76,21 @@ __global__ void depth_hist_kernel(const uint64_t* __restrict__ key64, int32_t n,
                                   int32_t* __restrict__ hist) {
   pdl_wait();
   pdl_trigger();
+  __shared__ int32_t s_culled;
+  if (threadIdx.x == 0) s_culled = 0;
+  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t k = i < n ? key64[i] : 0ull;
-  // culled keys all land in bucket nb: one atomic per warp for them (off-view
-  // splats are most of a novel view's store), one per key otherwise
+  // culled keys all land in bucket nb: counted per CTA in shared memory and
+  // added with one global atomic per CTA (off-view splats are most of a novel
+  // view's store; a global atomic per warp on one address serialises), one
+  // atomic per kept key otherwise
   const bool culled = i < n && k == ~0ull;
   const uint32_t cm = __ballot_sync(0xffffffffu, culled);
-  if (culled && (threadIdx.x & 31) == __ffs(cm) - 1) atomicAdd(&hist[nb], __popc(cm));
+  if (culled && (threadIdx.x & 31) == __ffs(cm) - 1) atomicAdd(&s_culled, __popc(cm));
   if (i < n && !culled) atomicAdd(&hist[depth_bucket(k, ~range[0], range[1], nb)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_culled) atomicAdd(&hist[nb], s_culled);
 }
 
 __global__ void depth_scatter_kernel(const uint64_t* __restrict__ key64, int32_t n,
@@ -97,11 +104,18 @@ __global__ void depth_scatter_kernel(const uint64_t* __restrict__ key64, int32_t
   const bool culled = i < n && k == ~0ull;
   // culled keys: one warp-aggregated atomic on bucket nb (their order inside
   // the trailing culled run is free)
+  // (per CTA: warps take offsets in shared memory, one global atomic per CTA)
+  __shared__ int32_t s_culled, s_base;
+  if (threadIdx.x == 0) s_culled = 0;
+  __syncthreads();
   const uint32_t cm = __ballot_sync(0xffffffffu, culled);
   int32_t cbase = 0;
   const int lane = threadIdx.x & 31;
-  if (cm && lane == __ffs(cm) - 1) cbase = atomicAdd(&cursor[nb], __popc(cm));
-  cbase = __shfl_sync(0xffffffffu, cbase, cm ? __ffs(cm) - 1 : 0);
+  if (cm && lane == __ffs(cm) - 1) cbase = atomicAdd(&s_culled, __popc(cm));
+  __syncthreads();
+  if (threadIdx.x == 0 && s_culled) s_base = atomicAdd(&cursor[nb], s_culled);
+  __syncthreads();
+  cbase = __shfl_sync(0xffffffffu, cbase, cm ? __ffs(cm) - 1 : 0) + (cm ? s_base : 0);
   if (i >= n) return;
   const uint32_t b = culled ? nb : depth_bucket(k, ~range[0], range[1], nb);
   const int32_t pos = culled ? cbase + __popc(cm & ((1u << lane) - 1u)) : atomicAdd(&cursor[b], 1);
