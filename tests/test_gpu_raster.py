@@ -305,12 +305,14 @@ def test_deterministic_backward_bit_identical(ss):
     grad_check(ga, g1, tol=1e-5, what="atomic vs deterministic")
 
 
-def test_depth_order_exact_on_adversarial_keys():
+@pytest.mark.parametrize("n_culled", [5000, 160_000])
+def test_depth_order_exact_on_adversarial_keys(n_culled):
     """ss_depth_order (range-normalised buckets + per-bucket sort) equals the
     stable 64-bit order, i.e. np.lexsort((index, z)) (raster.py:153): depths
     sharing their high 32 bits, exact ties, culled keys, long runs, runs whose
     keys share the prefix but not the high word, and far depths that clamp to
-    one prefix."""
+    one prefix.  n_culled = 160k: most of the store off-view, as in a novel
+    view (the culled run is placed by one global atomic per CTA)."""
     import torch
     from paper_2409_07759_b200 import _lib as L
     rng = np.random.default_rng(0)
@@ -325,7 +327,7 @@ def test_depth_order_exact_on_adversarial_keys():
     h = (np.array([2.9]).view(np.uint64)[0] >> np.uint64(32)) & ~np.uint64(1)
     hi = h + rng.integers(0, 2, 3000).astype(np.uint64)
     keys[63_000:66_000] = (hi << np.uint64(32)) | rng.integers(0, 2 ** 32, 3000).astype(np.uint64)
-    keys[rng.choice(n, 5000, replace=False)] = np.uint64(0xFFFFFFFFFFFFFFFF)  # culled
+    keys[rng.choice(n, n_culled, replace=False)] = np.uint64(0xFFFFFFFFFFFFFFFF)  # culled
     perm = rng.permutation(n)
     keys = keys[perm]
     kt = torch.from_numpy(keys.view(np.int64)).cuda()
