@@ -2,6 +2,9 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <atomic>
+#include <mutex>
+
 #include "ss_common.cuh"
 
 namespace ss {
@@ -46,6 +49,29 @@ int memzero(void* p, size_t bytes, cudaStream_t stream) {
   if (blocks > 148 * 8) blocks = 148 * 8;
   launch_k(memzero_kernel, (unsigned)blocks, 256, 0, stream, (unsigned char*)p, bytes);
   return check_launch("memzero");
+}
+
+// Per (device, kernel) high-water mark of the dynamic shared-memory attribute.
+constexpr int kAttrDevs = 64;
+static std::atomic<size_t> g_smem_attr[kAttrDevs][kSmemSlots];
+
+int ensure_smem(const void* kernel, int slot, size_t bytes) {
+  if (bytes <= 48 * 1024) return SS_OK;  // below the default limit
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kAttrDevs || slot < 0 ||
+      slot >= kSmemSlots)
+    return set_error(SS_ERR_CUDA, "ensure_smem: bad device or slot");
+  std::atomic<size_t>& hw = g_smem_attr[dev][slot];
+  if (bytes <= hw.load(std::memory_order_acquire)) return SS_OK;
+  // slow path serialised: the attribute and the mark only ever grow together
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (bytes <= hw.load(std::memory_order_relaxed)) return SS_OK;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      cudaSuccess)
+    return check_launch("ensure_smem");
+  hw.store(bytes, std::memory_order_release);
+  return SS_OK;
 }
 
 }  // namespace ss

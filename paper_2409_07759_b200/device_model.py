@@ -114,7 +114,13 @@ class DeviceModel:
         lib = L.lib()
         self.ws_compact = torch.empty(int(lib.ss_compact_workspace_bytes(n_rows_all)),
                                       dtype=torch.uint8, device=dev)
-        self.gen_host = torch.zeros(swin * GEN_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+        # double-buffered pinned generation table: a buffer is rewritten only
+        # after the event recorded behind its previous H2D copy has completed
+        self._gen_bufs = [torch.zeros(swin * GEN_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+                          for _ in range(2)]
+        self._gen_events = [None, None]
+        self._gen_i = 0
+        self.gen_host = self._gen_bufs[0]
         self.gen_dev = torch.zeros(swin * GEN_DTYPE.itemsize, dtype=torch.uint8, device=dev)
         self.reloc_ws = torch.empty(int(lib.ss_relocate_workspace_bytes(num_gs)),
                                     dtype=torch.uint8, device=dev)
@@ -176,6 +182,11 @@ class DeviceModel:
 
     def _gen_table(self, stepped):
         cfg = self.cfg
+        self._gen_i ^= 1
+        k = self._gen_i
+        if self._gen_events[k] is not None:
+            self._gen_events[k].synchronize()  # its previous copy has landed
+        self.gen_host = self._gen_bufs[k]
         tab = self.gen_host.numpy().view(GEN_DTYPE)
         for i, gen in enumerate(self.state.slices):
             e = tab[i]
@@ -190,9 +201,10 @@ class DeviceModel:
                                if cfg.gradient_scaling else 1.0)
             else:
                 e["active"] = 0
-        # the copy completes before the next step rewrites gen_host: every step
-        # synchronizes once (tile-pair count readback) after this point
         self.gen_dev.copy_(self.gen_host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._gen_events[k] = ev
 
     def compact(self, frame: int):
         """Active row ids of `frame` (a-2): optimizable rows of generations in
@@ -227,18 +239,24 @@ class DeviceModel:
         """One training view (train.py:375-417).  `draws` are the (frame, view)
         samples of every data-parallel rank this iteration; this rank renders
         draws[rank]; generations active in any drawn frame are stepped."""
-        state, cfg, sl = self.state, self.cfg, self.sl
-        lib = L.lib()
-        sp = L.stream_ptr()
-        frame, view = draws[rank]
-        frames = [f for f, _ in draws]
-        live = lambda ls, f: ls.start <= f < ls.expire  # noqa: E731
         from .train import stepped_generations
 
-        stepped = stepped_generations(state.slices, frames)
+        stepped = stepped_generations(self.state.slices, [f for f, _ in draws])
         self._gen_table(stepped)
+        sums = self.view_gradients(draws[rank], dataset)
+        if self.state.dp is not None:
+            self.state.dp.allreduce_grads(self.grads)
+        self.apply_step(stepped, it)
+        return sums
+
+    def view_gradients(self, draw, dataset):
+        """Forward, loss and backward of one (frame, view) draw: the
+        optimization-space gradient lands in self.grads (zeroed first).
+        Returns the device loss sums."""
+        frame, view = draw
+        sp = L.stream_ptr()
         rows, n, n_opt_here = self.compact(frame)
-        L.check(lib.ss_memzero(L.ptr(self.grads), self.grads.numel() * 4, sp), "memzero")
+        L.check(L.lib().ss_memzero(L.ptr(self.grads), self.grads.numel() * 4, sp), "memzero")
         cam = dataset.cameras[view]
         # ground truth may still be in flight on a copy stream: only the loss
         # waits for it, the projection / binning / raster run meanwhile
@@ -247,29 +265,35 @@ class DeviceModel:
             gt, gt_ready = get_async(frame, view)
         else:
             gt, gt_ready = dataset.device_frame(frame, view), None
-        self.pipe.deterministic = state.deterministic
+        self.pipe.deterministic = self.state.deterministic
         img = self.pipe.forward(self.store, rows, n, cam)
         if gt_ready is not None:
             torch.cuda.current_stream().wait_event(gt_ready)
         dimg, sums = self.lossbuf.run(img, cam.height, cam.width, gt_u8=gt, lut=self.lut,
-                                      ssim_weight=cfg.ssim_weight)
+                                      ssim_weight=self.cfg.ssim_weight)
         self.pipe.backward(dimg, self.grads, trainable_rows=self.num_gs)
-        if state.dp is not None:
-            state.dp.allreduce_grads(self.grads)
-        n_reg = sl * sum(stepped)
+        self.last_sums = sums
+        self.last_counts = (n, n_opt_here)
+        return sums
+
+    def apply_step(self, stepped, it):
+        """Fused Adam + gamma^w + projections + SGLD over the stepped
+        generations (the table _gen_table wrote), relocation every
+        relocate_period iterations (train.py:400-417)."""
+        state, cfg = self.state, self.cfg
+        lib = L.lib()
+        sp = L.stream_ptr()
+        n_reg = self.sl * sum(stepped)
         eta = None
         if state.noise_source == "numpy":
             eta = self._numpy_eta(stepped)
         h = _hyper(cfg, n_reg, True, self.seed, state.iteration)
         L.check(lib.ss_adam_sgld_step(L.ptr(self.opt), L.ptr(self.grads), L.ptr(self.m),
-                                      L.ptr(self.v), self.num_gs, sl, L.ptr(self.gen_dev),
+                                      L.ptr(self.v), self.num_gs, self.sl, L.ptr(self.gen_dev),
                                       ctypes.byref(h), L.ptr(eta), sp), "adam_sgld_step")
         if it % cfg.relocate_period == 0:
             self.relocate_device(cfg.dead_opacity_threshold)
         state.iteration += 1
-        self.last_sums = sums
-        self.last_counts = (n, n_opt_here)
-        return sums
 
     def _numpy_eta(self, stepped):
         """eta drawn per stepped generation in list order (train.py:255-258)."""

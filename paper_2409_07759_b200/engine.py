@@ -124,7 +124,7 @@ class ViewPipeline:
             return lib.ss_render_fwd(ctypes.byref(self.store_struct),
                                      ctypes.byref(self.cam_struct), ctypes.byref(v), sp)
 
-        return self._run_forward(n, int(cam.width), int(cam.height), call)
+        return self._run_forward(n, int(cam.width), int(cam.height), call, stream)
 
     def forward2d(self, splats: "Splats2D", width: int, height: int, stream=None):
         """_kernels.blend_forward on device-resident 2D splats (ss_render2d_fwd)."""
@@ -138,9 +138,9 @@ class ViewPipeline:
             return lib.ss_render2d_fwd(ctypes.byref(splats.struct), int(width), int(height),
                                        ctypes.byref(v), sp)
 
-        return self._run_forward(splats.n, int(width), int(height), call)
+        return self._run_forward(splats.n, int(width), int(height), call, stream)
 
-    def _run_forward(self, n: int, W: int, H: int, call):
+    def _run_forward(self, n: int, W: int, H: int, call, stream=None):
         tiles_x, tiles_y = (W + TILE - 1) // TILE, (H + TILE - 1) // TILE
         n_tiles = tiles_x * tiles_y
         self.n, self.width, self.height, self.n_tiles = n, W, H, n_tiles
@@ -180,12 +180,18 @@ class ViewPipeline:
             rc = call(v)
             if rc in (L.SS_ERR_CAPACITY, L.SS_ERR_WORKSPACE) and self.events is not None:
                 self.events["_pending"].pop()  # this attempt recorded nothing
+            # kernels queued by the failed attempt may still use the old
+            # buffers on `stream`: keep them alive in the caching allocator
+            # until that stream passes this point
+            s_ = stream if stream is not None else torch.cuda.current_stream()
             if rc == L.SS_ERR_CAPACITY:
                 cap = int(v.n_pairs * 1.25) + 1024
                 for name in ("keys", "vals", "keys_alt", "vals_alt"):
+                    self._b[name].record_stream(s_)
                     self._b[name] = torch.empty(cap, dtype=torch.int32, device=self.dev)
                 continue
             if rc == L.SS_ERR_WORKSPACE:
+                self._b["ws_bin"].record_stream(s_)
                 self._b["ws_bin"] = torch.empty(int(v.ws_needed * 1.25), dtype=torch.uint8,
                                                 device=self.dev)
                 continue
