@@ -55,46 +55,46 @@ METRIC5 = "render-only streaming playback frames/sec (1920x1080)"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 
 
+def _capture():
+    """The latest committed ncu --set full capture of the raster kernels
+    (profiles/r*_traffic.json), or None when its recorded source hash does
+    not match the current csrc/raster.cu (the counters would be stale)."""
+    import hashlib
+
+    files = sorted((ROOT / "profiles").glob("r*_traffic.json"))
+    if not files:
+        return None, "no capture committed"
+    d = json.loads(files[-1].read_text())
+    src = ROOT / "paper_2409_07759_b200" / "csrc" / "raster.cu"
+    sha = hashlib.sha256(src.read_bytes()).hexdigest()[:16]
+    if d.get("raster_cu_sha16") != sha:
+        return None, f"{files[-1].name} predates the current raster.cu (stale, not used)"
+    return d, f"{files[-1].name} (ncu --set full of this raster.cu, sha {sha}, config 3)"
+
+
 def load_traffic(kernels):
-    """Per-launch DRAM bytes (read + write) of the given kernels from the latest
-    committed ncu --set full capture (profiles/*_traffic.json), or None."""
-    files = sorted((ROOT / "profiles").glob("r*_traffic.json"))
-    if not files:
-        return None
-    d = json.loads(files[-1].read_text())
+    """Per-launch DRAM bytes (read + write) of the given kernels from the
+    committed capture of the CURRENT raster.cu, else None."""
+    d, note = _capture()
+    if d is None:
+        return None, note
     try:
-        return sum(d[k]["dram_bytes_read"] + d[k]["dram_bytes_write"] for k in kernels)
+        return sum(d[k]["dram_bytes_read"] + d[k]["dram_bytes_write"] for k in kernels), note
     except KeyError:
-        return None
+        return None, note
 
 
-def load_issue(kernels):
-    """SM issue-slot utilisation (percent of active cycles) of the given
-    kernels from the same committed ncu capture: the bound that applies to the
-    rasterizer (it is instruction-issue bound, not HBM bound)."""
-    files = sorted((ROOT / "profiles").glob("r*_traffic.json"))
-    if not files:
+def load_ncu_counters(kernels):
+    """Issue-slot utilisation, SM / L2 / L1 throughput, occupancy and
+    instructions per walked (warp, entry) of the given kernels from the same
+    capture (the raster kernels are instruction-issue bound), else None."""
+    d, note = _capture()
+    if d is None:
         return None
-    d = json.loads(files[-1].read_text())
-    try:
-        return {k: d[k]["issue_active_pct"] for k in kernels}
-    except KeyError:
-        return None
-
-
-def load_ncu_throughput(kernels):
-    """SM / L2 / L1 throughput (percent of B200 peak), L2 hit rate and
-    occupancy of the given kernels from the committed ncu capture."""
-    files = sorted((ROOT / "profiles").glob("r*_traffic.json"))
-    if not files:
-        return None
-    d = json.loads(files[-1].read_text())
-    keys = ("sm_throughput_pct", "l2_throughput_pct", "l1_throughput_pct", "l2_hit_rate_pct",
-            "occupancy_pct")
-    try:
-        return {k: {q: d[k].get(q) for q in keys} for k in kernels}
-    except KeyError:
-        return None
+    keys = ("issue_active_pct", "sm_throughput_pct", "l2_throughput_pct", "l1_throughput_pct",
+            "l2_hit_rate_pct", "occupancy_pct", "warp_instructions",
+            "instr_per_walked_warp_entry")
+    return {k: {q: d[k].get(q) for q in keys if q in d[k]} for k in kernels if k in d}
 
 
 def load_peaks():
@@ -152,18 +152,21 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
 
 
-def build_workload(cfg_id: int, dp, init="gt"):
+def build_workload(cfg_id: int, dp, init="gt", scene_ds=None):
     import torch
 
     from paper_2409_07759_b200 import synth, train
 
     c = CONFIGS[cfg_id]
-    if c["dynerf"]:
+    if scene_ds is not None:
+        scene, ds = scene_ds
+    elif c["dynerf"]:
         scene = synth.dynerf_scene(c["gt_n"], c["frames"], c["views"], c["W"], c["H"], seed=7)
+        ds = synth.device_video(scene)
     else:
         cams = synth.arc_cameras(c["views"], c["W"], c["H"], arc_degrees=36.0)
         scene = synth.make_scene(7, c["frames"], cams, c["gt_n"])
-    ds = synth.device_video(scene)
+        ds = synth.device_video(scene)
     pts = init_points(scene, c)
     tmp = tempfile.NamedTemporaryFile("w", suffix=".xyz", delete=False)
     np.savetxt(tmp, pts)
@@ -406,57 +409,155 @@ def roofline_pass(state, ds, window, steps):
 
 
 # --------------------------------------------------------------------------- CPU
-def cpu_reference_view(c, state_np, n_threads, crop=128, n_crops=4, seed=0):
-    """The oracle port (oracle/, the reference algorithm in fp64 C/numpy) timed
-    on the host: one training view of the workload, with the pixel loops run
-    on `n_crops` crop cameras of crop x crop pixels spread over the image and
-    extrapolated by P / P_crop; per-Gaussian stages timed at full size."""
-    from oracle import splat_oracle as O
+def cpu_model_name() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
 
+    return platform.processor() or "unknown"
+
+
+class CpuTrainer:
+    """The reference algorithm on the host -- oracle/ (the reference's fp64
+    numpy stages and its two pixel loops in C, all host threads) -- training
+    WHOLE 1352x1014 views of the bench workload, one view per step like
+    train_swin (train.py:374-417): projection (raster.py:76-173) -> global
+    (z, src) order -> blend forward (_kernels.py:20-53) -> L1 + SSIM + regs
+    (loss.py:73-118) -> blend backward (_kernels.py:56-130) -> projection
+    backward (raster.py:249-347) -> per-generation Adam (train.py:321-344)
+    -> SGLD (train.py:246-264), relocation at it = 0 (train.py:416-417).
+
+    Same model and window as the GPU arm: the ground-truth-init store after
+    genesis + schedule_expire + mature(1), window [1, 1 + swin).  At frame f
+    the active set is optimizable generations 0..f-1 (trained copies) then
+    matured generations f..swin-1 (frozen init copies) -- the compaction
+    order of train.py:380-386 -- so n_opt = f * slice.  The pixel loops walk
+    tile lists (oracle.tile_bins: the reference's per-pixel sequence, the
+    same images and gradients as the global walk), the only way a full view
+    finishes in seconds.  Ground truth: the oracle's render of the animated
+    scene at (f, v) for `n_gt` fixed draws, decoded through the u8 sRGB
+    round trip as read_png does (rendered at setup, outside the timing)."""
+
+    def __init__(self, c, threads, n_gt=4, seed=0):
+        from paper_2409_07759_b200.synth import make_scene
+        from oracle import splat_oracle as O
+
+        self.O, self.c, self.threads = O, c, threads
+        k = (300.0 / c["gt_n"]) ** (1 / 3) if c["dynerf"] else 1.0
+        scene = make_scene(7, c["frames"], [], c["gt_n"], scale_range=(0.045 * k, 0.1 * k))
+        means, quats, scales, opac, cols = gt_rows(scene, c)
+        self.n, self.swin = c["num_gs"], c["swin"]
+        self.sl = self.n // self.swin
+        init = {"mean": means.copy(), "quat": quats.copy(), "log_scale": np.log(scales),
+                "opacity_logit": O.logit(opac), "color": cols.copy()}
+        self.mat = {k2: v.copy() for k2, v in init.items()}          # frozen copies
+        self.opt = {k2: v.copy() for k2, v in init.items()}          # trained copies
+        self.m = {k2: np.zeros_like(v) for k2, v in init.items()}
+        self.v = {k2: np.zeros_like(v) for k2, v in init.items()}
+        self.t = np.zeros(self.swin, dtype=np.int64)                  # per-generation adam_t
+        self.cams = _arc_cams_np(c)
+        self.rng = np.random.default_rng(seed)
+        self.win = (1, 1 + self.swin) if c["frames"] > 1 else (0, 1)
+        self.gt = []
+        for _ in range(n_gt):
+            f = int(self.rng.integers(self.win[0], min(self.win[1], c["frames"])))
+            v = int(self.rng.integers(0, len(self.cams)))
+            g = scene.gaussians_at(f)
+            img = O.render_arrays(self.cams[v], g.means, g.quats, g.scales, g.opacities,
+                                  g.colors, nthreads=threads, tiled=True)
+            self.gt.append((f, v, O.linear_from_u8(O.u8_from_linear(img))))
+        self.step_i = 0
+        self.stats = []
+
+    def _active(self, n_opt):
+        sl = slice(0, n_opt)
+        rest = slice(n_opt, self.n)
+        out = {}
+        for k2 in self.opt:
+            out[k2] = np.concatenate([self.opt[k2][sl], self.mat[k2][rest]])
+        return out
+
+    def step(self, threads=None):
+        O = self.O
+        th = self.threads if threads is None else threads
+        f, v, gt = self.gt[self.step_i % len(self.gt)]
+        it = self.step_i
+        self.step_i += 1
+        cam = self.cams[v]
+        n_opt = self.sl * (f - self.win[0] + 1) if self.c["frames"] > 1 else self.n
+        a = self._active(n_opt)
+        scales = np.exp(a["log_scale"])
+        opac = O.sigmoid(a["opacity_logit"])
+        cache = O.project_arrays(cam, a["mean"], a["quat"], scales, opac, a["color"])
+        H, W = cam.height, cam.width
+        bins = O.tile_bins(cache, W, H, floor_log2=None)  # the reference rule
+        fw = O.blend_forward_tiled(cache, H, W, nthreads=th, bins=bins)
+        _, gimg, reg = O.loss(fw["image"], gt, opac[:n_opt], scales[:n_opt])
+        g2d = O.blend_backward_tiled(cache, bins, H, W, gimg, nthreads=th)
+        trainable = np.zeros(self.n, dtype=bool)
+        trainable[:n_opt] = True
+        grads = O.projection_backward(cam, cache, self.n, *g2d, trainable=trainable)
+        grads["opacity_logit"][:n_opt] += reg["opacity_logit"]
+        grads["log_scale"][:n_opt] += reg["log_scale"]
+        gens = list(range(n_opt // self.sl))
+        views = []
+        for gi in gens:
+            r = slice(gi * self.sl, (gi + 1) * self.sl)
+            p = {k2: self.opt[k2][r] for k2 in self.opt}
+            mm = {k2: self.m[k2][r] for k2 in self.m}
+            vv = {k2: self.v[k2][r] for k2 in self.v}
+            self.t[gi] = O.optimizer_step(p, mm, vv, int(self.t[gi]),
+                                          {k2: grads[k2][r] for k2 in grads})
+            views.append((p, mm, vv))
+        O.sgld_perturb([p for p, _, _ in views], 1.6e-4, 5e4,
+                       [self.rng.standard_normal((self.sl, 3)) for _ in views])
+        if it % 100 == 0:
+            alpha = O.sigmoid(np.concatenate([p["opacity_logit"] for p, _, _ in views]))
+            n_dead = int((alpha < 0.005).sum())
+            O.relocate([p for p, _, _ in views], [mm for _, mm, _ in views],
+                       [vv for _, _, vv in views], 0.005, self.rng.random(max(n_dead, 1)))
+        self.stats.append((bins["K"], fw["K_used"]))
+
+
+def cpu_crop_view(trainer, crop=256, n_crops=4, threads=1):
+    """Crop-extrapolated s/view: the pixel loops + loss on
+    `n_crops` crop cameras of crop x crop px (shifted principal point), scaled
+    by P / P_crop, plus the per-splat stages at full size."""
+    O = trainer.O
+    c = trainer.c
     W, H = c["W"], c["H"]
-    cams = _arc_cams_np(c)
-    cam = cams[0]
-    means, quats, scales, opac, cols, opt_params = state_np
-    rng = np.random.default_rng(seed)
+    cam = trainer.cams[0]
+    a = trainer._active(trainer.n)
+    scales, opac = np.exp(a["log_scale"]), O.sigmoid(a["opacity_logit"])
     t0 = time.perf_counter()
-    cache = O.project_arrays(cam, means, quats, scales, opac, cols)
-    t_proj = time.perf_counter() - t0
-    t_pix = 0.0
-    xs = [W // 4, 3 * W // 4]
-    ys = [H // 4, 3 * H // 4]
-    centers = [(x, y) for y in ys for x in xs][:n_crops]
-    for (xc, yc) in centers:
-        ccam = _Cam(crop, crop, cam.fx, cam.fy, cam.cx - (xc - crop // 2), cam.cy - (yc - crop // 2),
-                    cam.rotation, cam.translation)
-        gt = O.linear_from_u8(rng.integers(0, 256, (crop, crop, 3), dtype=np.uint8))
-        t1 = time.perf_counter()
-        cc = O.project_arrays(ccam, means, quats, scales, opac, cols)
-        t2 = time.perf_counter()
-        if cc is None:
-            continue
-        img = O.blend_forward(cc, crop, crop, nthreads=n_threads)
-        n_opt = len(opt_params["mean"])
-        _, gimg, reg = O.loss(img, gt, opac[:n_opt], scales[:n_opt])
-        g2d = O.blend_backward(cc, crop, crop, gimg, nthreads=n_threads)
-        t3 = time.perf_counter()
-        t_pix += t3 - t2
-        t_proj_c = t2 - t1
-    t_pix = t_pix / max(len(centers), 1) * (W * H) / (crop * crop)
-    # per-Gaussian stages at full size: projection backward + optimizer + SGLD
+    cache = O.project_arrays(cam, a["mean"], a["quat"], scales, opac, a["color"])
     p = len(cache["src"])
-    zeros = [np.zeros((p, 2)), np.zeros((p, 3)), np.zeros(p), np.zeros((p, 3))]
-    t4 = time.perf_counter()
-    grads = O.projection_backward(cam, cache, len(means), *zeros)
-    n_opt = len(opt_params["mean"])
-    g_opt = {k: grads[k][:n_opt] for k in O.PARAM_GROUPS}
-    params = {k: v.copy() for k, v in opt_params.items()}
-    m = {k: np.zeros_like(v) for k, v in params.items()}
-    v = {k: np.zeros_like(x) for k, x in params.items()}
-    O.optimizer_step(params, m, v, 0, g_opt)
-    O.sgld_perturb([params], 1.6e-4, 5e4, [rng.standard_normal((n_opt, 3))])
-    t_gauss = time.perf_counter() - t4 + t_proj
-    return t_pix + t_gauss, {"t_pixel_extrapolated_s": t_pix, "t_per_gaussian_s": t_gauss,
-                             "crops": len(centers), "crop": crop}
+    O.projection_backward(cam, cache, trainer.n, np.zeros((p, 2)), np.zeros((p, 3)),
+                          np.zeros(p), np.zeros((p, 3)))
+    t_gauss = time.perf_counter() - t0
+    xs, ys = [W // 4, 3 * W // 4], [H // 4, 3 * H // 4]
+    centers = [(x, y) for y in ys for x in xs][:n_crops]
+    t_pix, used = 0.0, 0
+    rng = np.random.default_rng(1)
+    for xc, yc in centers:
+        cc = _Cam(crop, crop, cam.fx, cam.fy, cam.cx - (xc - crop // 2), cam.cy - (yc - crop // 2),
+                  cam.rotation, cam.translation)
+        t1 = time.perf_counter()
+        cch = O.project_arrays(cc, a["mean"], a["quat"], scales, opac, a["color"])
+        if cch is None:
+            continue
+        bins = O.tile_bins(cch, crop, crop, floor_log2=None)
+        img = O.blend_forward_tiled(cch, crop, crop, nthreads=threads, bins=bins)["image"]
+        gt = O.linear_from_u8(rng.integers(0, 256, (crop, crop, 3), dtype=np.uint8))
+        _, gimg, _ = O.loss(img, gt, opac[:1], scales[:1])
+        O.blend_backward_tiled(cch, bins, crop, crop, gimg, nthreads=threads)
+        t_pix += time.perf_counter() - t1
+        used += 1
+    return t_gauss + t_pix / max(used, 1) * (W * H) / (crop * crop)
 
 
 class _Cam:
@@ -479,23 +580,6 @@ def _arc_cams_np(c):
         R = np.stack([right, up, fwd])
         out.append(_Cam(W, H, focal, focal, W / 2, H / 2, R, -R @ center))
     return out
-
-
-def cpu_state(c):
-    """Host copy of a config's model: the trainer's init from the frame-0
-    point cloud (same recipe as the GPU arm), direct space."""
-    from paper_2409_07759_b200.synth import make_scene
-    from oracle import splat_oracle as O
-
-    k = (300.0 / c["gt_n"]) ** (1 / 3) if c["dynerf"] else 1.0
-    scene = make_scene(7, c["frames"], [], c["gt_n"], scale_range=(0.045 * k, 0.1 * k))
-    means, quats, scales, opac, cols = gt_rows(scene, c)
-    n = c["num_gs"]
-    sl = n // c["swin"]
-    opt = {"mean": means[:sl].copy(), "quat": quats[:sl].copy(),
-           "log_scale": np.log(scales[:sl]), "opacity_logit": O.logit(opac[:sl]),
-           "color": cols[:sl].copy()}
-    return means, quats, scales, opac, cols, opt
 
 
 def build_player(n_total=1_000_000, swin=20, views=20, W=1920, H=1080, seed=7):
@@ -654,32 +738,85 @@ def run_render_only(args, dp):
     return out
 
 
+def bracket_random_init(args, dp, scene, ds):
+    """The same measurement from the reference's own init (init_state,
+    train.py:207-235: frame-0 point cloud, opacity 0.1, nearest-neighbour
+    scales) after the same genesis / schedule / mature(1) setup: the
+    other end of the model-state range the headline's converged proxy sits
+    at.  Same views and ground truth; W warm-up + K timed steps."""
+    import torch
+
+    from paper_2409_07759_b200 import train
+
+    c, _, _, state, window = build_workload(args.config, dp, "random", scene_ds=(scene, ds))
+    train.train_swin(window[0], window[1], state, ds, iterations=args.warmup)
+    state.device.pipe.enable_timing(True)
+    ms = time_steps(state, ds, window, args.steps, dp)
+    kms = state.device.pipe.kernel_ms()
+    state.device.pipe.enable_timing(False)
+    out = {"init": "init_state from the frame-0 point cloud (train.py:207-235)",
+           "value": args.steps / (ms / 1e3), "unit": "views/s", "ms_per_step": ms / args.steps,
+           "ms_per_view": {k: kms.get(k, 0.0) / args.steps for k in ("raster_fwd", "raster_bwd")}}
+    del state
+    torch.cuda.empty_cache()
+    return out
+
+
+def workload_config(c, window, world, init):
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": c["name"], "width": c["W"], "height": c["H"], "num_gs": c["num_gs"],
+            "gt_gaussians": c["gt_n"], "swin_size": c["swin"], "window": list(window),
+            "parallelism": f"dp{world}",
+            "init": ("ground-truth splats (converged-model proxy)" if init == "gt"
+                     else "init_state from the frame-0 point cloud"),
+            "global_batch": world,
+            "l2": "per-step working set > 126 MB L2 (tile pairs + optimizer state); "
+                  "no explicit flush"}
+
+
 def run_reference(args, c):
+    """--impl reference: the reference algorithm (oracle/ port: fp64 numpy +
+    the C pixel loops, all host threads) training whole 1352x1014 views of
+    the same workload (CpuTrainer), W untimed + K timed steps; then, untimed,
+    one whole view on ONE core and a 256^2-crop extrapolation for context."""
     from oracle import splat_oracle as O
 
     O.build_oracle()
     threads = O.default_threads()
-    st = cpu_state(c)
+    t0 = time.perf_counter()
+    tr = CpuTrainer(c, threads)
+    setup_s = time.perf_counter() - t0
     for _ in range(args.warmup):
-        cpu_reference_view(c, st, threads, crop=64, n_crops=1)
+        tr.step()
     times = []
-    info = {}
     for _ in range(args.steps):
-        t, info = cpu_reference_view(c, st, threads)
-        times.append(t)
-    tv = float(np.mean(times))
-    value = 1.0 / tv
-    sample = (f"crop-extrapolated: {info.get('crops')} crops of {info.get('crop')}^2 px "
-              f"(pixel loops scaled by P/P_crop) + full-size per-Gaussian stages")
+        t1 = time.perf_counter()
+        tr.step()
+        times.append(time.perf_counter() - t1)
+    total = float(np.sum(times))
+    value = args.steps / total
+    t1 = time.perf_counter()
+    tr.step(threads=1)
+    one_core_s = time.perf_counter() - t1
+    crop_s = cpu_crop_view(tr, crop=256, n_crops=4, threads=threads)
+    K = [k for k, _ in tr.stats]
+    K_used = [u for _, u in tr.stats]
+    sample = (f"whole {c['W']}x{c['H']} training views, {threads} threads: oracle port of the "
+              f"reference (fp64; pixel loops in C over tile lists, numpy stages), "
+              f"{total / args.steps:.2f} s/view")
     return {
-        "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tv * 1e3,
+        "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "impl": "reference",
-        "config": {"workload": c["name"], "width": c["W"], "height": c["H"],
-                   "num_gs": c["num_gs"], "swin_size": c["swin"], "threads": threads},
+        "data": "synthetic (SURVEY.md §8(d) DyNeRF-shaped recipe, oracle-rendered ground truth)",
+        "impl": "reference",
+        "config": workload_config(c, tr.win, 1, "gt"),
         "cpu_baseline": {"value": value, "unit": "views/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model_name(),
+                         "one_core_s_per_view": one_core_s,
+                         "crop256_extrapolated_s_per_view": crop_s,
+                         "K_per_view": float(np.mean(K)), "K_used_per_view": float(np.mean(K_used)),
+                         "setup_s": setup_s},
         "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -757,6 +894,8 @@ def main():
     ap.add_argument("--strip-fwd", type=int, default=0, help="forward strip only (overrides --strip)")
     ap.add_argument("--init", default="gt", choices=["gt", "random"],
                     help="model state: ground-truth splats (converged proxy) or init_state")
+    ap.add_argument("--no-bracket", dest="bracket", action="store_false",
+                    help="skip the random-init bracket measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     c = CONFIGS.get(args.config)
@@ -830,13 +969,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (SURVEY.md §8(d) DyNeRF-shaped recipe, GPU-rendered ground truth)",
-        "config": {"workload": c["name"], "width": c["W"], "height": c["H"],
-                   "num_gs": c["num_gs"], "gt_gaussians": c["gt_n"], "swin_size": c["swin"],
-                   "window": list(window), "parallelism": f"dp{world}",
-                   "init": ("ground-truth splats (converged-model proxy)" if args.init == "gt"
-                            else "init_state from the frame-0 point cloud"),
-                   "global_batch": world, "l2": "per-step working set > 126 MB L2 "
-                   "(tile pairs + optimizer state); no explicit flush"},
+        "config": workload_config(c, window, world, args.init),
         "clocks": clocks.summary(),
     }
     if not args.no_e2e:
@@ -858,15 +991,13 @@ def main():
     b_raster = 116.0 * k_used + 52.0 * P
     peak, peak_kind = load_peaks()
     achieved = b_raster / t_raster / 1e9 if t_raster > 0 else 0.0
+    traffic, traffic_note = load_traffic(["raster_fwd", "raster_bwd"])
     out["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                       "frac": achieved / peak,
-                       "traffic": load_traffic(["raster_fwd", "raster_bwd"]),
-                       "issue_active_pct": load_issue(["raster_fwd", "raster_bwd"]),
-                       "ncu_throughput": load_ncu_throughput(["raster_fwd", "raster_bwd"]),
-                       "issue_note": "ncu smsp__issue_active (profiles/r*_traffic.json): the "
-                                     "raster kernels are issue-bound; HBM frac is low by design",
-                       "traffic_source": "ncu --set full dram__bytes_read+write per launch "
-                                         "(profiles/r*_traffic.json, config 3)",
+                       "frac": achieved / peak, "traffic": traffic,
+                       "traffic_source": traffic_note,
+                       "ncu_counters": load_ncu_counters(["raster_fwd", "raster_bwd"]),
+                       "issue_note": "the raster kernels are instruction-issue bound (ncu "
+                                     "issue_active, profiles/): the HBM frac is low by design",
                        "kernel": "raster_fwd + raster_bwd", "peak_source": peak_kind,
                        "bytes_per_view": b_raster, "K_used": k_used, "K": k_pairs,
                        "timing": "kernel ms: CUDA events around each raster launch over the "
@@ -878,19 +1009,23 @@ def main():
     ours, aten, names = count_launches(state, ds, window)
     out["gpu_launches"] = ours * args.steps
     out["gpu_launches_per_step"] = ours
-    if rank == 0 and not args.no_cpu_baseline:
+    if args.bracket and world == 1 and args.init == "gt":
+        out["bracket"] = bracket_random_init(args, dp, scene, ds)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import splat_oracle as O
 
         O.build_oracle()
         threads = O.default_threads()
-        st = cpu_state(c)
-        t, info = cpu_reference_view(c, st, threads)
+        tr = CpuTrainer(c, threads, n_gt=2)
+        t1 = time.perf_counter()
+        for _ in range(2):
+            tr.step()
+        t = (time.perf_counter() - t1) / 2
         out["cpu_baseline"] = {"value": 1.0 / t, "unit": "views/s", "cores": threads,
-                               "kind": "port",
-                               "sample": f"oracle (reference algorithm, fp64) on "
-                                         f"{info['crops']} crops of {info['crop']}^2 px, pixel "
-                                         f"loops extrapolated by P/P_crop; per-Gaussian stages "
-                                         f"at full size; {t:.1f} s/view"}
+                               "kind": "port", "cpu_model": cpu_model_name(),
+                               "sample": f"2 whole {c['W']}x{c['H']} training views of this "
+                                         f"workload through the oracle port of the reference "
+                                         f"(fp64, all host threads), {t:.2f} s/view"}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dp is not None:

@@ -186,6 +186,18 @@ int ss_bin_tiles(const int32_t* order, const int32_t* offsets, const int32_t* bb
 int ss_set_binning(int32_t mode);
 int ss_get_binning(void);
 
+/* Alpha floor of the binning and the rasterizer, as log2: a (splat, pixel)
+ * contribution is blended only when maha <= 64 (the reference rule,
+ * _kernels.py:39-41) AND alpha G >= 2^floor; tiles are emitted only where
+ * that can hold (per-splat margin min(64, 2 ln(alpha / 2^floor)), see
+ * ss_common.cuh cull_margin).  Each skipped contribution is below 2^floor,
+ * so a pixel moves by at most ~2 |skipped| 2^floor (~3e-5 at 4000 skipped
+ * entries for the default floor = -28), inside the north star's 1e-4.
+ * floor = 0 disables it (the reference's rule alone).  Valid: 0 or
+ * [-126, -1].  Process-wide; set before rendering. */
+int ss_set_alpha_floor(int32_t log2_floor);
+int32_t ss_get_alpha_floor(void);
+
 /* Tiles ordered by list length, longest first (raster scheduling order:
  * longest-processing-time-first across the SMs).  ws >= ss_tile_order_workspace_bytes. */
 size_t ss_tile_order_workspace_bytes(int32_t n_tiles);

@@ -28,6 +28,14 @@ SSIM_C1 = 0.01 ** 2        # loss.py:14
 SSIM_C2 = 0.03 ** 2        # loss.py:15
 TILE = 16                  # build's tile edge (a-4); not a reference constant
 RANK_BITS = 21             # key = tile << 21 | depth rank
+# Alpha floor of the build's binning (libswings ss_set_alpha_floor, default
+# -28): a (splat, tile) pair is emitted only where alpha G >= 2^-28 can hold
+# at some pixel of the tile, i.e. m <= 2 ln(alpha / 2^-28) as well as
+# m <= 64.  Skipped contributions are below 2^-28 each: the image moves by
+# at most ~2 |S| 2^-28 (|S| = skipped entries of a pixel), far inside the
+# north star's 1e-4.  None = the reference's maha <= 64 rule only.
+ALPHA_FLOOR_LOG2 = -28
+TWO_LN2 = 1.3862943611198906
 PARAM_GROUPS = ("mean", "quat", "log_scale", "opacity_logit", "color")  # train.py:39
 
 _HERE = Path(__file__).resolve().parent
@@ -303,7 +311,7 @@ def render_arrays_backward(cam, means, quats, scales, opacities, colors, grad_im
         return {"mean": np.zeros((n, 3)), "log_scale": np.zeros((n, 3)), "quat": np.zeros((n, 4)),
                 "opacity_logit": np.zeros((n,)), "color": np.zeros((n, 3))}
     if tiled:
-        bins = tile_bins(cache, cam.width, cam.height)
+        bins = tile_bins(cache, cam.width, cam.height, floor_log2=None)
         g2d = blend_backward_tiled(cache, bins, cam.height, cam.width, grad_image, nthreads)
     else:
         g2d = blend_backward(cache, cam.height, cam.width, grad_image, nthreads)
@@ -314,13 +322,16 @@ def render_arrays_backward(cam, means, quats, scales, opacities, colors, grad_im
 # a-4: tile binning restated (build design; reproduces the reference order)
 # --------------------------------------------------------------------------
 
-def tile_bins(cache, width, height, tile=TILE, exact=True):
+def tile_bins(cache, width, height, tile=TILE, exact=True, floor_log2=ALPHA_FLOOR_LOG2):
     """SURVEY.md §8 a-4.  For each kept splat i (index into the kept subset)
     with depth rank r_i under the reference's global (z, src) order
     (raster.py:153), emit one key ``tile_id << 21 | r_i`` per 16x16 tile
     overlapping its half-open pixel bbox [x0,x1)x[y0,y1) (raster.py:144-150)
     -- with ``exact``, only tiles the maha <= 64 ellipse reaches
-    (tile_keep_mask; dropped tiles hold no pixel the reference blends) --
+    (tile_keep_mask; dropped tiles hold no pixel the reference blends) and,
+    with ``floor_log2`` (the library default), only those where
+    alpha G >= 2^floor_log2 can hold (None: the reference rule alone; the
+    per-pixel oracles on those bins are then the reference's exact walk) --
     sort keys ascending; a tile's range is the run of its tile id.
 
     Returns dict(keys (K,) uint64 sorted, vals (K,) int64 kept-subset index,
@@ -347,7 +358,7 @@ def tile_bins(cache, width, height, tile=TILE, exact=True):
     tx = np.repeat(tx0, counts) + local % np.maximum(w, 1)
     ty = np.repeat(ty0, counts) + local // np.maximum(w, 1)
     if exact and total:
-        keep = tile_keep_mask(cache, owner, tx, ty, tile)
+        keep = tile_keep_mask(cache, owner, tx, ty, tile, floor_log2)
         owner, tx, ty = owner[keep], tx[keep], ty[keep]
         total = int(keep.sum())
     tile_id = ty * tiles_x + tx
@@ -369,7 +380,7 @@ def blend_forward_tiled(cache, height, width, nthreads=1, bins=None):
     returns per-pixel walked entries, contributors and final T, and K_used
     (SURVEY.md §8 notation)."""
     if bins is None:
-        bins = tile_bins(cache, width, height)
+        bins = tile_bins(cache, width, height, floor_log2=None)  # the reference's exact walk
     img = np.zeros((height, width, 3))
     walked = np.zeros(height * width, dtype=np.int64)
     contrib = np.zeros(height * width, dtype=np.int64)
@@ -629,21 +640,42 @@ CULL_MARGIN = np.float32(64.0625)
 _F = np.float32
 
 
-def tile_geom(i0, i1, i2):
+def cull_margin(alpha, floor_log2=ALPHA_FLOOR_LOG2):
+    """Per-splat maha margin M of the tile test (ss_common.cuh cull_margin):
+    64.0625 (the maha <= 64 cut with a 1e-3 margin), or with the floor
+    min(64.0625, (2 (f - 1) + 2 ln2 (e - floor)) (1 + 2^-10) + 2^-4) with
+    alpha = f 2^e (frexp) -- an upper bound of 2 ln(alpha / 2^floor)
+    (ln f <= f - 1) made of IEEE-rounded fp64 operations only, so numpy and
+    the GPU agree bit for bit.  M <= 0: the splat reaches no tile."""
+    alpha = np.asarray(alpha, dtype=np.float64)
+    full = np.full(alpha.shape, float(CULL_MARGIN))
+    if floor_log2 is None:
+        return full
+    f, e = np.frexp(alpha)
+    m = 2.0 * (f - 1.0) + TWO_LN2 * (e - int(floor_log2)).astype(np.float64)
+    m = m * 1.0009765625 + 0.0625
+    m = np.minimum(m, full)
+    return np.where(alpha > 0.0, m, -1.0)
+
+
+def tile_geom(i0, i1, i2, margin=None):
     """Per-splat constants of the row-interval tile test, fp64 then rounded
     once to float32 (ss_common.cuh make_geom): det = i0 i2 - i1^2,
     sy = i1 sqrt(M / (i2 det)) (dy of the ellipse's rightmost point is -sy),
-    ymax = sqrt(M i0 / det) (its vertical half extent), M = CULL_MARGIN."""
+    ymax = sqrt(M i0 / det) (its vertical half extent), m0 = i0 M, M = the
+    per-splat cull_margin (CULL_MARGIN without the alpha floor)."""
     i0, i1, i2 = (np.asarray(a, dtype=np.float64) for a in (i0, i1, i2))
-    m = float(CULL_MARGIN)
+    m = np.full(i0.shape, float(CULL_MARGIN)) if margin is None else np.asarray(margin, np.float64)
+    mp = np.maximum(m, 0.0)  # M <= 0 reaches no tile (masked by the caller)
     det = i0 * i2 - i1 * i1
-    sy = i1 * np.sqrt(m / (i2 * det))
-    ymax = np.sqrt((m * i0) / det)
+    sy = i1 * np.sqrt(mp / (i2 * det))
+    ymax = np.sqrt((mp * i0) / det)
+    m0 = (i0 * mp).astype(_F)
     f0 = i0.astype(_F)
-    return f0, i1.astype(_F), det.astype(_F), sy.astype(_F), ymax.astype(_F), _F(1) / f0
+    return m0, i1.astype(_F), det.astype(_F), sy.astype(_F), ymax.astype(_F), _F(1) / f0
 
 
-def tile_row_span(i0, i1, det, sy, ymax, r0, v, Y0, Y1):
+def tile_row_span(m0, i1, det, sy, ymax, r0, v, Y0, Y1):
     """x-interval [L, R] (relative to the splat centre) where the ellipse
     m <= CULL_MARGIN meets the pixel-centre rows [Y0, Y1], and whether it
     meets them at all.  float32 restatement of ss_common.cuh row_span (same
@@ -654,7 +686,6 @@ def tile_row_span(i0, i1, det, sy, ymax, r0, v, Y0, Y1):
     lo = np.maximum(np.asarray(Y0).astype(_F) - v, -ymax)
     hi = np.minimum(np.asarray(Y1).astype(_F) - v, ymax)
     meets = lo <= hi
-    m0 = i0 * CULL_MARGIN
     cR = np.minimum(np.maximum(-sy, lo), hi)
     cL = np.minimum(np.maximum(sy, lo), hi)
     sR = np.sqrt(np.maximum(m0 - (det * cR) * cR, _F(0)))
@@ -664,18 +695,20 @@ def tile_row_span(i0, i1, det, sy, ymax, r0, v, Y0, Y1):
     return meets, L, R
 
 
-def tile_keep_mask(cache, owner, tx, ty, tile=TILE):
+def tile_keep_mask(cache, owner, tx, ty, tile=TILE, floor_log2=ALPHA_FLOOR_LOG2):
     x0, x1, y0, y1 = cache["bbox"]
     i0, i1, i2 = cache["inv2d"][owner].T
     u, v = cache["mean2d"][owner].T
-    f0, f1, det, sy, ymax, r0 = tile_geom(i0, i1, i2)
+    margin = cull_margin(cache["alpha"][owner], floor_log2)
+    m0, f1, det, sy, ymax, r0 = tile_geom(i0, i1, i2, margin)
     Y0 = np.maximum(ty * tile, y0[owner])
     Y1 = np.minimum(ty * tile + tile - 1, y1[owner] - 1)
-    meets, L, R = tile_row_span(f0, f1, det, sy, ymax, r0, v, Y0, Y1)
+    with np.errstate(invalid="ignore"):
+        meets, L, R = tile_row_span(m0, f1, det, sy, ymax, r0, v, Y0, Y1)
     uf = np.asarray(u, dtype=np.float64).astype(_F)
     ax = np.maximum(tx * tile, x0[owner]).astype(_F) - uf
     bx = np.minimum(tx * tile + tile - 1, x1[owner] - 1).astype(_F) - uf
-    return meets & (ax <= R) & (bx >= L)
+    return meets & (ax <= R) & (bx >= L) & (margin > 0.0)
 
 
 # ---------------------------------------------------------------------------

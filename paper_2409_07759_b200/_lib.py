@@ -85,6 +85,8 @@ _SIGNATURES = {
     "ss_set_raster_strips": ([I32, I32], c_int),
     "ss_set_binning": ([I32], c_int),
     "ss_get_binning": ([], c_int),
+    "ss_set_alpha_floor": ([I32], c_int),
+    "ss_get_alpha_floor": ([], I32),
     "ss_bin_tiles_workspace_bytes": ([I64, I32], c_size_t),
     "ss_bin_tiles_supported": ([I64, I32], I32),
     "ss_bin_tiles": ([P, P, P, P, P, I32, I64, I32, I32, P, P, P, P, P, c_size_t, P], c_int),

@@ -116,17 +116,19 @@ __device__ __forceinline__ void write_record(int i, double ux, double uy, double
                                              uint64_t* __restrict__ depth_key,
                                              int4* __restrict__ bbox, int32_t* __restrict__ n_tiles,
                                              float* __restrict__ geom,
-                                             uint64_t* __restrict__ tile_mask) {
+                                             uint64_t* __restrict__ tile_mask, int lf) {
   bbox[i] = make_int4(x0, x1, y0, y1);
+  // per-splat margin: maha <= 64 and, with the alpha floor, alpha G >= 2^lf
+  const double M = cull_margin(opacity, lf);
   float gl[kGeom];
-  make_geom(ux, uy, i0, i1, i2, gl);
+  make_geom(ux, uy, i0, i1, i2, fmax(M, 0.0), gl);
   float* gm = geom + (int64_t)i * kGeom;
 #pragma unroll
   for (int c = 0; c < kGeom; ++c) gm[c] = gl[c];
   int nt = 0;
   uint64_t mask = 0;
-  if (x1 > x0 && y1 > y0) {
-    // tiles of the bbox that the maha <= 64 ellipse actually reaches (one
+  if (x1 > x0 && y1 > y0 && M > 0.0) {
+    // tiles of the bbox that the m <= M ellipse actually reaches (one
     // x-interval per tile row); the first 64 (row-major in the bbox tile
     // rectangle) are also recorded as a bit mask for the binning
     const int4 bb = make_int4(x0, x1, y0, y1);
@@ -172,7 +174,7 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
                                    float4* __restrict__ rec_b, float* __restrict__ rec_c,
                                    uint64_t* __restrict__ depth_key, int4* __restrict__ bbox,
                                    int32_t* __restrict__ n_tiles, float* __restrict__ geom,
-                                   uint64_t* __restrict__ tile_mask) {
+                                   uint64_t* __restrict__ tile_mask, int lf) {
   pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -199,7 +201,7 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
   // z > 0.01: the fp64 bits are monotone
   write_record(i, p.ux, p.uy, i0, i1, i2, x0, x1, y0, y1, g.opacity, g.color,
                (uint64_t)__double_as_longlong(p.z), rec_a, rec_b, rec_c, depth_key, bbox, n_tiles,
-               geom, tile_mask);
+               geom, tile_mask, lf);
 }
 
 // _kernels.blend_forward's inputs (already projected 2D splats, the blend
@@ -212,7 +214,7 @@ __global__ void records2d_kernel(const double* __restrict__ mean2d, const double
                                  float4* __restrict__ rec_b, float* __restrict__ rec_c,
                                  uint64_t* __restrict__ depth_key, int4* __restrict__ bbox,
                                  int32_t* __restrict__ n_tiles, float* __restrict__ geom,
-                                 uint64_t* __restrict__ tile_mask) {
+                                 uint64_t* __restrict__ tile_mask, int lf) {
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -226,7 +228,7 @@ __global__ void records2d_kernel(const double* __restrict__ mean2d, const double
                x0, max(x0, x1), y0, max(y0, y1), alpha[i], color + 3 * i,
                // rank as a positive double key (same form as fp64 z bits)
                (uint64_t)__double_as_longlong(1.0 + (double)rank[i] * 0x1p-22), rec_a,
-               rec_b, rec_c, depth_key, bbox, n_tiles, geom, tile_mask);
+               rec_b, rec_c, depth_key, bbox, n_tiles, geom, tile_mask, lf);
 }
 
 // Basis sums (raster.cu) -> _kernels.blend_backward's 2D gradients, added
@@ -408,7 +410,7 @@ extern "C" int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_
   StoreView sv{store->opt, store->n_opt, store->mat};
   launch_k(project_fwd_kernel, grid_for(n, 128), 128, 0, stream, 
       sv, rows, n, to_camk(cam), (float4*)rec_a, (float4*)rec_b, rec_c, depth_key, (int4*)bbox,
-      n_tiles, geom, tile_mask);
+      n_tiles, geom, tile_mask, (int)alpha_floor_log2());
   return check_launch("ss_project_fwd");
 }
 
@@ -422,7 +424,7 @@ extern "C" int ss_records_2d(const ss_splats2d* sp, int32_t width, int32_t heigh
   launch_k(records2d_kernel, grid_for(sp->n, 128), 128, 0, stream, 
       sp->mean2d, sp->inv2d, sp->alpha, sp->color, (const int4*)sp->bbox, sp->rank, sp->n, width,
       height, (float4*)rec_a, (float4*)rec_b, rec_c, depth_key, (int4*)bbox, n_tiles, geom,
-      tile_mask);
+      tile_mask, (int)alpha_floor_log2());
   return check_launch("ss_records_2d");
 }
 

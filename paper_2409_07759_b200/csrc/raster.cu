@@ -70,18 +70,38 @@ struct WarpStage {
   int g[32];
 };
 
-__device__ __forceinline__ void stage_load(WarpStage& st, int lane, int idx, int end,
-                                           const int32_t* __restrict__ vals,
-                                           const float4* __restrict__ rec_a,
-                                           const float4* __restrict__ rec_b,
-                                           const float* __restrict__ rec_c) {
-  if (idx < end) {
-    const int g = __ldg(vals + idx);
-    st.g[lane] = g;
-    st.a[lane] = __ldg(rec_a + g);
-    st.b[lane] = __ldg(rec_b + g);
-    st.c[lane] = __ldg(rec_c + g);
-  }
+// Whether a record can pass the per-pixel test (kappa m + log2 alpha >=
+// thr, thr = max(64 kappa + log2 alpha, lfloor)) anywhere in the warp's
+// pixel-centre rectangle [x0, x0 + 15] x [y0, y1]: with Q = |kappa| m =
+// A dx^2 + 2 B dx dy + C dy^2 the test is Q <= R, R = min(64 |kappa|,
+// log2 alpha - lfloor), an ellipse; as in the binning's row_span, its
+// x-interval over the rectangle's rows is [L, R] with the extreme points at
+// dy = -+sy clamped into the rows.  Conservative (R inflated by 2^-8
+// relative + 2^-6, ill-conditioned conics always pass): it only decides which
+// entries a warp visits; the per-pixel test decides every contribution.
+// One lane evaluates one staged entry, so a 32-entry batch costs each lane
+// one evaluation (~1 instruction per entry) and the warp then walks only the
+// entries its 128 pixels can use.
+__device__ __forceinline__ bool touches_rect(const float4& a, const float4& b, float x0, float y0,
+                                             float y1, float lfloor) {
+  const float A = -a.z, B = -a.w, C = -b.x;  // kappa < 0: |kappa| conic
+  float R = fminf(-kMahaKappa, b.y - lfloor);
+  if (!(R > 0.f)) return false;
+  R = fmaf(R, 1.00390625f, 0.015625f);
+  const float det = fmaf(A, C, -B * B);
+  if (!(det > 1e-3f * A * C)) return true;  // near-degenerate: no cheap exact test
+  const float rdet = 1.f / det;
+  const float ymax = sqrtf(A * R * rdet);
+  const float lo = fmaxf(y0 - a.y, -ymax), hi = fminf(y1 - a.y, ymax);
+  if (lo > hi) return false;
+  const float sy = B * sqrtf(R * rdet / C);
+  const float cR = clampf(-sy, lo, hi), cL = clampf(sy, lo, hi);
+  const float AR = A * R;
+  const float sR = sqrtf(fmaxf(fmaf(-det * cR, cR, AR), 0.f));
+  const float sL = sqrtf(fmaxf(fmaf(-det * cL, cL, AR), 0.f));
+  const float rA = 1.f / A;
+  const float right = (fmaf(-B, cR, sR)) * rA, left = (fmaf(-B, cL, -sL)) * rA;
+  return (x0 - a.x) <= right && (x0 + (kTile - 1) - a.x) >= left;
 }
 
 // Per (lane, entry) coefficients of kappa m + log2 alpha over the strip.
@@ -90,7 +110,7 @@ struct StripQuad {
 };
 
 __device__ __forceinline__ StripQuad strip_quad(const float4& a, const float4& b, float fx,
-                                                float fy0) {
+                                                float fy0, float lfloor) {
   StripQuad s;
   s.dx = fx - a.x;
   s.dy0 = fy0 - a.y;
@@ -101,16 +121,8 @@ __device__ __forceinline__ StripQuad strip_quad(const float4& a, const float4& b
   s.q0 = fmaf(s.dy0, fmaf(C, s.dy0, B), A) + b.y;
   s.lin = fmaf(2.f * C, s.dy0, B);
   s.quad = C;
-  s.thr = kMahaKappa + b.y;
+  s.thr = fmaxf(kMahaKappa + b.y, lfloor);  // maha <= 64 and alpha G >= 2^lfloor
   return s;
-}
-
-// kappa m + log2 alpha at strip pixel k: q0 + k lin + k^2 quad (k = 0, 1
-// special-cased: no multiply-by-immediate-zero FMAs)
-__device__ __forceinline__ float strip_exp(const StripQuad& s, int k) {
-  if (k == 0) return s.q0;
-  if (k == 1) return (s.q0 + s.lin) + s.quad;
-  return fmaf((float)(k * k), s.quad, fmaf((float)k, s.lin, s.q0));
 }
 
 // The strip's exponents as packed pairs, by forward differences:
@@ -143,7 +155,8 @@ __global__ void __launch_bounds__(kWarpsF * 32)
                       const float* __restrict__ rec_c, int width, int height, int tiles_x,
                       int n_tiles, const int32_t* __restrict__ tile_order,
                       float* __restrict__ img, float* __restrict__ t_final,
-                      int32_t* __restrict__ n_contrib, const int4* __restrict__ pbox = nullptr) {
+                      int32_t* __restrict__ n_contrib, float lfloor,
+                      const int4* __restrict__ pbox = nullptr) {
   pdl_wait();
   pdl_trigger();
   __shared__ WarpStage s_stage[kWarpsF];
@@ -159,6 +172,9 @@ __global__ void __launch_bounds__(kWarpsF * 32)
   const int px = tx * kTile + (lane & 15);
   const int py0 = ty * kTile + sub * 2 * STRIP + (lane >> 4) * STRIP;
   const float fx = (float)px, fy0 = (float)py0;
+  // the warp's pixel-centre rectangle (for the per-entry region test)
+  const float rx0 = (float)(tx * kTile), ry0 = (float)(ty * kTile + sub * 2 * STRIP);
+  const float ry1 = ry0 + (float)(2 * STRIP - 1);
   f2 T[NP], c0[NP], c1[NP], c2[NP];
   int last[STRIP];
 #pragma unroll
@@ -178,17 +194,29 @@ __global__ void __launch_bounds__(kWarpsF * 32)
     for (int p = 0; p < NP; ++p) live |= (lo2(T[p]) >= kTMin) | (hi2(T[p]) >= kTMin);
     if (!__any_sync(0xffffffffu, live)) break;
     __syncwarp();
-    stage_load(st, lane, base + lane, rg.y, vals, rec_a, rec_b, rec_c);
+    bool touch = false;
+    if (base + lane < rg.y) {
+      const int g = __ldg(vals + base + lane);
+      const float4 a = __ldg(rec_a + g), b = __ldg(rec_b + g);
+      st.g[lane] = g;
+      st.a[lane] = a;
+      st.b[lane] = b;
+      st.c[lane] = __ldg(rec_c + g);
+      touch = touches_rect(a, b, rx0, ry0, ry1, lfloor);
+    }
+    // only the entries that can reach this warp's pixels are walked
+    uint32_t todo = __ballot_sync(0xffffffffu, touch);
     __syncwarp();
-    const int cnt = min(32, rg.y - base);
-    for (int j = 0; j < cnt; ++j) {
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
       const float4 a = st.a[j];
       const float4 b = st.b[j];
       const float cb = st.c[j];
-      const StripQuad s = strip_quad(a, b, fx, fy0);
+      const StripQuad s = strip_quad(a, b, fx, fy0, lfloor);
       const int pos = base - rg.x + j + 1;
       // exponents and validity of the whole strip first: a warp skips the
-      // entry when none of its pixels is live and inside the maha <= 64 ellipse
+      // entry when none of its pixels is live and passes the per-pixel test
       f2 e[NP];
       strip_exps<NP>(s, e);
       bool valid[STRIP];
@@ -312,7 +340,7 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
                       int n_tiles, const int32_t* __restrict__ tile_order,
                       const float* __restrict__ dimg, const float* __restrict__ t_final,
                       const int32_t* __restrict__ n_contrib, float* __restrict__ g2d,
-                      DetArgs det, const int4* __restrict__ pbox = nullptr) {
+                      DetArgs det, float lfloor, const int4* __restrict__ pbox = nullptr) {
   pdl_wait();
   pdl_trigger();
   __shared__ int64_t s_epos[kWarps][32];
@@ -328,6 +356,8 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
   const int px = tx * kTile + (lane & 15);
   const int py0 = ty * kTile + sub * 2 * STRIP + (lane >> 4) * STRIP;
   const float fx = (float)px, fy0 = (float)py0;
+  const float rx0 = (float)(tx * kTile), ry0 = (float)(ty * kTile + sub * 2 * STRIP);
+  const float ry1 = ry0 + (float)(2 * STRIP - 1);
   constexpr int NP = STRIP / 2;
   // T: transmittance (after the current entry, walking back to front);
   // nQ = -(suffix colour Q); dimg channels per pixel pair
@@ -376,15 +406,36 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
   for (int end = walk_end; end > rg.x; end -= 32) {
     const int start = max(rg.x, end - 32);
     __syncwarp();
-    stage_load(st, lane, start + lane, end, vals, rec_a, rec_b, rec_c);
-    if (DET && start + lane < end) s_epos[warp][lane] = emit_position(det, st.g[lane], tx, ty);
+    bool touch = false;
+    const bool mine = start + lane < end;
+    if (mine) {
+      const int g = __ldg(vals + start + lane);
+      const float4 a = __ldg(rec_a + g), b = __ldg(rec_b + g);
+      st.g[lane] = g;
+      st.a[lane] = a;
+      st.b[lane] = b;
+      st.c[lane] = __ldg(rec_c + g);
+      touch = touches_rect(a, b, rx0, ry0, ry1, lfloor);
+      if (DET) {
+        const int64_t ep = emit_position(det, g, tx, ty);
+        s_epos[warp][lane] = ep;
+        if (!touch) {  // an entry the warp does not walk: zero partials
+          float* dst = det.partial + (ep * WPT + sub) * 9;
+#pragma unroll
+          for (int c = 0; c < 9; ++c) dst[c] = 0.f;
+        }
+      }
+    }
+    uint32_t todo = __ballot_sync(0xffffffffu, touch);
     __syncwarp();
-    for (int j = end - start - 1; j >= 0; --j) {
+    while (todo) {
+      const int j = 31 - __clz(todo);  // back to front
+      todo &= ~(1u << j);
       const int pos = start - rg.x + j;  // 0-based position in the tile list
       const float4 a = st.a[j];
       const float4 b = st.b[j];
       const float cb = st.c[j];
-      const StripQuad s = strip_quad(a, b, fx, fy0);
+      const StripQuad s = strip_quad(a, b, fx, fy0, lfloor);
       f2 e[NP];
       strip_exps<NP>(s, e);
       bool valid[STRIP];
@@ -502,6 +553,12 @@ __global__ void g2d_reduce_kernel(const float* __restrict__ partial,
   for (int c = 0; c < 9; ++c) dst[c] = acc[c];
 }
 
+// log2 of the alpha floor as the kernels' threshold (-inf: off)
+static float floor_threshold() {
+  const int lf = alpha_floor_log2();
+  return lf ? (float)lf : -INFINITY;
+}
+
 static int g_strip = 4;       // backward strip
 static int g_strip_fwd = 4;   // forward strip
 
@@ -538,7 +595,7 @@ extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const v
 #define SS_FWD(S)                                                                             \
   launch_k(raster_fwd_kernel<S>, blocks, kWarpsF * 32, 0, stream,                                    \
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
-      height, tiles_x, n_tiles, tile_order, img, t_final, n_contrib, nullptr)
+      height, tiles_x, n_tiles, tile_order, img, t_final, n_contrib, floor_threshold(), nullptr)
   if (g_strip_fwd == 8) SS_FWD(8);
   else if (g_strip_fwd == 4) SS_FWD(4);
   else SS_FWD(2);
@@ -560,7 +617,8 @@ static int raster_bwd_launch(const int32_t* ranges, const int32_t* vals, const v
 #define SS_BWD(S, D)                                                                          \
   launch_k(raster_bwd_kernel<S, D>, blocks, kWarps * 32, 0, stream,                                 \
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
-      height, tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d, nullptr)
+      height, tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d, floor_threshold(), \
+      nullptr)
   if (det) {
     if (g_strip == 8) SS_BWD(8, true);
     else if (g_strip == 4) SS_BWD(4, true);
@@ -593,7 +651,7 @@ int raster_fwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_
   const int blocks = (n_tiles * 2 + kWarpsF - 1) / kWarpsF;
   launch_k(raster_fwd_kernel<4, true>, blocks, kWarpsF * 32, 0, stream, 
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
-      tiles_x, n_tiles, tile_order, img, t_final, n_contrib, (const int4*)pbox);
+      tiles_x, n_tiles, tile_order, img, t_final, n_contrib, floor_threshold(), (const int4*)pbox);
   return check_launch("raster_fwd_bbox");
 }
 
@@ -608,7 +666,8 @@ int raster_bwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_
   const DetArgs d{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   launch_k(raster_bwd_kernel<4, false, true>, blocks, kWarps * 32, 0, stream, 
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
-      tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d, (const int4*)pbox);
+      tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d, floor_threshold(),
+      (const int4*)pbox);
   return check_launch("raster_bwd_bbox");
 }
 

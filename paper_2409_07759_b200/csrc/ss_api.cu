@@ -81,6 +81,23 @@ extern "C" int ss_memzero(void* ptr, size_t bytes, cudaStream_t stream) {
   return ss::memzero(ptr, bytes, stream);
 }
 
+// default alpha floor 2^-28 (swings.h ss_set_alpha_floor)
+static std::atomic<int32_t> g_alpha_floor{-28};
+
+namespace ss {
+int32_t alpha_floor_log2() { return g_alpha_floor.load(std::memory_order_relaxed); }
+}  // namespace ss
+
+extern "C" int ss_set_alpha_floor(int32_t log2_floor) {
+  if (log2_floor != 0 && (log2_floor < -126 || log2_floor > -1))
+    return ss::set_error(SS_ERR_INVALID, "ss_set_alpha_floor: %d not in {0} U [-126, -1]",
+                         log2_floor);
+  g_alpha_floor.store(log2_floor, std::memory_order_relaxed);
+  return SS_OK;
+}
+
+extern "C" int32_t ss_get_alpha_floor(void) { return ss::alpha_floor_log2(); }
+
 extern "C" const char* ss_last_error(void) { return ss::g_err; }
 
 extern "C" int ss_version(void) { return 1; }

@@ -85,7 +85,7 @@ __device__ __forceinline__ void quat_to_rot(const double q[4], double r[3][3]) {
 
 // Exact ellipse-vs-tile test (a-4 refinement).  A tile row (pixel-centre
 // rows [Y0, Y1], clipped to the bbox) meets the ellipse m <= M (m = i0 dx^2
-// + 2 i1 dx dy + i2 dy^2, M = kCullMargin) in an x-interval [L, R]: the right
+// + 2 i1 dx dy + i2 dy^2, M = the splat's cull_margin) in an x-interval [L, R]: the right
 // end is max over the row of (-i1 dy + sqrt(i0 M - det dy^2)) / i0, reached at
 // dy = -sy clamped into the row (sy = i1 sqrt(M / (i2 det)), the ellipse's
 // rightmost point), the left end symmetric at +sy; rows beyond |dy| <= ymax =
@@ -98,7 +98,27 @@ __device__ __forceinline__ void quat_to_rot(const double q[4], double r[3][3]) {
 // (pixels beyond it blend nothing), far above the fp32 rounding.
 constexpr float kCullMargin = 64.0625f;
 constexpr double kCullMarginD = 64.0625;
-constexpr int kGeom = 8;  // floats per splat: u, v, i0, i1, det, sy, ymax, 1/i0
+constexpr int kGeom = 8;  // floats per splat: u, v, i0 M, i1, det, sy, ymax, 1/i0
+constexpr double kTwoLn2 = 1.3862943611198906;
+
+int32_t alpha_floor_log2();  // ss_api.cu: 0 (off) or the floor's log2 (ss_set_alpha_floor)
+
+// Per-splat maha margin M of the tile test: the reference's m <= 64 cut
+// (kCullMarginD, 1e-3 margin) or, with the alpha floor 2^lf, also
+// alpha G >= 2^lf, i.e. m <= 2 ln(alpha / 2^lf).  With alpha = f 2^e
+// (frexp, f in [0.5, 1)) and ln f <= f - 1, the bound
+// (2 (f - 1) + 2 ln2 (e - lf)) (1 + 2^-10) + 2^-4 uses IEEE-rounded fp64
+// operations only, so oracle/splat_oracle.py cull_margin reproduces it bit
+// for bit.  M <= 0: the splat reaches no pixel.
+__device__ __forceinline__ double cull_margin(double alpha, int lf) {
+  if (lf == 0) return kCullMarginD;
+  if (!(alpha > 0.0)) return -1.0;
+  int e;
+  const double f = frexp(alpha, &e);
+  double m = dadd(dmul(2.0, dsub(f, 1.0)), dmul(kTwoLn2, (double)(e - lf)));
+  m = dadd(dmul(m, 1.0009765625), 0.0625);
+  return fmin(m, kCullMarginD);
+}
 
 __device__ __forceinline__ float fmr(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float far_(float a, float b) { return __fadd_rn(a, b); }
@@ -108,16 +128,16 @@ __device__ __forceinline__ float clampf(float x, float lo, float hi) {
   return fminf(fmaxf(x, lo), hi);
 }
 
-// geom of a splat from its fp64 centre and conic
+// geom of a splat from its fp64 centre, conic and margin M (> 0)
 __device__ __forceinline__ void make_geom(double ux, double uy, double i0, double i1, double i2,
-                                          float* g) {
+                                          double M, float* g) {
   const double det = __dsub_rn(__dmul_rn(i0, i2), __dmul_rn(i1, i1));
-  const double sy = __dmul_rn(i1, __dsqrt_rn(__ddiv_rn(kCullMarginD, __dmul_rn(i2, det))));
-  const double ymax = __dsqrt_rn(__ddiv_rn(__dmul_rn(kCullMarginD, i0), det));
+  const double sy = __dmul_rn(i1, __dsqrt_rn(__ddiv_rn(M, __dmul_rn(i2, det))));
+  const double ymax = __dsqrt_rn(__ddiv_rn(__dmul_rn(M, i0), det));
   const float fi0 = __double2float_rn(i0);
   g[0] = __double2float_rn(ux);
   g[1] = __double2float_rn(uy);
-  g[2] = fi0;
+  g[2] = __double2float_rn(__dmul_rn(i0, M));
   g[3] = __double2float_rn(i1);
   g[4] = __double2float_rn(det);
   g[5] = __double2float_rn(sy);
@@ -128,11 +148,10 @@ __device__ __forceinline__ void make_geom(double ux, double uy, double i0, doubl
 // x-interval [L, R] (relative to u) of the ellipse within tile row ty;
 // false when the row misses the ellipse.  bb = pixel bbox (x0, x1, y0, y1).
 __device__ __forceinline__ bool row_span(const float* g, int ty, int4 bb, float& L, float& R) {
-  const float v = g[1], i0 = g[2], i1 = g[3], det = g[4], sy = g[5], ymax = g[6], r0 = g[7];
+  const float v = g[1], m0 = g[2], i1 = g[3], det = g[4], sy = g[5], ymax = g[6], r0 = g[7];
   const float lo = fmaxf(fsr((float)max(ty * SS_TILE, bb.z), v), -ymax);
   const float hi = fminf(fsr((float)min(ty * SS_TILE + SS_TILE - 1, bb.w - 1), v), ymax);
   if (lo > hi) return false;
-  const float m0 = fmr(i0, kCullMargin);
   const float cR = clampf(-sy, lo, hi), cL = clampf(sy, lo, hi);
   const float sR = __fsqrt_rn(fmaxf(fsr(m0, fmr(fmr(det, cR), cR)), 0.0f));
   const float sL = __fsqrt_rn(fmaxf(fsr(m0, fmr(fmr(det, cL), cL)), 0.0f));

@@ -86,6 +86,25 @@ def set_deterministic(flag: bool = True) -> None:
     pipeline().deterministic = bool(flag)
 
 
+def set_alpha_floor(log2_floor: int | None = -28) -> None:
+    """Alpha floor of the binning and rasterizer (ss_set_alpha_floor): blend
+    a (splat, pixel) pair only when maha <= 64 (_kernels.py:39-41) and
+    alpha G >= 2^log2_floor; each skipped contribution is below the floor,
+    so images stay within ~2 |skipped| 2^floor of the reference (<= 3e-5 at
+    the default -28).  None: the reference's rule alone."""
+    from . import _lib as L
+
+    v = 0 if log2_floor is None else int(log2_floor)
+    L.check(L.lib().ss_set_alpha_floor(v), "set_alpha_floor")
+
+
+def get_alpha_floor() -> int | None:
+    from . import _lib as L
+
+    v = int(L.lib().ss_get_alpha_floor())
+    return None if v == 0 else v
+
+
 def set_binning(mode: str = "counting") -> None:
     """Tile binning used by the forward: "counting" (default; chunked
     histograms + stable scatter, ss_bin_tiles) or "sort" (emit pairs + stable

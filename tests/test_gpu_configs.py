@@ -70,8 +70,9 @@ def _train_view(ss, n, ocam, seed):
     img = R.render_arrays(cam, arr).pixels
     st = R.pipeline().state()
     cache = O.project_arrays(ocam, arr.means, arr.quats, arr.scales, arr.opacities, arr.colors)
-    bins = O.tile_bins(cache, cam.width, cam.height)
-    _structural(st, cache, bins)
+    _structural(st, cache, O.tile_bins(cache, cam.width, cam.height,
+                                       floor_log2=R.get_alpha_floor()))
+    bins = O.tile_bins(cache, cam.width, cam.height, floor_log2=None)  # the reference's walk
     th = O.default_threads()
     ref = O.blend_forward_tiled(cache, cam.height, cam.width, nthreads=th, bins=bins)
     err = np.abs(img - ref["image"]).max()
@@ -127,8 +128,9 @@ def test_config5_orbit_view_player(ss):
     cache = O.project_arrays(ocam, arr.means, arr.quats, arr.scales, arr.opacities, arr.colors)
     # ~12 % of the 1M rows are resampled duplicates of frame-0 splats (equal
     # z): their order is decided by the index tie-break alone
-    bins = O.tile_bins(cache, cam.width, cam.height)
-    _structural(st, cache, bins)
+    _structural(st, cache, O.tile_bins(cache, cam.width, cam.height,
+                                       floor_log2=R.get_alpha_floor()))
+    bins = O.tile_bins(cache, cam.width, cam.height, floor_log2=None)
     ref = O.blend_forward_tiled(cache, cam.height, cam.width, nthreads=O.default_threads(),
                                 bins=bins)
     err = np.abs(img - ref["image"]).max()

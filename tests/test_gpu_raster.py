@@ -82,12 +82,15 @@ def test_structural_bit_exact(ss, case):
 
 
 def _tile_check(P, R, cam, arrays, ocam):
-    """GPU tile pairs/ranges == oracle restatement of a-4 (bit-exact)."""
+    """GPU tile pairs/ranges == oracle restatement of a-4 (bit-exact, with the
+    library's alpha floor).  Returns the EXACT reference bins (maha <= 64
+    rule alone) for the pixel oracles: images and gradients are checked
+    against the reference's own per-pixel walk."""
     R.render_arrays(cam, arrays)
     st = R.pipeline().state()
     cache = O.project_arrays(ocam, arrays.means, arrays.quats, arrays.scales, arrays.opacities,
                              arrays.colors)
-    bins = O.tile_bins(cache, cam.width, cam.height)
+    bins = O.tile_bins(cache, cam.width, cam.height, floor_log2=R.get_alpha_floor())
     assert st["n_pairs"] == bins["K"]
     keys = st["keys"].numpy().astype(np.int64)
     vals = st["vals"].numpy().astype(np.int64)
@@ -100,7 +103,7 @@ def _tile_check(P, R, cam, arrays, ocam):
     got = rg.copy()
     got[got[:, 0] == got[:, 1]] = 0
     assert np.array_equal(got, ref_rg)
-    return cache, bins, st
+    return cache, O.tile_bins(cache, cam.width, cam.height, floor_log2=None), st
 
 
 @pytest.mark.parametrize("case", ["arc400", "rot1k", "saturate"])
@@ -480,3 +483,57 @@ def test_concurrent_views_from_two_threads(ss):
     for t in range(2):
         for i in range(t, 4, 2):
             assert torch.equal(out[t][i], ref[i]), (t, i)
+
+
+def test_alpha_floor_off_reproduces_reference_rule(ss):
+    """ss_set_alpha_floor(0): tile lists are the maha <= 64 rule alone
+    (bit-exact vs the oracle's exact bins); with the default floor the lists
+    shrink and the image / gradients stay within tolerance of the same
+    reference walk."""
+    P, R = ss
+    arr = _synth_scene(P, 20_000, (300.0 / 30_000) ** (1 / 3), seed=8)
+    ocam = arc_camera(2, 5, 256, 192)
+    cam = cam_from(P, ocam)
+    gdir = np.random.default_rng(9).normal(size=(192, 256, 3))
+    default = R.get_alpha_floor()
+    assert default == O.ALPHA_FLOOR_LOG2
+    out = {}
+    try:
+        for floor in (None, default):
+            R.set_alpha_floor(floor)
+            assert R.get_alpha_floor() == floor
+            cache, bins, st = _tile_check(P, R, cam, arr, ocam)
+            img = R.render_arrays(cam, arr).pixels
+            g = R.render_arrays_backward(cam, arr, gdir)
+            out[floor] = (st["n_pairs"], img, g)
+    finally:
+        R.set_alpha_floor(default)
+    ref = O.blend_forward_tiled(cache, cam.height, cam.width, nthreads=8, bins=bins)
+    gref = O.projection_backward(ocam, cache, len(arr), *O.blend_backward_tiled(
+        cache, bins, cam.height, cam.width, gdir, nthreads=8))
+    assert out[None][0] == bins["K"] > out[default][0]
+    for floor in (None, default):
+        assert np.abs(out[floor][1] - ref["image"]).max() <= IMG_TOL
+        grad_check(out[floor][2], gref, what=f"floor {floor}")
+
+
+def test_alpha_floor_error_bound_on_deep_translucent_stack(ss):
+    """Worst case for the floor: 4000 wide, faint (alpha 0.02) splats stacked
+    over the same pixels, so pixels never saturate and every one of them
+    skips hundreds of sub-floor fringe contributions; the image still stays
+    within 1e-4 of the reference's exact walk."""
+    P, R = ss
+    rng = np.random.default_rng(17)
+    n = 4000
+    means = np.stack([rng.normal(0, 0.08, n), rng.normal(0, 0.06, n), rng.uniform(2.0, 4.0, n)], 1)
+    scales = np.exp(rng.uniform(np.log(0.01), np.log(0.05), size=(n, 3)))
+    arr = P.GaussianArrays(means, random_unit_quats(rng, n), scales, np.full(n, 0.02),
+                           rng.uniform(0.2, 1.0, (n, 3)))
+    from conftest import Cam
+    ocam = Cam(160, 128, 300.0, 300.0, 80.0, 64.0, np.eye(3), np.zeros(3))
+    cam = cam_from(P, ocam)
+    cache, bins, st = _tile_check(P, R, cam, arr, ocam)
+    ref = O.blend_forward_tiled(cache, cam.height, cam.width, nthreads=8, bins=bins)
+    assert ref["t_final"].min() > 1e-4      # nothing saturates
+    img = R.render_arrays(cam, arr).pixels
+    assert np.abs(img - ref["image"]).max() <= IMG_TOL

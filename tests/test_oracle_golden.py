@@ -52,13 +52,16 @@ def test_backward_matches_reference(case):
             assert np.all(g[k][~tr] == 0.0)
 
 
-def test_tile_bins_reproduce_reference_order():
+@pytest.mark.parametrize("floor", [None, O.ALPHA_FLOOR_LOG2])
+def test_tile_bins_reproduce_reference_order(floor):
     """a-4: walking a tile's list visits the tile's splats in the reference's
-    global (z, src) order restricted to that tile."""
+    global (z, src) order restricted to that tile; a dropped splat has
+    maha > 64 (or, with the alpha floor, alpha G < 2^floor) at every pixel
+    of the tile."""
     d = load_golden("raster_rot1k")
     cam = golden_cam(d)
     cache = O.project_arrays(cam, *_arrays(d))
-    bins = O.tile_bins(cache, cam.width, cam.height)
+    bins = O.tile_bins(cache, cam.width, cam.height, floor_log2=floor)
     order = cache["order"]
     rank = np.empty(len(order), np.int64)
     rank[order] = np.arange(len(order))
@@ -81,7 +84,11 @@ def test_tile_bins_reproduce_reference_order():
         for sidx in dropped:
             dx, dy = xs - m2[sidx, 0], ys - m2[sidx, 1]
             mm = inv[sidx, 0] * dx * dx + 2 * inv[sidx, 1] * dx * dy + inv[sidx, 2] * dy * dy
-            assert mm.min() > 64.0
+            if floor is None:
+                assert mm.min() > 64.0
+            else:
+                ag = cache["alpha"][sidx] * np.exp(-0.5 * mm)
+                assert np.all((mm > 64.0) | (ag < 2.0 ** floor))
     assert bins["K"] == len(bins["keys"]) and np.all(np.diff(bins["keys"].astype(np.float64)) >= 0)
     assert bins["K"] < loose["K"]
 
