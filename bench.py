@@ -949,7 +949,9 @@ def main():
         train.train_swin(window[0], window[1], state, ds, iterations=args.profile_steps)
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
-        print(json.dumps({"profiled_steps": args.profile_steps, "n_pairs": state.device.pipe.n_pairs}))
+        pipe = state.device.pipe
+        print(json.dumps({"profiled_steps": args.profile_steps, "n_pairs": pipe.n_pairs,
+                          "K_used": pipe.k_used(), "n_active": pipe.n}))
         return
     # raster kernel times come from CUDA events recorded by the native driver
     # on the launch stream around every raster launch INSIDE the timed region

@@ -851,7 +851,7 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
                                                          scratch32, nb);
   // long runs: a run of length L >= 33 sorts in shared memory, or beyond
   // kSmemRun in the 4n u64 region (a run of L at offset 2 run.x pairs)
-  if (int rc2 = ensure_smem((const void*)long_runs_kernel, kSlotLongRuns, kSmemRun * 16)) return rc2;
+  if (int rc2 = ensure_smem((const void*)long_runs_kernel, kSmemRun * 16)) return rc2;
   launch_k(long_runs_kernel, 64, 1024, kSmemRun * 16, stream, depth_key, order, long_runs, scratch32,
                                                          (ulonglong2*)big);
   return check_launch("ss_depth_order");
@@ -958,9 +958,9 @@ int bin_tiles_with_order(const int32_t* order, const int32_t* offsets, const int
   const size_t smem = (size_t)n_tiles * 4;
   const size_t smem_scatter = (size_t)n_tiles * 12;
   int rc;
-  if ((rc = ensure_smem((const void*)bin_emit_kernel, kSlotBinEmit, smem)) ||
-      (rc = ensure_smem((const void*)bin_tile_scan_kernel, kSlotBinTileScan, smem)) ||
-      (rc = ensure_smem((const void*)bin_scatter_kernel, kSlotBinScatter, smem_scatter)))
+  if ((rc = ensure_smem((const void*)bin_emit_kernel, smem)) ||
+      (rc = ensure_smem((const void*)bin_tile_scan_kernel, smem)) ||
+      (rc = ensure_smem((const void*)bin_scatter_kernel, smem_scatter)))
     return rc;
   launch_k(bin_bounds_kernel, (32 * (C + 1) + 127) / 128, 128, 0, stream, offsets, n, C, bounds);
   launch_k(bin_emit_kernel, C, kBinThreads, smem, stream, order, offsets, (const int4*)bbox, geom,

@@ -299,6 +299,65 @@ __device__ __forceinline__ int red9_slot(int lane, bool& valid) {
   return 5 * b4 + p;
 }
 
+// Batched per-entry reduction (the default, non-deterministic backward): a
+// warp parks each blended entry's 32 x 9 lane values in shared memory (one
+// 12-float row per lane: 2 x STS.128 + STS.32) and every kRedE entries
+// reduces them at once -- lane L = 4 e + r sums rows r, r + 4, ..., r + 28 of
+// entry e (8 x 3 LDS, 9 running sums), two transposed shuffle rounds over
+// the entry's 4 lanes leave its 9 totals on those lanes, which add them to
+// g2d.  ~22 instructions per entry instead of the 12-shuffle transposed warp
+// reduction's ~50.  Entry stride 400 words (= 16 mod 32): the 8 lanes of a
+// quarter-warp read 8 distinct 4-bank groups.
+constexpr int kRedE = 8;
+constexpr int kRedRow = 12;                  // floats per lane row (9 used)
+constexpr int kRedStride = 32 * kRedRow + 16;  // floats per entry
+constexpr int kRedWarpFloats = kRedE * kRedStride;
+
+__device__ __forceinline__ void red_park(float* buf, int k, int lane, const float v[9]) {
+  float* row = buf + k * kRedStride + lane * kRedRow;
+  reinterpret_cast<float4*>(row)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(row)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  row[8] = v[8];
+}
+
+__device__ __forceinline__ void red_flush(const float* buf, const int* gid, int nacc, int lane,
+                                          float* __restrict__ g2d) {
+  __syncwarp();
+  const int e = lane >> 2, r = lane & 3;
+  float acc[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) acc[c] = 0.f;
+  if (e < nacc) {
+    const float* base = buf + e * kRedStride + r * kRedRow;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float* row = base + k * 4 * kRedRow;
+      const float4 p = reinterpret_cast<const float4*>(row)[0];
+      const float4 q = reinterpret_cast<const float4*>(row)[1];
+      acc[0] += p.x; acc[1] += p.y; acc[2] += p.z; acc[3] += p.w;
+      acc[4] += q.x; acc[5] += q.y; acc[6] += q.z; acc[7] += q.w;
+      acc[8] += row[8];
+    }
+  }
+  // 9 values over the entry's 4 lanes: 9 -> 5 (xor 2) -> 3 (xor 1)
+  const bool b1 = lane & 2, b0 = lane & 1;
+  float w[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) w[i] = red_round(acc[i], i + 5 < 9 ? acc[i + 5] : 0.f, b1, 2);
+  float x[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) x[i] = red_round(w[i], i + 3 < 5 ? w[i + 3] : 0.f, b0, 1);
+  if (e < nacc) {
+    // lane (b1, b0) holds components 5 b1 + 3 b0 + i, i < 3 (of 9)
+    float* dst = g2d + (int64_t)gid[e] * SS_G2D_ROW + 5 * b1 + 3 * b0;
+    const int cnt = b1 ? (b0 ? 1 : 3) : (b0 ? 2 : 3);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (i < cnt) atomicAdd(dst + i, x[i]);
+  }
+  __syncwarp();
+}
+
 // Deterministic mode (DET): instead of float atomics into g2d, a warp writes
 // its 9 reduced values for an entry to partial[(e * WPT + sub) * 9 + c], where
 // e is the entry's position in emit order (rank-ordered runs per splat, see
@@ -343,8 +402,9 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
                       DetArgs det, float lfloor, const int4* __restrict__ pbox = nullptr) {
   pdl_wait();
   pdl_trigger();
-  __shared__ int64_t s_epos[kWarps][32];
+  __shared__ int64_t s_epos[kWarps][DET ? 32 : 1];
   __shared__ WarpStage s_stage[kWarps];
+  extern __shared__ __align__(16) float s_red[];  // !DET: kWarps x (entry rows + ids)
   constexpr int WPT = kTile / (2 * STRIP);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gwarp = blockIdx.x * kWarps + warp;
@@ -394,6 +454,9 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
   const int walk_end = rg.x + __reduce_max_sync(0xffffffffu, my_max);
   bool slot_ok;
   const int slot = red9_slot(lane, slot_ok);
+  float* rbuf = s_red + warp * (kRedWarpFloats + kRedE);
+  int* rgid = reinterpret_cast<int*>(rbuf + kRedWarpFloats);
+  int nacc = 0;  // entries parked in rbuf (warp-uniform)
   if (DET) {
     // entries this warp never visits contribute zero partials
     for (int idx = walk_end + lane; idx < rg.y; idx += 32) {
@@ -516,13 +579,20 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
       v[6] = -(lo2(nsc0) + hi2(nsc0));
       v[7] = -(lo2(nsc1) + hi2(nsc1));
       v[8] = -(lo2(nsc2) + hi2(nsc2));
-      const float tot = reduce9(v, lane);
-      if (slot_ok) {
-        if (DET) det.partial[(s_epos[warp][j] * WPT + sub) * 9 + slot] = tot;
-        else atomicAdd(g2d + (int64_t)st.g[j] * SS_G2D_ROW + slot, tot);
+      if (DET) {
+        const float tot = reduce9(v, lane);
+        if (slot_ok) det.partial[(s_epos[warp][j] * WPT + sub) * 9 + slot] = tot;
+      } else {
+        red_park(rbuf, nacc, lane, v);
+        if (lane == 0) rgid[nacc] = st.g[j];
+        if (++nacc == kRedE) {
+          red_flush(rbuf, rgid, nacc, lane, g2d);
+          nacc = 0;
+        }
       }
     }
   }
+  if (!DET && nacc > 0) red_flush(rbuf, rgid, nacc, lane, g2d);
 }
 
 __global__ void rank_kernel(const int32_t* __restrict__ order, int n, int32_t* __restrict__ rank) {
@@ -558,6 +628,9 @@ static float floor_threshold() {
   const int lf = alpha_floor_log2();
   return lf ? (float)lf : -INFINITY;
 }
+
+// dynamic shared memory of the non-deterministic backward (reduction rows)
+constexpr size_t kBwdSmem = sizeof(float) * kWarps * (kRedWarpFloats + kRedE);
 
 static int g_strip = 4;       // backward strip
 static int g_strip_fwd = 4;   // forward strip
@@ -614,11 +687,15 @@ static int raster_bwd_launch(const int32_t* ranges, const int32_t* vals, const v
   const int wpt = kTile / (2 * g_strip);
   const int blocks = (n_tiles * wpt + kWarps - 1) / kWarps;
   DetArgs d = det ? *det : DetArgs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int rc = 0;
 #define SS_BWD(S, D)                                                                          \
-  launch_k(raster_bwd_kernel<S, D>, blocks, kWarps * 32, 0, stream,                                 \
-      (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
-      height, tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d, floor_threshold(), \
-      nullptr)
+  do {                                                                                        \
+    if (!D && (rc = ensure_smem((const void*)raster_bwd_kernel<S, D>, kBwdSmem))) return rc;   \
+    launch_k(raster_bwd_kernel<S, D>, blocks, kWarps * 32, D ? 0 : kBwdSmem, stream,           \
+        (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, \
+        height, tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d,              \
+        floor_threshold(), nullptr);                                                          \
+  } while (0)
   if (det) {
     if (g_strip == 8) SS_BWD(8, true);
     else if (g_strip == 4) SS_BWD(4, true);
@@ -664,7 +741,8 @@ int raster_bwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_
   const int n_tiles = tiles_x * tiles_y;
   const int blocks = (n_tiles * 2 + kWarps - 1) / kWarps;
   const DetArgs d{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  launch_k(raster_bwd_kernel<4, false, true>, blocks, kWarps * 32, 0, stream, 
+  if (int rc = ensure_smem((const void*)raster_bwd_kernel<4, false, true>, kBwdSmem)) return rc;
+  launch_k(raster_bwd_kernel<4, false, true>, blocks, kWarps * 32, kBwdSmem, stream, 
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
       tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d, floor_threshold(),
       (const int4*)pbox);

@@ -53,24 +53,31 @@ int memzero(void* p, size_t bytes, cudaStream_t stream) {
 
 // Per (device, kernel) high-water mark of the dynamic shared-memory attribute.
 constexpr int kAttrDevs = 64;
-static std::atomic<size_t> g_smem_attr[kAttrDevs][kSmemSlots];
+constexpr int kAttrKernels = 32;
+struct SmemMark {
+  const void* kernel;
+  size_t bytes;
+};
+static SmemMark g_smem_attr[kAttrDevs][kAttrKernels];
+static std::mutex g_smem_mu;
 
-int ensure_smem(const void* kernel, int slot, size_t bytes) {
-  if (bytes <= 48 * 1024) return SS_OK;  // below the default limit
+int ensure_smem(const void* kernel, size_t bytes) {
+  if (bytes == 0) return SS_OK;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kAttrDevs || slot < 0 ||
-      slot >= kSmemSlots)
-    return set_error(SS_ERR_CUDA, "ensure_smem: bad device or slot");
-  std::atomic<size_t>& hw = g_smem_attr[dev][slot];
-  if (bytes <= hw.load(std::memory_order_acquire)) return SS_OK;
-  // slow path serialised: the attribute and the mark only ever grow together
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  if (bytes <= hw.load(std::memory_order_relaxed)) return SS_OK;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kAttrDevs)
+    return set_error(SS_ERR_CUDA, "ensure_smem: bad device");
+  std::lock_guard<std::mutex> lock(g_smem_mu);
+  SmemMark* marks = g_smem_attr[dev];
+  int i = 0;
+  while (i < kAttrKernels && marks[i].kernel && marks[i].kernel != kernel) ++i;
+  if (i == kAttrKernels) return set_error(SS_ERR_CUDA, "ensure_smem: too many kernels");
+  if (marks[i].kernel == kernel && bytes <= marks[i].bytes) return SS_OK;
+  // the attribute and the mark only ever grow together (under the lock)
   if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
       cudaSuccess)
     return check_launch("ensure_smem");
-  hw.store(bytes, std::memory_order_release);
+  marks[i].kernel = kernel;
+  marks[i].bytes = bytes;
   return SS_OK;
 }
 

@@ -270,9 +270,7 @@ int bin_tiles_with_order(const int32_t* order, const int32_t* offsets, const int
 namespace ss {
 int memzero(void* p, size_t bytes, cudaStream_t stream);  // ss_api.cu: PDL zero fill
 // ss_api.cu: raise `kernel`'s dynamic shared-memory limit to at least `bytes`
-// on the CURRENT device (the attribute is per device).  `slot` names the
-// kernel (one of kSmemSlots); thread-safe, one driver call per (device, slot,
-// larger size).
-enum SmemSlot { kSlotLongRuns = 0, kSlotBinEmit, kSlotBinTileScan, kSlotBinScatter, kSmemSlots };
-int ensure_smem(const void* kernel, int slot, size_t bytes);
+// on the CURRENT device (the attribute is per device); thread-safe, one
+// driver call per (device, kernel, larger size).
+int ensure_smem(const void* kernel, size_t bytes);
 }

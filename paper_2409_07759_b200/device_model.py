@@ -109,7 +109,6 @@ class DeviceModel:
         self.row_expire = torch.zeros(n_rows_all, dtype=torch.int32, device=dev)
         self.blk_map = torch.zeros(self.n_blocks, dtype=torch.int32, device=dev)
         self.active_rows = torch.empty(n_rows_all, dtype=torch.int32, device=dev)
-        self._active_cache = {}  # frame -> (rows, n, n_opt), valid while lifespans hold
         self.counts = torch.zeros(2, dtype=torch.int32, device=dev)
         lib = L.lib()
         self.ws_compact = torch.empty(int(lib.ss_compact_workspace_bytes(n_rows_all)),
@@ -149,7 +148,6 @@ class DeviceModel:
             self.dirty = False
             return
         self._life_sig = sig
-        self._active_cache = {}
         sl, n_opt = self.sl, self.num_gs
         for i, gen in enumerate(self.state.slices):
             self.row_start[i * sl:(i + 1) * sl].fill_(gen.lifespan.start)
@@ -213,11 +211,6 @@ class DeviceModel:
         state, sl = self.state, self.sl
         if self.dirty:
             self.sync_lifespans()
-        hit = self._active_cache.get(frame)
-        if hit is not None:
-            # lifespans unchanged since this frame was compacted (the cache is
-            # dropped whenever they change): same rows, no kernel launches
-            return hit
         live = lambda ls: ls.start <= frame < ls.expire  # noqa: E731
         n_opt = sl * sum(live(g.lifespan) for g in state.slices)
         n_mat = sl * sum(live(m.lifespan) for m in state.matured)
@@ -228,11 +221,9 @@ class DeviceModel:
                                       L.ptr(self.ws_compact), self.ws_compact.numel(),
                                       L.stream_ptr()), "compact_active")
         n = n_opt + n_mat
-        rows = self.active_rows[: max(n, 1)].clone()
-        if len(self._active_cache) >= 64:
-            self._active_cache.pop(next(iter(self._active_cache)))
-        self._active_cache[frame] = (rows, n, n_opt)
-        return rows, n, n_opt
+        # recomputed every view, as the reference does (train.py:380-386);
+        # the buffer is rewritten, in stream order, by the next view's call
+        return self.active_rows[: max(n, 1)], n, n_opt
 
     # ------------------------------------------------------------------ step
     def train_step(self, draws, rank, dataset, it):

@@ -518,7 +518,7 @@ def test_alpha_floor_off_reproduces_reference_rule(ss):
 
 
 def test_alpha_floor_error_bound_on_deep_translucent_stack(ss):
-    """Worst case for the floor: 4000 wide, faint (alpha 0.02) splats stacked
+    """Worst case for the floor: 4000 wide, faint (alpha 0.002) splats stacked
     over the same pixels, so pixels never saturate and every one of them
     skips hundreds of sub-floor fringe contributions; the image still stays
     within 1e-4 of the reference's exact walk."""
@@ -527,7 +527,7 @@ def test_alpha_floor_error_bound_on_deep_translucent_stack(ss):
     n = 4000
     means = np.stack([rng.normal(0, 0.08, n), rng.normal(0, 0.06, n), rng.uniform(2.0, 4.0, n)], 1)
     scales = np.exp(rng.uniform(np.log(0.01), np.log(0.05), size=(n, 3)))
-    arr = P.GaussianArrays(means, random_unit_quats(rng, n), scales, np.full(n, 0.02),
+    arr = P.GaussianArrays(means, random_unit_quats(rng, n), scales, np.full(n, 0.002),
                            rng.uniform(0.2, 1.0, (n, 3)))
     from conftest import Cam
     ocam = Cam(160, 128, 300.0, 300.0, 80.0, 64.0, np.eye(3), np.zeros(3))
