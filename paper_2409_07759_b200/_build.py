@@ -17,6 +17,13 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libswings.so"
 OBJ_DIR = PKG.parent / "build" / "obj"
+# the checked variant: same sources with -DSS_CHECKED, device-side bounds /
+# invariant checks (SS_DCHECK in ss_common.cuh) that trap on violation --
+# the in-house stand-in for compute-sanitizer's memcheck (closed on the GPU
+# pool); tests/test_gpu_checked.py runs scenes through it
+VARIANTS = {"": (LIB, OBJ_DIR, []),
+            "checked": (LIB_DIR / "libswings_checked.so", PKG.parent / "build" / "obj_checked",
+                        ["-DSS_CHECKED"])}
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -40,25 +47,27 @@ def _deps():
     return sorted(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "swings.h"]
 
 
-def needs_build() -> bool:
-    if not LIB.exists():
+def needs_build(variant: str = "") -> bool:
+    lib = VARIANTS[variant][0]
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     return any(p.stat().st_mtime > t for p in _sources() + _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
-        return LIB
-    OBJ_DIR.mkdir(parents=True, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> Path:
+    lib, obj_dir, extra = VARIANTS[variant]
+    if not force and not needs_build(variant):
+        return lib
+    obj_dir.mkdir(parents=True, exist_ok=True)
     LIB_DIR.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
     dep_t = max(p.stat().st_mtime for p in _deps())
 
     def compile_one(src: Path) -> Path:
-        obj = OBJ_DIR / (src.stem + ".o")
+        obj = obj_dir / (src.stem + ".o")
         if force or not obj.exists() or obj.stat().st_mtime < max(src.stat().st_mtime, dep_t):
-            cmd = [cc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+            cmd = [cc, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
             if verbose:
                 print(" ".join(cmd))
             r = subprocess.run(cmd, capture_output=True, text=True)
@@ -70,17 +79,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, _sources()))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [cc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *map(str, objs),
            "-o", str(tmp), "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     import sys
 
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True,
+                variant="checked" if "--checked" in sys.argv else ""))

@@ -10,7 +10,9 @@ from __future__ import annotations
 import ctypes
 from ctypes import POINTER, Structure, c_double, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
 
-from ._build import LIB, build, needs_build
+import os
+
+from ._build import VARIANTS, build, needs_build
 from .core import InvalidParameterError
 
 SS_OK, SS_ERR_INVALID, SS_ERR_CUDA, SS_ERR_CAPACITY, SS_ERR_WORKSPACE = 0, 1, 2, 3, 4
@@ -128,12 +130,14 @@ class SwingsError(RuntimeError):
 
 
 def lib():
-    """Load libswings.so (building it first when sources are newer)."""
+    """Load libswings.so (building it first when sources are newer).
+    SS_LIB_VARIANT=checked loads the bounds-checked build instead."""
     global _LIB
     if _LIB is None:
-        if needs_build():
-            build()
-        handle = ctypes.CDLL(str(LIB))
+        variant = os.environ.get("SS_LIB_VARIANT", "")
+        if needs_build(variant):
+            build(variant=variant)
+        handle = ctypes.CDLL(str(VARIANTS[variant][0]))
         for name, (args, res) in _SIGNATURES.items():
             fn = getattr(handle, name)
             fn.argtypes = args

@@ -119,6 +119,7 @@ __global__ void depth_scatter_kernel(const uint64_t* __restrict__ key64, int32_t
   if (i >= n) return;
   const uint32_t b = culled ? nb : depth_bucket(k, ~range[0], range[1], nb);
   const int32_t pos = culled ? cbase + __popc(cm & ((1u << lane) - 1u)) : atomicAdd(&cursor[b], 1);
+  SS_DCHECK(pos >= 0 && pos < n);
   order[pos] = i;
   bucket_of[pos] = b;
 }
@@ -545,6 +546,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
         const int bit = nth_set_bit(((uint64_t)mhi << 32) | mlo, j);
         const int r = div_small(bit, srw);
         const int t = (sty0 + r) * tiles_x + stx0 + bit - r * sw;
+        SS_DCHECK(bit >= 0 && bit < 64 && t >= 0 && t < n_tiles && so0 + j < offsets[bounds[gridDim.x]]);
         keys[so0 + j] = (uint16_t)t;
         vals[so0 + j] = si;
         atomicAdd(&s_hist[t], 1);
@@ -583,6 +585,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
         const uint32_t kb2 = __ballot_sync(0xffffffffu, keep);
         if (keep) {
           const int q = e + __popc(kb2 & ((1u << lane) - 1u));
+          SS_DCHECK(t >= 0 && t < n_tiles && q < offsets[bounds[gridDim.x]]);
           keys[q] = (uint16_t)t;
           vals[q] = si;
           atomicAdd(&s_hist[t], 1);
@@ -767,6 +770,8 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(
       // byte sum of the lower warps' counts (each <= 32, sum <= 224 < 256)
       prefix = (int)(((word & below_mask) * 0x0101010101010101ull) >> 56);
       last = warp == 7 || (word >> (8 * (warp + 1))) == 0ull;
+      SS_DCHECK(t >= 0 && t < n_tiles && s_cur[t] + prefix + rin >= start[t] &&
+                s_cur[t] + prefix + rin < (t + 1 < n_tiles ? start[t + 1] : offsets[bounds[gridDim.x]]));
       out[s_cur[t] + prefix + rin] = v;
     }
     __syncthreads();

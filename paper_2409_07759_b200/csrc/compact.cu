@@ -123,6 +123,7 @@ __global__ void compact_scatter(CandMap m, const int32_t* block_offsets, int32_t
       chunk += v;
     }
     int pos = s_base + before + wpre;
+    SS_DCHECK(row < 0 || (pos >= 0 && pos < *total));
     if (row >= 0) out_rows[pos] = row;
     // the thread owning candidate n_opt - 1 publishes #active optimizable
     if (c == m.n_opt - 1) out_counts[1] = pos + (row >= 0 ? 1 : 0);

@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(kWarpsF * 32)
 #pragma unroll
   for (int k = 0; k < STRIP; ++k) last[k] = 0;
   const int2 rg = ranges[tile];
+  SS_DCHECK(rg.x >= 0 && rg.x <= rg.y);
   for (int base = rg.x; base < rg.y; base += 32) {
     bool live = false;
 #pragma unroll
@@ -348,6 +349,7 @@ __device__ __forceinline__ void red_flush(const float* buf, const int* gid, int 
 #pragma unroll
   for (int i = 0; i < 3; ++i) x[i] = red_round(w[i], i + 3 < 5 ? w[i + 3] : 0.f, b0, 1);
   if (e < nacc) {
+    SS_DCHECK(gid[e] >= 0);
     // lane (b1, b0) holds components 5 b1 + 3 b0 + i, i < 3 (of 9)
     float* dst = g2d + (int64_t)gid[e] * SS_G2D_ROW + 5 * b1 + 3 * b0;
     const int cnt = b1 ? (b0 ? 1 : 3) : (b0 ? 2 : 3);
@@ -452,6 +454,7 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
   }
   const int2 rg = ranges[tile];
   const int walk_end = rg.x + __reduce_max_sync(0xffffffffu, my_max);
+  SS_DCHECK(rg.x >= 0 && rg.x <= rg.y && walk_end <= rg.y);
   bool slot_ok;
   const int slot = red9_slot(lane, slot_ok);
   float* rbuf = s_red + warp * (kRedWarpFloats + kRedE);

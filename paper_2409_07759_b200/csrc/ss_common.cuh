@@ -6,6 +6,24 @@
 
 #include "../../include/swings.h"
 
+// Device-side invariant / bounds checks of the checked build (-DSS_CHECKED,
+// lib/libswings_checked.so): a violation prints its site and traps.
+#ifdef SS_CHECKED
+#include <cstdio>
+#define SS_DCHECK(cond)                                                                   \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("SS_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,    \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                \
+      asm volatile("trap;");                                                              \
+    }                                                                                     \
+  } while (0)
+#else
+#define SS_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace ss {
 
 constexpr float kAlphaMax = 0.999f;       // _kernels.py:15

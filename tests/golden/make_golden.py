@@ -15,6 +15,10 @@ Fixtures:
   optim.npz      _optimizer_step / sgld_perturb / relocate with the numpy
                  draws the reference consumed (reference train.py)
   train_tiny.npz a few train_swin iterations on a tiny synthetic scene
+  train_window.npz  genesis -> schedule_expire -> mature(1) -> window [1, 3)
+                 -> mature(2) -> window [2, 4): matured rows in the views,
+                 relocation inside a window, gamma^w < 1 on a surviving
+                 generation (reference train.py:353-506)
   golden_render.npz  the frontend fixture model (golden_decode.json) rendered
                  at frame 3 from golden_camera.json with render_offline
 """
@@ -270,6 +274,56 @@ def make_train_tiny(ref):
     print("train_tiny: ok")
 
 
+def make_train_window(ref):
+    """Reference train_swin past genesis: two window slides with maturation,
+    relocation at it = 0 and 2 of each window and a generation that survives
+    a slide (windows_trained = 1 -> gamma^w = 0.5 on its mean gradients)."""
+    T = ref.train
+    tmp = Path(tempfile.mkdtemp(prefix="golden_window_"))
+    scene, ds = ref.synth.synth_scene(seed=5, total_frames=5, n_views=2, n_gaussians=60,
+                                      out_dir=tmp / "ds", width=28, height=24)
+    cfg = T.TrainConfig(swin_size=2, num_gs=60, genesis_iterations=3, window_iterations=4,
+                        relocate_period=2, rng_seed=13)
+    state = T.init_state(cfg)
+    out = {"cam_count": np.array(ds.n_views)}
+    gts = np.stack([np.stack([ds.load(f, v).pixels for v in range(ds.n_views)])
+                    for f in range(ds.total_frames)])
+    out["gt"] = gts
+    for vi, cam in enumerate(ds.cameras):
+        out[f"cam{vi}_R"] = cam.rotation
+        out[f"cam{vi}_T"] = cam.translation
+        out[f"cam{vi}_f"] = np.array([cam.fx, cam.fy, cam.cx, cam.cy])
+        out[f"cam{vi}_wh"] = np.array([cam.width, cam.height])
+
+    def snap(tag):
+        for gi, g in enumerate(state.slices):
+            for k in T.PARAM_GROUPS:
+                out[f"{tag}_{gi}_{k}"] = g.params[k].copy()
+            out[f"{tag}_t_{gi}"] = np.array(g.adam_t)
+            out[f"{tag}_w_{gi}"] = np.array(g.windows_trained)
+            out[f"{tag}_life_{gi}"] = np.array([g.lifespan.birth, g.lifespan.start,
+                                                g.lifespan.expire])
+        out[f"{tag}_n_matured"] = np.array(len(state.matured))
+        for mi, m in enumerate(state.matured):
+            out[f"{tag}_mat_{mi}_rows"] = np.concatenate(
+                [m.arrays.means, m.arrays.quats, m.arrays.scales, m.arrays.opacities[:, None],
+                 m.arrays.colors], axis=1)
+            out[f"{tag}_mat_{mi}_life"] = np.array([m.lifespan.birth, m.lifespan.start,
+                                                    m.lifespan.expire])
+
+    T.train_swin(0, cfg.swin_size, state, ds)
+    snap("genesis")
+    T.schedule_expire(state)
+    T.mature(1, state, writer=None)
+    T.train_swin(1, 1 + cfg.swin_size, state, ds)
+    snap("w1")
+    T.mature(2, state, writer=None)
+    T.train_swin(2, 2 + cfg.swin_size, state, ds, iterations=3)
+    snap("w2")
+    np.savez_compressed(OUT / "train_window.npz", **out)
+    print("train_window: ok")
+
+
 def make_golden_render(ref):
     fx = Path("/root/reference/pkg/frontend/test/fixtures")
     gens_json = json.loads((fx / "golden_decode.json").read_text())
@@ -377,10 +431,15 @@ def make_abr(ref):
 def main():
     ref = load_reference()
     import ref_splatstream.synth  # noqa: F401
+    if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `train_window`
+        for name in sys.argv[1:]:
+            globals()[f"make_{name}"](ref)
+        return
     make_raster(ref)
     make_loss(ref)
     make_optim(ref)
     make_train_tiny(ref)
+    make_train_window(ref)
     make_golden_render(ref)
     import ref_splatstream.codec  # noqa: F401
     make_codec(ref)

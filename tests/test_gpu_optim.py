@@ -140,3 +140,63 @@ def test_train_swin_matches_reference_tiny(T):
             total += diff.size
             bad += int((diff > 1e-6 * max(1.0, np.abs(ref).max())).sum())
     assert bad <= 0.02 * total, (bad, total)
+
+
+def test_train_window_slides_match_reference(T):
+    """Past genesis (train_window.npz, the reference trainer itself): two
+    window slides with maturation -- views mix optimizable and matured rows
+    -- relocation at it = 0 and 2 of each window, and a surviving generation
+    trained with gamma^w = 0.5 (train.py:353-506).  GPU trainer in the
+    reference's numpy draw order; tolerance as the genesis test (fp32
+    gradients, sign-like early Adam steps)."""
+    import paper_2409_07759_b200 as P
+    from paper_2409_07759_b200.dataset import DeviceVideoDataset
+    from paper_2409_07759_b200.raster import to_u8
+    import torch
+    d = load_golden("train_window")
+    cams = []
+    for v in range(int(d["cam_count"])):
+        w, h = d[f"cam{v}_wh"]
+        fx, fy, cx, cy = d[f"cam{v}_f"]
+        cams.append(P.Camera(int(w), int(h), fx, fy, cx, cy, d[f"cam{v}_R"], d[f"cam{v}_T"]))
+    gts = d["gt"]
+    ds = DeviceVideoDataset(cams, gts.shape[0],
+                            lambda f, v: torch.from_numpy(to_u8(gts[f, v])).cuda())
+    cfg = T.TrainConfig(swin_size=2, num_gs=60, genesis_iterations=3, window_iterations=4,
+                        relocate_period=2, rng_seed=13)
+    state = T.init_state(cfg)
+    state.noise_source = "numpy"
+
+    def check(tag):
+        total = bad = 0
+        for gi, g in enumerate(state.slices):
+            assert g.adam_t == int(d[f"{tag}_t_{gi}"]), (tag, gi)
+            assert g.windows_trained == int(d[f"{tag}_w_{gi}"]), (tag, gi)
+            assert [g.lifespan.birth, g.lifespan.start, g.lifespan.expire] == \
+                d[f"{tag}_life_{gi}"].tolist()
+            for k in GROUPS:
+                got = g.params[k].cpu().numpy()
+                ref = d[f"{tag}_{gi}_{k}"]
+                diff = np.abs(got - ref)
+                assert diff.max() <= 12 * cfg.group_lr(k) + 1e-12, (tag, gi, k, diff.max())
+                total += diff.size
+                bad += int((diff > 1e-6 * max(1.0, np.abs(ref).max())).sum())
+        assert len(state.matured) == int(d[f"{tag}_n_matured"])
+        for mi, m in enumerate(state.matured):
+            a = m.arrays
+            rows = np.concatenate([a.means, a.quats, a.scales, a.opacities[:, None], a.colors], 1)
+            ref = d[f"{tag}_mat_{mi}_rows"]
+            assert np.abs(rows - ref).max() <= 0.05, (tag, mi)
+            assert [m.lifespan.birth, m.lifespan.start, m.lifespan.expire] == \
+                d[f"{tag}_mat_{mi}_life"].tolist()
+        assert bad <= 0.05 * total, (tag, bad, total)
+
+    T.train_swin(0, cfg.swin_size, state, ds)
+    check("genesis")
+    T.schedule_expire(state)
+    T.mature(1, state, writer=None)
+    T.train_swin(1, 1 + cfg.swin_size, state, ds)
+    check("w1")
+    T.mature(2, state, writer=None)
+    T.train_swin(2, 2 + cfg.swin_size, state, ds, iterations=3)
+    check("w2")
