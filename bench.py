@@ -93,7 +93,7 @@ def load_ncu_counters(kernels):
         return None
     keys = ("issue_active_pct", "sm_throughput_pct", "l2_throughput_pct", "l1_throughput_pct",
             "l2_hit_rate_pct", "occupancy_pct", "warp_instructions",
-            "instr_per_walked_warp_entry")
+            "warp_instructions_per_k_used_entry", "k_used")
     return {k: {q: d[k].get(q) for q in keys if q in d[k]} for k in kernels if k in d}
 
 

@@ -302,16 +302,21 @@ __device__ __forceinline__ int red9_slot(int lane, bool& valid) {
 
 // Batched per-entry reduction (the default, non-deterministic backward): a
 // warp parks each blended entry's 32 x 9 lane values in shared memory (one
-// 12-float row per lane: 2 x STS.128 + STS.32) and every kRedE entries
-// reduces them at once -- lane L = 4 e + r sums rows r, r + 4, ..., r + 28 of
-// entry e (8 x 3 LDS, 9 running sums), two transposed shuffle rounds over
-// the entry's 4 lanes leave its 9 totals on those lanes, which add them to
-// g2d.  ~22 instructions per entry instead of the 12-shuffle transposed warp
-// reduction's ~50.  Entry stride 400 words (= 16 mod 32): the 8 lanes of a
-// quarter-warp read 8 distinct 4-bank groups.
-constexpr int kRedE = 8;
-constexpr int kRedRow = 12;                  // floats per lane row (9 used)
-constexpr int kRedStride = 32 * kRedRow + 16;  // floats per entry
+// 12-float row per lane: 2 x STS.128 + STS.32) and every kRedE = 4 entries
+// reduces them at once -- lane L = 8 e + r sums rows r, r + 8, r + 16,
+// r + 24 of entry e (4 x 3 LDS, 9 running sums), three transposed shuffle
+// rounds over the entry's 8 lanes (9 -> 5 -> 3 -> 2 values) leave its 9
+// totals on those lanes, which add them to g2d.  ~26 instructions per entry
+// instead of the 12-shuffle transposed warp reduction's ~50.  The 8 lanes
+// of a quarter-warp read rows r * 12 words apart: 8 distinct 4-bank groups.
+// 6 KB per warp keeps the backward at its register-limited 8 CTAs per SM
+// (8 entries per flush: fewer instructions, but 12.8 KB per warp capped
+// residency at ~3 CTAs).
+constexpr int kRedE = 4;  // (8 measured slower: 0.524 vs 0.509 ms, same box)
+constexpr int kRedLanes = 32 / kRedE;             // lanes per entry in a flush
+static_assert(kRedLanes == 8, "red_flush reduces over 8 lanes (xor 4, 2, 1)");
+constexpr int kRedRow = 12;                       // floats per lane row (9 used)
+constexpr int kRedStride = 32 * kRedRow;          // floats per entry
 constexpr int kRedWarpFloats = kRedE * kRedStride;
 
 __device__ __forceinline__ void red_park(float* buf, int k, int lane, const float v[9]) {
@@ -324,15 +329,15 @@ __device__ __forceinline__ void red_park(float* buf, int k, int lane, const floa
 __device__ __forceinline__ void red_flush(const float* buf, const int* gid, int nacc, int lane,
                                           float* __restrict__ g2d) {
   __syncwarp();
-  const int e = lane >> 2, r = lane & 3;
+  const int e = lane / kRedLanes, r = lane % kRedLanes;
   float acc[9];
 #pragma unroll
   for (int c = 0; c < 9; ++c) acc[c] = 0.f;
   if (e < nacc) {
     const float* base = buf + e * kRedStride + r * kRedRow;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float* row = base + k * 4 * kRedRow;
+    for (int k = 0; k < 32 / kRedLanes; ++k) {
+      const float* row = base + k * kRedLanes * kRedRow;
       const float4 p = reinterpret_cast<const float4*>(row)[0];
       const float4 q = reinterpret_cast<const float4*>(row)[1];
       acc[0] += p.x; acc[1] += p.y; acc[2] += p.z; acc[3] += p.w;
@@ -340,22 +345,27 @@ __device__ __forceinline__ void red_flush(const float* buf, const int* gid, int 
       acc[8] += row[8];
     }
   }
-  // 9 values over the entry's 4 lanes: 9 -> 5 (xor 2) -> 3 (xor 1)
-  const bool b1 = lane & 2, b0 = lane & 1;
+  // 9 values over the entry's 8 lanes: 9 -> 5 (xor 4) -> 3 (xor 2) -> 2 (xor 1)
+  const int b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1, b0 = lane & 1;
   float w[5];
 #pragma unroll
-  for (int i = 0; i < 5; ++i) w[i] = red_round(acc[i], i + 5 < 9 ? acc[i + 5] : 0.f, b1, 2);
+  for (int i = 0; i < 5; ++i) w[i] = red_round(acc[i], i + 5 < 9 ? acc[i + 5] : 0.f, b2, 4);
   float x[3];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) x[i] = red_round(w[i], i + 3 < 5 ? w[i + 3] : 0.f, b0, 1);
+  for (int i = 0; i < 3; ++i) x[i] = red_round(w[i], i + 3 < 5 ? w[i + 3] : 0.f, b1, 2);
+  float y[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) y[i] = red_round(x[i], i + 2 < 3 ? x[i + 2] : 0.f, b0, 1);
   if (e < nacc) {
     SS_DCHECK(gid[e] >= 0);
-    // lane (b1, b0) holds components 5 b1 + 3 b0 + i, i < 3 (of 9)
-    float* dst = g2d + (int64_t)gid[e] * SS_G2D_ROW + 5 * b1 + 3 * b0;
-    const int cnt = b1 ? (b0 ? 1 : 3) : (b0 ? 2 : 3);
+    // lane (b2, b1, b0) holds components 5 b2 + 3 b1 + 2 b0 + i of the 9
+    float* dst = g2d + (int64_t)gid[e] * SS_G2D_ROW + 5 * b2 + 3 * b1 + 2 * b0;
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
-      if (i < cnt) atomicAdd(dst + i, x[i]);
+    for (int i = 0; i < 2; ++i) {
+      const bool ok = (i < (b0 ? 1 : 2)) && (2 * b0 + i < (b1 ? 2 : 3)) &&
+                      (3 * b1 + 2 * b0 + i < (b2 ? 4 : 5));
+      if (ok) atomicAdd(dst + i, y[i]);
+    }
   }
   __syncwarp();
 }

@@ -36,6 +36,42 @@ PIPES = ["smsp__issue_active.avg.pct_of_peak_sustained_active",
          "sm__warps_active.avg.pct_of_peak_sustained_active"]
 
 
+def raster_sha16():
+    import hashlib
+
+    src = ROOT / "paper_2409_07759_b200" / "csrc" / "raster.cu"
+    return hashlib.sha256(src.read_bytes()).hexdigest()[:16]
+
+
+def kernel_table(rep, peak_gbs):
+    """Per-kernel DRAM bytes / duration / achieved GB/s / fraction of the
+    measured HBM peak and issue utilisation from a --set full report."""
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hdr, units = rows[0], rows[1]
+
+    def val(r, w):
+        i = hdr.index(w)
+        try:
+            return float(r[i]) * UNITS.get(units[i], 1.0)
+        except ValueError:
+            return float("nan")
+
+    out = ["| kernel | time (us) | DRAM read+write (MB) | achieved DRAM GB/s | frac of "
+           f"{peak_gbs:.0f} GB/s | issue busy % | SM throughput % | occupancy % |",
+           "|---|---|---|---|---|---|---|---|"]
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")]
+        short = name.split("(")[0].replace("void ", "").replace("ss::", "")[:40]
+        us = val(r, "gpu__time_duration.sum")
+        b = val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")
+        gbs = b / (us * 1e-6) / 1e9
+        out.append(f"| `{short}` | {us:.1f} | {b / 1e6:.1f} | {gbs:.0f} | {gbs / peak_gbs:.3f} | "
+                   f"{val(r, PIPES[0]):.0f} | {val(r, PIPES[9]):.0f} | {val(r, PIPES[13]):.0f} |")
+    return "\n".join(out)
+
+
 def raw_metrics(rep):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
@@ -64,11 +100,15 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--raster", required=True)
     ap.add_argument("--extra", nargs="*", default=[])
+    ap.add_argument("--k-used", type=float, default=None,
+                    help="K_used of the profiled view (bench --profile-steps prints it)")
+    ap.add_argument("--peak", type=float, default=6553.6)
     a = ap.parse_args()
     prof = ROOT / "profiles"
     shutil.copy(a.launches, prof / f"{a.round}_config3_launches.csv")
     m = raw_metrics(a.raster)
     f, b = m["raster_fwd"], m["raster_bwd"]
+    sha = raster_sha16()
     traffic = {k: {"dram_bytes_read": v["dram__bytes_read.sum"],
                    "dram_bytes_write": v["dram__bytes_write.sum"],
                    "duration_us": v["gpu__time_duration.sum"],
@@ -78,8 +118,12 @@ def main():
                    "l2_throughput_pct": v.get("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
                    "l1_throughput_pct": v.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
                    "l2_hit_rate_pct": v.get("lts__t_sector_hit_rate.pct"),
-                   "occupancy_pct": v.get("sm__warps_active.avg.pct_of_peak_sustained_active")}
+                   "occupancy_pct": v.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                   **({"k_used": a.k_used,
+                       "warp_instructions_per_k_used_entry": v["smsp__inst_executed.sum"] / a.k_used}
+                      if a.k_used else {})}
                for k, v in (("raster_fwd", f), ("raster_bwd", b))}
+    traffic["raster_cu_sha16"] = sha
     traffic["source"] = (f"ncu --set full --clock-control none, config 3 (bench.py --profile-steps 1), "
                          f"round {a.round[1:]}; bytes converted from the raw page's units")
     (prof / f"{a.round}_traffic.json").write_text(json.dumps(traffic, indent=1))
@@ -94,6 +138,7 @@ def main():
                 f"{g(PIPES[12]):.0f} | {g(PIPES[13]):.0f} |")
 
     reports = "\n".join(ncu_summary.report(r) for r in [a.raster] + a.extra)
+    tables = "\n\n".join(kernel_table(r, a.peak) for r in [a.raster] + a.extra)
     md = f"""# Round {a.round[1:]} — config 3 profile (DyNeRF-shaped, 300k splats, 1352x1014, B200)
 
 Commands (one B200; each ncu command ran after the same command exited 0 without ncu):
@@ -132,6 +177,14 @@ re-read from L1/L2, hit rate below).
 |---|---|---|---|---|---|
 {row2("raster_fwd", f)}
 {row2("raster_bwd", b)}
+
+## Per-kernel DRAM roofline (ncu --set full, one launch each, config 3)
+
+Achieved DRAM GB/s = (dram__bytes_read + dram__bytes_write) / duration, over
+the measured HBM copy peak (MEASURED_PEAKS.json).  Serialised, cold-cache
+replays: read the fractions, not the absolute times.
+
+{tables}
 
 {reports}
 """
