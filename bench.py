@@ -635,7 +635,9 @@ def run_render_only(args, dp):
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
         return {"profiled_frames": args.profile_steps}
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clocks:
+    from paper_2409_07759_b200.parallel import local_device_index
+
+    with ClockSampler(local_device_index()) as clocks:
         if dp is not None:
             dp.barrier()
         torch.cuda.synchronize()
@@ -909,8 +911,10 @@ def main():
 
         from paper_2409_07759_b200.parallel import init_from_env
 
+        from paper_2409_07759_b200.parallel import local_device_index
+
         dp = init_from_env("nccl")
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        torch.cuda.set_device(local_device_index())
         out = run_render_only(args, dp)
         if rank == 0:
             print(json.dumps(out), flush=True)
@@ -936,7 +940,9 @@ def main():
 
         bwd = args.strip or 4
         _lib.check(_lib.lib().ss_set_raster_strips(args.strip_fwd, bwd), "set_raster_strips")
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2409_07759_b200.parallel import local_device_index
+
+    local = local_device_index()  # LOCAL_RANK wrapped onto the visible GPUs
     torch.cuda.set_device(local)
     world = 1 if dp is None else dp.world_size
     c, scene, ds, state, window = build_workload(args.config, dp, args.init)
