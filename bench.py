@@ -896,10 +896,16 @@ def main():
     ap.add_argument("--strip-fwd", type=int, default=0, help="forward strip only (overrides --strip)")
     ap.add_argument("--init", default="gt", choices=["gt", "random"],
                     help="model state: ground-truth splats (converged proxy) or init_state")
+    ap.add_argument("--binning", default="counting", choices=["counting", "sort"],
+                    help="tile binning: chunked counting sort (default) or emit + radix pair sort")
     ap.add_argument("--no-bracket", dest="bracket", action="store_false",
                     help="skip the random-init bracket measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.impl == "ours" and args.binning != "counting":
+        from paper_2409_07759_b200 import raster
+
+        raster.set_binning(args.binning)
     c = CONFIGS.get(args.config)
     rank = int(os.environ.get("RANK", "0"))
     if args.config == 5:

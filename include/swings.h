@@ -196,6 +196,15 @@ int ss_get_binning(void);
  * floor = 0 disables it (the reference's rule alone).  Valid: 0 or
  * [-126, -1].  Process-wide; set before rendering. */
 int ss_set_alpha_floor(int32_t log2_floor);
+
+/* Write up to 2048 bytes of host memory to device memory, stream-ordered, as
+ * a kernel argument (no copy-engine operation between the library's
+ * kernels; used for the per-step generation table and slot maps). */
+int ss_write_small(void* dst, const void* host_src, size_t bytes, ss_stream_t stream);
+
+/* Host nanoseconds ss_render_fwd spent waiting for the pair count K since
+ * the previous call (diagnostics: host work per view = wall - this). */
+uint64_t ss_poll_wait_ns(void);
 int32_t ss_get_alpha_floor(void);
 
 /* Tiles ordered by list length, longest first (raster scheduling order:

@@ -88,6 +88,8 @@ _SIGNATURES = {
     "ss_set_binning": ([I32], c_int),
     "ss_get_binning": ([], c_int),
     "ss_set_alpha_floor": ([I32], c_int),
+    "ss_write_small": ([P, P, c_size_t, P], c_int),
+    "ss_poll_wait_ns": ([], c_uint64),
     "ss_get_alpha_floor": ([], I32),
     "ss_bin_tiles_workspace_bytes": ([I64, I32], c_size_t),
     "ss_bin_tiles_supported": ([I64, I32], I32),

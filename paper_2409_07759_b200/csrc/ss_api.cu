@@ -1,6 +1,8 @@
 // Error reporting and device queries for the libswings.so C ABI.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <atomic>
 #include <mutex>
@@ -42,6 +44,14 @@ __global__ void memzero_kernel(unsigned char* __restrict__ p, size_t bytes) {
   for (size_t i = h + nv * 16 + tid; i < bytes; i += stride) p[i] = 0;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SS_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 int memzero(void* p, size_t bytes, cudaStream_t stream) {
   if (bytes == 0) return SS_OK;
   size_t blocks = (bytes / 16 + 255) / 256;
@@ -81,7 +91,32 @@ int ensure_smem(const void* kernel, size_t bytes) {
   return SS_OK;
 }
 
+// Small host -> device writes (per-step tables: a few hundred bytes) as a
+// kernel whose argument carries the bytes: no copy-engine operation in the
+// stream, so the surrounding kernels keep their programmatic-dependent-launch
+// overlap (a DMA memcpy between two kernels left a ~15 us bubble).
+constexpr int kSmallMax = 2048;
+struct SmallBlob {
+  unsigned char b[kSmallMax];
+};
+
+__global__ void write_small_kernel(unsigned char* __restrict__ dst, SmallBlob blob, int n) {
+  pdl_wait();
+  pdl_trigger();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = blob.b[i];
+}
+
 }  // namespace ss
+
+extern "C" int ss_write_small(void* dst, const void* host_src, size_t bytes, cudaStream_t stream) {
+  if (bytes > (size_t)ss::kSmallMax || (!dst && bytes) || (!host_src && bytes))
+    return ss::set_error(SS_ERR_INVALID, "ss_write_small: %zu bytes (max %d)", bytes, ss::kSmallMax);
+  if (bytes == 0) return SS_OK;
+  ss::SmallBlob blob;
+  memcpy(blob.b, host_src, bytes);
+  ss::launch_k(ss::write_small_kernel, 1, 256, 0, stream, (unsigned char*)dst, blob, (int)bytes);
+  return ss::check_launch("ss_write_small");
+}
 
 extern "C" int ss_memzero(void* ptr, size_t bytes, cudaStream_t stream) {
   if (!ptr && bytes) return ss::set_error(SS_ERR_INVALID, "ss_memzero: null pointer");

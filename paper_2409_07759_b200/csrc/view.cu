@@ -65,6 +65,12 @@ __global__ void __launch_bounds__(256) sum_kernel(const int32_t* __restrict__ v,
   }
 }
 
+static std::atomic<uint64_t> g_poll_ns{0};
+
+// Host nanoseconds spent waiting for the pair count K since the last call
+// (diagnostics: the host's own per-view work is wall time minus this).
+extern "C" uint64_t ss_poll_wait_ns(void) { return g_poll_ns.exchange(0); }
+
 static void record(void* ev, cudaStream_t stream) {
   if (ev) cudaEventRecord((cudaEvent_t)ev, stream);
 }
@@ -154,6 +160,14 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   const auto arrived = [&]() { return (uint32_t)(*k_poll >> 32) == seq; };
   if (!arrived()) {
     const auto t0 = std::chrono::steady_clock::now();
+    struct PollClock {  // host time spent waiting for K (ss_poll_wait_ns)
+      std::chrono::steady_clock::time_point t0;
+      ~PollClock() {
+        g_poll_ns.fetch_add((uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                std::chrono::steady_clock::now() - t0).count(),
+                            std::memory_order_relaxed);
+      }
+    } poll_clock{t0};
     while (!arrived()) {
 #if defined(__x86_64__) || defined(__i386__)
       __builtin_ia32_pause();  // spin politely (SMT sibling, power)

@@ -32,6 +32,20 @@ COLS = {"mean": (0, 3), "quat": (3, 7), "log_scale": (7, 10), "opacity_logit": (
         "color": (11, 14)}
 
 
+def write_small(dst: torch.Tensor, host: np.ndarray) -> None:
+    """Stream-ordered write of a small host array into device tensor `dst`
+    (ss_write_small: the bytes travel as a kernel argument); falls back to a
+    copy for tables over 2 KB."""
+    host = np.ascontiguousarray(host)
+    if host.nbytes <= 2048:
+        L.check(L.lib().ss_write_small(L.ptr(dst), host.ctypes.data, host.nbytes, L.stream_ptr()),
+                "write_small")
+    else:
+        dst.view(torch.uint8)[: host.nbytes].copy_(
+            torch.from_numpy(host.view(np.uint8)).pin_memory(), non_blocking=True)
+        torch.cuda.current_stream().synchronize()  # the pinned staging buffer is freed after
+
+
 def _views(t: torch.Tensor) -> dict:
     out = {}
     for k, (a, b) in COLS.items():
@@ -113,13 +127,10 @@ class DeviceModel:
         lib = L.lib()
         self.ws_compact = torch.empty(int(lib.ss_compact_workspace_bytes(n_rows_all)),
                                       dtype=torch.uint8, device=dev)
-        # double-buffered pinned generation table: a buffer is rewritten only
-        # after the event recorded behind its previous H2D copy has completed
-        self._gen_bufs = [torch.zeros(swin * GEN_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
-                          for _ in range(2)]
-        self._gen_events = [None, None]
-        self._gen_i = 0
-        self.gen_host = self._gen_bufs[0]
+        # per-step generation table, written to gen_dev through ss_write_small
+        # (a kernel argument: no copy-engine op in the stream, and the host
+        # buffer is free again as soon as the launch returns)
+        self.gen_host = np.zeros(swin, dtype=GEN_DTYPE)
         self.gen_dev = torch.zeros(swin * GEN_DTYPE.itemsize, dtype=torch.uint8, device=dev)
         self.reloc_ws = torch.empty(int(lib.ss_relocate_workspace_bytes(num_gs)),
                                     dtype=torch.uint8, device=dev)
@@ -158,7 +169,7 @@ class DeviceModel:
             self.row_expire[r0:r0 + sl].fill_(mg.lifespan.expire)
         blocks = [mg.block for mg in self.state.matured]
         if blocks:
-            self.blk_map[: len(blocks)].copy_(torch.tensor(blocks, dtype=torch.int32))
+            write_small(self.blk_map, np.asarray(blocks, dtype=np.int32))
         self.dirty = False
 
     def freeze(self, gen):
@@ -180,12 +191,7 @@ class DeviceModel:
 
     def _gen_table(self, stepped):
         cfg = self.cfg
-        self._gen_i ^= 1
-        k = self._gen_i
-        if self._gen_events[k] is not None:
-            self._gen_events[k].synchronize()  # its previous copy has landed
-        self.gen_host = self._gen_bufs[k]
-        tab = self.gen_host.numpy().view(GEN_DTYPE)
+        tab = self.gen_host
         for i, gen in enumerate(self.state.slices):
             e = tab[i]
             if stepped[i]:
@@ -199,10 +205,7 @@ class DeviceModel:
                                if cfg.gradient_scaling else 1.0)
             else:
                 e["active"] = 0
-        self.gen_dev.copy_(self.gen_host, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        self._gen_events[k] = ev
+        write_small(self.gen_dev, tab)
 
     def compact(self, frame: int):
         """Active row ids of `frame` (a-2): optimizable rows of generations in
@@ -306,7 +309,7 @@ class DeviceModel:
         sp = L.stream_ptr()
         uniforms = None
         if state.noise_source == "numpy":
-            tab = self.gen_host.numpy().view(GEN_DTYPE)
+            tab = self.gen_host
             rows = torch.cat([torch.arange(i * self.sl, (i + 1) * self.sl, device=self.dev)
                               for i in range(len(state.slices)) if tab[i]["active"]] or
                              [torch.zeros(0, dtype=torch.int64, device=self.dev)])

@@ -94,9 +94,9 @@ class _DeviceSlots:
         from .engine import Store
 
         L = self.L
-        # pinned staging: a pageable copy would block the host on the stream
-        order_h = self.torch.tensor(order, dtype=self.torch.int32).pin_memory()
-        self.blk_map[: len(order)].copy_(order_h, non_blocking=True)
+        from .device_model import write_small
+
+        write_small(self.blk_map, np.asarray(order, dtype=np.int32))
         L.check(L.lib().ss_compact_active(L.ptr(self.start), L.ptr(self.expire), 0,
                                           self.swin * self.sl, L.ptr(self.blk_map), self.sl, frame,
                                           L.ptr(self.active_rows), L.ptr(self.counts),

@@ -13,7 +13,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2409_07759_b200 import train  # noqa: E402
 
-c, scene, ds, state, window = bench.build_workload(3, None, "gt")
+c, scene, ds, state, window = bench.build_workload(int(sys.argv[1]) if len(sys.argv) > 1 else 3, None, "gt")
 train.train_swin(window[0], window[1], state, ds, iterations=5)
 torch.cuda.synchronize()
 t = time.perf_counter()

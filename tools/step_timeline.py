@@ -26,25 +26,40 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--e2e", action="store_true",
                     help="the bench's e2e arm: ground truth from pinned host memory + loss readback")
+    ap.add_argument("--binning", default="counting", choices=["counting", "sort"])
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
 
     import bench
-    from paper_2409_07759_b200 import train
+    from paper_2409_07759_b200 import raster, train
 
-    c, scene, ds, state, window = bench.build_workload(a.config, None, "gt")
-    progress = None
-    if a.e2e:
-        ds = bench.HostFeed(ds, window, c["views"])
-        progress = bench.LossReadback(state.device)
-    train.train_swin(window[0], window[1], state, ds, iterations=5, progress=progress)
-    torch.cuda.synchronize()
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        train.train_swin(window[0], window[1], state, ds, iterations=a.steps, progress=progress)
-        if progress is not None:
-            progress.flush()
+    raster.set_binning(a.binning)
+
+    if a.config == 5:  # render-only playback frames (bench.run_render_only's path)
+        buf, cams, arr, sl = bench.build_player()
+
+        def run(n):
+            for i in range(n):
+                buf.render_device(cams[i % len(cams)], 0)
+        run(5)
         torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            run(a.steps)
+            torch.cuda.synchronize()
+    else:
+        c, scene, ds, state, window = bench.build_workload(a.config, None, "gt")
+        progress = None
+        if a.e2e:
+            ds = bench.HostFeed(ds, window, c["views"])
+            progress = bench.LossReadback(state.device)
+        train.train_swin(window[0], window[1], state, ds, iterations=5, progress=progress)
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            train.train_swin(window[0], window[1], state, ds, iterations=a.steps, progress=progress)
+            if progress is not None:
+                progress.flush()
+            torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     spans = sorted((e.time_range.start, e.time_range.end, e.name) for e in evs)
     t0, t1 = spans[0][0], max(s[1] for s in spans)
