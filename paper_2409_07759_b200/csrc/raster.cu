@@ -301,71 +301,47 @@ __device__ __forceinline__ int red9_slot(int lane, bool& valid) {
 }
 
 // Batched per-entry reduction (the default, non-deterministic backward): a
-// warp parks each blended entry's 32 x 9 lane values in shared memory (one
-// 12-float row per lane: 2 x STS.128 + STS.32) and every kRedE = 4 entries
-// reduces them at once -- lane L = 8 e + r sums rows r, r + 8, r + 16,
-// r + 24 of entry e (4 x 3 LDS, 9 running sums), three transposed shuffle
-// rounds over the entry's 8 lanes (9 -> 5 -> 3 -> 2 values) leave its 9
-// totals on those lanes, which add them to g2d.  ~26 instructions per entry
-// instead of the 12-shuffle transposed warp reduction's ~50.  The 8 lanes
-// of a quarter-warp read rows r * 12 words apart: 8 distinct 4-bank groups.
-// 6 KB per warp keeps the backward at its register-limited 8 CTAs per SM
-// (8 entries per flush: fewer instructions, but 12.8 KB per warp capped
-// residency at ~3 CTAs).
-constexpr int kRedE = 4;  // (8 measured slower: 0.524 vs 0.509 ms, same box)
-constexpr int kRedLanes = 32 / kRedE;             // lanes per entry in a flush
-static_assert(kRedLanes == 8, "red_flush reduces over 8 lanes (xor 4, 2, 1)");
-constexpr int kRedRow = 12;                       // floats per lane row (9 used)
-constexpr int kRedStride = 32 * kRedRow;          // floats per entry
+// warp parks each blended entry's 32 x 9 lane values in shared memory,
+// component-major (value c of lane l at [entry][c][l]: 9 STS.32 per lane),
+// and every kRedE = 3 entries reduces them at once: lane L < 27 owns the sum
+// (entry L / 9, component L % 9), reads its 32 contiguous lane values with
+// 8 LDS.128, adds them (4 running sums) and issues one float atomic into
+// g2d.  ~22 instructions per entry instead of the 12-shuffle transposed warp
+// reduction's ~50 (and of the earlier lane-major rows + shuffle rounds'
+// ~35).  Component rows are padded to 36 floats and entries are 324 floats
+// apart (= 4 mod 32), so a quarter-warp's LDS.128 hit 8 distinct 4-bank
+// groups.
+constexpr int kRedE = 3;
+constexpr int kRedCompPitch = 36;                  // floats per component row (32 used)
+constexpr int kRedStride = 9 * kRedCompPitch;      // floats per entry
 constexpr int kRedWarpFloats = kRedE * kRedStride;
+static_assert(kRedE * 9 <= 32, "one sum per lane");
+constexpr int kRedWarpTotal = kRedWarpFloats + 4;  // + entry ids; keeps 16-B alignment
+static_assert(kRedWarpFloats % 4 == 0 && kRedE <= 4, "16-B aligned per-warp buffers");
 
 __device__ __forceinline__ void red_park(float* buf, int k, int lane, const float v[9]) {
-  float* row = buf + k * kRedStride + lane * kRedRow;
-  reinterpret_cast<float4*>(row)[0] = make_float4(v[0], v[1], v[2], v[3]);
-  reinterpret_cast<float4*>(row)[1] = make_float4(v[4], v[5], v[6], v[7]);
-  row[8] = v[8];
+  float* col = buf + k * kRedStride + lane;
+#pragma unroll
+  for (int c = 0; c < 9; ++c) col[c * kRedCompPitch] = v[c];
 }
 
 __device__ __forceinline__ void red_flush(const float* buf, const int* gid, int nacc, int lane,
                                           float* __restrict__ g2d) {
   __syncwarp();
-  const int e = lane / kRedLanes, r = lane % kRedLanes;
-  float acc[9];
+  if (lane < 9 * nacc) {
+    const int e = lane / 9, c = lane - 9 * e;
+    const float4* row = reinterpret_cast<const float4*>(buf + e * kRedStride + c * kRedCompPitch);
+    float4 s = row[0];
 #pragma unroll
-  for (int c = 0; c < 9; ++c) acc[c] = 0.f;
-  if (e < nacc) {
-    const float* base = buf + e * kRedStride + r * kRedRow;
-#pragma unroll
-    for (int k = 0; k < 32 / kRedLanes; ++k) {
-      const float* row = base + k * kRedLanes * kRedRow;
-      const float4 p = reinterpret_cast<const float4*>(row)[0];
-      const float4 q = reinterpret_cast<const float4*>(row)[1];
-      acc[0] += p.x; acc[1] += p.y; acc[2] += p.z; acc[3] += p.w;
-      acc[4] += q.x; acc[5] += q.y; acc[6] += q.z; acc[7] += q.w;
-      acc[8] += row[8];
+    for (int k = 1; k < 8; ++k) {
+      const float4 q = row[k];
+      s.x += q.x;
+      s.y += q.y;
+      s.z += q.z;
+      s.w += q.w;
     }
-  }
-  // 9 values over the entry's 8 lanes: 9 -> 5 (xor 4) -> 3 (xor 2) -> 2 (xor 1)
-  const int b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1, b0 = lane & 1;
-  float w[5];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) w[i] = red_round(acc[i], i + 5 < 9 ? acc[i + 5] : 0.f, b2, 4);
-  float x[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) x[i] = red_round(w[i], i + 3 < 5 ? w[i + 3] : 0.f, b1, 2);
-  float y[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) y[i] = red_round(x[i], i + 2 < 3 ? x[i + 2] : 0.f, b0, 1);
-  if (e < nacc) {
     SS_DCHECK(gid[e] >= 0);
-    // lane (b2, b1, b0) holds components 5 b2 + 3 b1 + 2 b0 + i of the 9
-    float* dst = g2d + (int64_t)gid[e] * SS_G2D_ROW + 5 * b2 + 3 * b1 + 2 * b0;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const bool ok = (i < (b0 ? 1 : 2)) && (2 * b0 + i < (b1 ? 2 : 3)) &&
-                      (3 * b1 + 2 * b0 + i < (b2 ? 4 : 5));
-      if (ok) atomicAdd(dst + i, y[i]);
-    }
+    atomicAdd(g2d + (int64_t)gid[e] * SS_G2D_ROW + c, (s.x + s.y) + (s.z + s.w));
   }
   __syncwarp();
 }
@@ -467,7 +443,7 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
   SS_DCHECK(rg.x >= 0 && rg.x <= rg.y && walk_end <= rg.y);
   bool slot_ok;
   const int slot = red9_slot(lane, slot_ok);
-  float* rbuf = s_red + warp * (kRedWarpFloats + kRedE);
+  float* rbuf = s_red + warp * kRedWarpTotal;
   int* rgid = reinterpret_cast<int*>(rbuf + kRedWarpFloats);
   int nacc = 0;  // entries parked in rbuf (warp-uniform)
   if (DET) {
@@ -643,7 +619,7 @@ static float floor_threshold() {
 }
 
 // dynamic shared memory of the non-deterministic backward (reduction rows)
-constexpr size_t kBwdSmem = sizeof(float) * kWarps * (kRedWarpFloats + kRedE);
+constexpr size_t kBwdSmem = sizeof(float) * kWarps * kRedWarpTotal;
 
 static int g_strip = 4;       // backward strip
 static int g_strip_fwd = 4;   // forward strip
