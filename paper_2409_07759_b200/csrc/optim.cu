@@ -73,7 +73,7 @@ __device__ __forceinline__ void sgld_row(double* p, const HyperK& h, const doubl
   }
 }
 
-__global__ void __launch_bounds__(128, 5) adam_sgld_kernel(double* __restrict__ opt, const float* __restrict__ grads,
+__global__ void __launch_bounds__(128, 4) adam_sgld_kernel(double* __restrict__ opt, const float* __restrict__ grads,
                                  double* __restrict__ m, double* __restrict__ v, int64_t n_rows,
                                  int32_t rows_per_gen, const ss_gen_step* __restrict__ gens,
                                  HyperK h, const double* __restrict__ eta) {
@@ -112,20 +112,34 @@ __global__ void __launch_bounds__(128, 5) adam_sgld_kernel(double* __restrict__ 
   } else {
     double2* mr = reinterpret_cast<double2*>(m + r * SS_ROW);
     double2* vr = reinterpret_cast<double2*>(v + r * SS_ROW);
+    // moments in two halves, each half's loads issued together (one memory
+    // round trip per half instead of one per column pair)
 #pragma unroll
-    for (int k2 = 0; k2 < SS_ROW / 2; ++k2) {
-      double2 mm = mr[k2], vv = vr[k2];
-      double mk[2] = {mm.x, mm.y}, vk[2] = {vv.x, vv.y};
+    for (int half = 0; half < 2; ++half) {
+      constexpr int kH = 4;  // column pairs of the first half (7 = 4 + 3)
+      const int b0 = half ? kH : 0, nb = half ? SS_ROW / 2 - kH : kH;
+      double2 mm[kH], vv[kH];
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int k = 2 * k2 + h2;
-        mk[h2] = __dadd_rn(__dmul_rn(mk[h2], h.b1), __dmul_rn(1.0 - h.b1, g[k]));
-        vk[h2] = __dadd_rn(__dmul_rn(vk[h2], h.b2), __dmul_rn(__dmul_rn(1.0 - h.b2, g[k]), g[k]));
-        const double step = ddiv(ddiv(mk[h2], gs.bc1), dadd(sqrt(ddiv(vk[h2], gs.bc2)), h.eps));
-        pv[k] = dsub(pv[k], dmul(h.lr[group[k]], step));
+      for (int q = 0; q < kH; ++q)
+        if (q < nb) {
+          mm[q] = mr[b0 + q];
+          vv[q] = vr[b0 + q];
+        }
+#pragma unroll
+      for (int q = 0; q < kH; ++q) {
+        if (q >= nb) continue;
+        double mk[2] = {mm[q].x, mm[q].y}, vk[2] = {vv[q].x, vv[q].y};
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int k = 2 * (b0 + q) + h2;
+          mk[h2] = __dadd_rn(__dmul_rn(mk[h2], h.b1), __dmul_rn(1.0 - h.b1, g[k]));
+          vk[h2] = __dadd_rn(__dmul_rn(vk[h2], h.b2), __dmul_rn(__dmul_rn(1.0 - h.b2, g[k]), g[k]));
+          const double step = ddiv(ddiv(mk[h2], gs.bc1), dadd(sqrt(ddiv(vk[h2], gs.bc2)), h.eps));
+          pv[k] = dsub(pv[k], dmul(h.lr[group[k]], step));
+        }
+        mr[b0 + q] = make_double2(mk[0], mk[1]);
+        vr[b0 + q] = make_double2(vk[0], vk[1]);
       }
-      mr[k2] = make_double2(mk[0], mk[1]);
-      vr[k2] = make_double2(vk[0], vk[1]);
     }
   }
   // train.py:341-344 projections
