@@ -228,6 +228,8 @@ int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
  * in a fixed order into g2d (all of g2d's n rows are written).  rank: n
  * int32 scratch.  Bit-identical results run to run. */
 int64_t ss_raster_partial_floats(int64_t n_pairs);
+/* Entry-use mask words for K pairs over n_tiles tiles (ss_view.used). */
+int64_t ss_raster_used_words(int64_t n_pairs, int32_t n_tiles);
 int ss_raster_bwd_deterministic(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                                 const void* rec_b, const float* rec_c, int32_t width,
                                 int32_t height, const int32_t* tile_order, const float* dimg,
@@ -342,6 +344,12 @@ typedef struct {
   void* events[4];      /* optional cudaEvent_t: raster fwd start/end, bwd start/end */
   float* partial;       /* deterministic backward: ss_raster_partial_floats(K) floats, */
   int32_t* rank;        /*   and n int32; partial == NULL selects the atomic backward */
+  uint32_t* used;       /* optional entry-use masks, >= ss_raster_used_words(pair_cap, */
+                        /*   tiles) words: the forward records which list entries     */
+                        /*   reached each warp's pixels, the backward walks only those */
+  int64_t used_cap;     /* words in used                                               */
+  int32_t used_ok;      /* out (forward): masks valid for this view's backward         */
+  int32_t pad2;
 } ss_view;
 
 /* Projection -> depth order -> tile offsets -> [one stream sync for K] ->

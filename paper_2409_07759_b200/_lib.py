@@ -58,7 +58,8 @@ class SSView(Structure):
                 ("tile_order", P), ("img", P), ("t_final", P), ("n_contrib", P), ("ws", P),
                 ("ws_bytes", c_size_t), ("ws_needed", c_size_t), ("n_pairs", c_int64),
                 ("sorted_sel", c_int32), ("pad1", c_int32), ("events", P * 4),
-                ("partial", P), ("rank", P)]
+                ("partial", P), ("rank", P), ("used", P), ("used_cap", c_int64),
+                ("used_ok", c_int32), ("pad2", c_int32)]
 
 class SSSplats2D(Structure):
     _fields_ = [("mean2d", P), ("inv2d", P), ("alpha", P), ("color", P), ("bbox", P),
@@ -89,6 +90,7 @@ _SIGNATURES = {
     "ss_get_binning": ([], c_int),
     "ss_set_alpha_floor": ([I32], c_int),
     "ss_write_small": ([P, P, c_size_t, P], c_int),
+    "ss_raster_used_words": ([I64, I32], I64),
     "ss_poll_wait_ns": ([], c_uint64),
     "ss_get_alpha_floor": ([], I32),
     "ss_bin_tiles_workspace_bytes": ([I64, I32], c_size_t),

@@ -104,6 +104,17 @@ __device__ __forceinline__ bool touches_rect(const float4& a, const float4& b, f
   return (x0 - a.x) <= right && (x0 + (kTile - 1) - a.x) >= left;
 }
 
+// Entry-use masks (view driver, strips equal): the forward records, per
+// (tile, 32-entry batch, warp), which batch entries contributed to at least
+// one of the warp's pixels; the backward walks exactly those (its per-pixel
+// validity equals the forward's: a position before a pixel's last
+// contributor was reached with T >= 1e-4).  Batch b of tile t's list
+// (positions rg.x + 32 b ...) has slot floor(rg.x / 32) + t + b: lists lie in
+// tile order, so slots never collide; ss_raster_used_words(K, tiles) words.
+__device__ __forceinline__ int64_t used_slot(int list_start, int tile, int batch) {
+  return (int64_t)(list_start >> 5) + tile + batch;
+}
+
 // Per (lane, entry) coefficients of kappa m + log2 alpha over the strip.
 struct StripQuad {
   float q0, lin, quad, thr, dx, dy0;
@@ -156,7 +167,8 @@ __global__ void __launch_bounds__(kWarpsF * 32)
                       int n_tiles, const int32_t* __restrict__ tile_order,
                       float* __restrict__ img, float* __restrict__ t_final,
                       int32_t* __restrict__ n_contrib, float lfloor,
-                      const int4* __restrict__ pbox = nullptr) {
+                      const int4* __restrict__ pbox = nullptr,
+                      uint32_t* __restrict__ used = nullptr) {
   pdl_wait();
   pdl_trigger();
   __shared__ WarpStage s_stage[kWarpsF];
@@ -207,6 +219,7 @@ __global__ void __launch_bounds__(kWarpsF * 32)
     }
     // only the entries that can reach this warp's pixels are walked
     uint32_t todo = __ballot_sync(0xffffffffu, touch);
+    uint32_t used_bits = 0;  // entries that contributed to one of the warp's pixels
     __syncwarp();
     while (todo) {
       const int j = __ffs(todo) - 1;
@@ -236,6 +249,7 @@ __global__ void __launch_bounds__(kWarpsF * 32)
         any |= valid[2 * p] | valid[2 * p + 1];
       }
       if (!__any_sync(0xffffffffu, any)) continue;
+      used_bits |= 1u << j;
       // branch-free over the strip: invalid pixels get alpha' = 0, which
       // leaves C and T untouched
 #pragma unroll
@@ -251,6 +265,7 @@ __global__ void __launch_bounds__(kWarpsF * 32)
         last[2 * p + 1] = valid[2 * p + 1] ? pos : last[2 * p + 1];
       }
     }
+    if (used && lane == 0) used[used_slot(rg.x, tile, (base - rg.x) >> 5) * WPT + sub] = used_bits;
   }
 #pragma unroll
   for (int k = 0; k < STRIP; ++k) {
@@ -387,7 +402,8 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
                       int n_tiles, const int32_t* __restrict__ tile_order,
                       const float* __restrict__ dimg, const float* __restrict__ t_final,
                       const int32_t* __restrict__ n_contrib, float* __restrict__ g2d,
-                      DetArgs det, float lfloor, const int4* __restrict__ pbox = nullptr) {
+                      DetArgs det, float lfloor, const int4* __restrict__ pbox = nullptr,
+                      const uint32_t* __restrict__ used = nullptr) {
   pdl_wait();
   pdl_trigger();
   __shared__ int64_t s_epos[kWarps][DET ? 32 : 1];
@@ -455,19 +471,25 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
       for (int c = 0; c < 9; ++c) dst[c] = 0.f;
     }
   }
-  for (int end = walk_end; end > rg.x; end -= 32) {
-    const int start = max(rg.x, end - 32);
+  // batches aligned with the forward's (list positions rg.x + 32 b ...),
+  // walked back to front from the one holding walk_end - 1
+  for (int bt = (walk_end - rg.x - 1) >> 5; bt >= 0; --bt) {
+    const int start = rg.x + 32 * bt;
+    const int end = min(start + 32, walk_end);
     __syncwarp();
     bool touch = false;
     const bool mine = start + lane < end;
-    if (mine) {
+    // the forward's entry-use mask, else the per-entry region test
+    const uint32_t umask = used ? used[used_slot(rg.x, tile, bt) * WPT + sub] : ~0u;
+    const bool want = mine && ((umask >> lane) & 1u);
+    if (DET ? mine : want) {
       const int g = __ldg(vals + start + lane);
       const float4 a = __ldg(rec_a + g), b = __ldg(rec_b + g);
       st.g[lane] = g;
       st.a[lane] = a;
       st.b[lane] = b;
       st.c[lane] = __ldg(rec_c + g);
-      touch = touches_rect(a, b, rx0, ry0, ry1, lfloor);
+      touch = want && (used || touches_rect(a, b, rx0, ry0, ry1, lfloor));
       if (DET) {
         const int64_t ep = emit_position(det, g, tx, ty);
         s_epos[warp][lane] = ep;
@@ -645,54 +667,72 @@ extern "C" int ss_set_raster_strips(int32_t strip_fwd, int32_t strip_bwd) {
   return SS_OK;
 }
 
-extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
-                             const void* rec_b, const float* rec_c, int32_t width, int32_t height,
-                             const int32_t* tile_order, float* img, float* t_final,
-                             int32_t* n_contrib, cudaStream_t stream) {
+// Forward launch; pbox != nullptr selects the explicit per-pixel bbox test
+// (strip 4); used != nullptr records the entry-use masks.
+int raster_fwd_ex(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                  const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                  const int32_t* tile_order, float* img, float* t_final, int32_t* n_contrib,
+                  const int32_t* pbox, uint32_t* used, cudaStream_t stream) {
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_raster_fwd: bad size");
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
-  const int wpt = kTile / (2 * g_strip_fwd);
+  const int strip = pbox ? 4 : g_strip_fwd;
+  const int wpt = kTile / (2 * strip);
   const int blocks = (n_tiles * wpt + kWarpsF - 1) / kWarpsF;
-#define SS_FWD(S)                                                                             \
-  launch_k(raster_fwd_kernel<S>, blocks, kWarpsF * 32, 0, stream,                                    \
+#define SS_FWD(S, B)                                                                          \
+  launch_k(raster_fwd_kernel<S, B>, blocks, kWarpsF * 32, 0, stream,                          \
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
-      height, tiles_x, n_tiles, tile_order, img, t_final, n_contrib, floor_threshold(), nullptr)
-  if (g_strip_fwd == 8) SS_FWD(8);
-  else if (g_strip_fwd == 4) SS_FWD(4);
-  else SS_FWD(2);
+      height, tiles_x, n_tiles, tile_order, img, t_final, n_contrib, floor_threshold(),     \
+      (const int4*)pbox, used)
+  if (pbox) SS_FWD(4, true);
+  else if (strip == 8) SS_FWD(8, false);
+  else if (strip == 4) SS_FWD(4, false);
+  else SS_FWD(2, false);
 #undef SS_FWD
   return check_launch("ss_raster_fwd");
 }
 
-static int raster_bwd_launch(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                              const void* rec_b, const float* rec_c, int32_t width, int32_t height,
-                             const int32_t* tile_order, const float* dimg, const float* t_final,
-                             const int32_t* n_contrib, float* g2d, const DetArgs* det,
-                             cudaStream_t stream) {
+                             const int32_t* tile_order, float* img, float* t_final,
+                             int32_t* n_contrib, cudaStream_t stream) {
+  return raster_fwd_ex(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, img, t_final,
+                       n_contrib, nullptr, nullptr, stream);
+}
+
+// Backward launch; det selects the deterministic partials, pbox the bbox
+// test (strip 4), used the forward's entry-use masks (else the region test).
+int raster_bwd_ex(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                  const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                  const int32_t* tile_order, const float* dimg, const float* t_final,
+                  const int32_t* n_contrib, float* g2d, const DetArgs* det, const int32_t* pbox,
+                  const uint32_t* used, cudaStream_t stream) {
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_raster_bwd: bad size");
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
-  const int wpt = kTile / (2 * g_strip);
+  const int strip = pbox ? 4 : g_strip;
+  const int wpt = kTile / (2 * strip);
   const int blocks = (n_tiles * wpt + kWarps - 1) / kWarps;
   DetArgs d = det ? *det : DetArgs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   int rc = 0;
-#define SS_BWD(S, D)                                                                          \
+#define SS_BWD(S, D, B)                                                                       \
   do {                                                                                        \
-    if (!D && (rc = ensure_smem((const void*)raster_bwd_kernel<S, D>, kBwdSmem))) return rc;   \
-    launch_k(raster_bwd_kernel<S, D>, blocks, kWarps * 32, D ? 0 : kBwdSmem, stream,           \
+    if (!D && (rc = ensure_smem((const void*)raster_bwd_kernel<S, D, B>, kBwdSmem))) return rc; \
+    launch_k(raster_bwd_kernel<S, D, B>, blocks, kWarps * 32, D ? 0 : kBwdSmem, stream,        \
         (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, \
         height, tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d,              \
-        floor_threshold(), nullptr);                                                          \
+        floor_threshold(), (const int4*)pbox, used);                                          \
   } while (0)
-  if (det) {
-    if (g_strip == 8) SS_BWD(8, true);
-    else if (g_strip == 4) SS_BWD(4, true);
-    else SS_BWD(2, true);
+  if (pbox) {
+    SS_BWD(4, false, true);
+  } else if (det) {
+    if (strip == 8) SS_BWD(8, true, false);
+    else if (strip == 4) SS_BWD(4, true, false);
+    else SS_BWD(2, true, false);
   } else {
-    if (g_strip == 8) SS_BWD(8, false);
-    else if (g_strip == 4) SS_BWD(4, false);
-    else SS_BWD(2, false);
+    if (strip == 8) SS_BWD(8, false, false);
+    else if (strip == 4) SS_BWD(4, false, false);
+    else SS_BWD(2, false, false);
   }
 #undef SS_BWD
   return check_launch("ss_raster_bwd");
@@ -702,44 +742,49 @@ extern "C" int ss_raster_bwd(const int32_t* ranges, const int32_t* vals, const v
                              const void* rec_b, const float* rec_c, int32_t width, int32_t height,
                              const int32_t* tile_order, const float* dimg, const float* t_final,
                              const int32_t* n_contrib, float* g2d, cudaStream_t stream) {
-  return raster_bwd_launch(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, dimg,
-                           t_final, n_contrib, g2d, nullptr, stream);
+  return raster_bwd_ex(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, dimg,
+                       t_final, n_contrib, g2d, nullptr, nullptr, nullptr, stream);
 }
 
-// Raster forward / backward with the explicit per-pixel bbox test (the 2D
-// path of the view driver; strip 4).
-int raster_fwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_a,
-                    const void* rec_b, const float* rec_c, int32_t width, int32_t height,
-                    const int32_t* tile_order, float* img, float* t_final, int32_t* n_contrib,
-                    const int32_t* pbox, cudaStream_t stream) {
-  const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
-  const int n_tiles = tiles_x * tiles_y;
-  const int blocks = (n_tiles * 2 + kWarpsF - 1) / kWarpsF;
-  launch_k(raster_fwd_kernel<4, true>, blocks, kWarpsF * 32, 0, stream, 
-      (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
-      tiles_x, n_tiles, tile_order, img, t_final, n_contrib, floor_threshold(), (const int4*)pbox);
-  return check_launch("raster_fwd_bbox");
+// Words of entry-use mask storage for K pairs over n_tiles tiles (every
+// strip: up to 4 warps per tile).
+extern "C" int64_t ss_raster_used_words(int64_t n_pairs, int32_t n_tiles) {
+  return 4 * (n_pairs / 32 + (int64_t)n_tiles + 2);
 }
 
-int raster_bwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_a,
-                    const void* rec_b, const float* rec_c, int32_t width, int32_t height,
-                    const int32_t* tile_order, const float* dimg, const float* t_final,
-                    const int32_t* n_contrib, float* g2d, const int32_t* pbox,
-                    cudaStream_t stream) {
-  const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
-  const int n_tiles = tiles_x * tiles_y;
-  const int blocks = (n_tiles * 2 + kWarps - 1) / kWarps;
-  const DetArgs d{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  if (int rc = ensure_smem((const void*)raster_bwd_kernel<4, false, true>, kBwdSmem)) return rc;
-  launch_k(raster_bwd_kernel<4, false, true>, blocks, kWarps * 32, kBwdSmem, stream, 
-      (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width, height,
-      tiles_x, n_tiles, tile_order, dimg, t_final, n_contrib, g2d, d, floor_threshold(),
-      (const int4*)pbox);
-  return check_launch("raster_bwd_bbox");
-}
+// masks are shared by the forward and backward warp mappings only when their
+// strips are equal
+bool raster_masks_usable() { return g_strip == g_strip_fwd; }
 
 extern "C" int64_t ss_raster_partial_floats(int64_t n_pairs) {
   return n_pairs * (kTile / (2 * g_strip)) * 9;
+}
+
+int raster_bwd_det_ex(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                      const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                      const int32_t* tile_order, const float* dimg, const float* t_final,
+                      const int32_t* n_contrib, const int32_t* order, const int32_t* offsets,
+                      const int32_t* bbox, const uint64_t* tile_mask, const float* geom, int32_t n,
+                      int32_t* rank, float* partial, float* g2d, const uint32_t* used,
+                      cudaStream_t stream) {
+  if (n <= 0) return SS_OK;
+  launch_k(rank_kernel, grid_for(n, 256), 256, 0, stream, order, n, rank);
+  DetArgs d{partial, rank, offsets, (const int4*)bbox, tile_mask, geom};
+  int rc = raster_bwd_ex(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, dimg,
+                         t_final, n_contrib, g2d, &d, nullptr, used, stream);
+  if (rc) return rc;
+  launch_k(g2d_reduce_kernel, grid_for(n, 128), 128, 0, stream, partial, order, offsets, n,
+                                                           kTile / (2 * g_strip), g2d);
+  return check_launch("ss_raster_bwd_deterministic");
+}
+
+int raster_bwd_plain_ex(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                        const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                        const int32_t* tile_order, const float* dimg, const float* t_final,
+                        const int32_t* n_contrib, float* g2d, const int32_t* pbox,
+                        const uint32_t* used, cudaStream_t stream) {
+  return raster_bwd_ex(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, dimg,
+                       t_final, n_contrib, g2d, nullptr, pbox, used, stream);
 }
 
 extern "C" int ss_raster_bwd_deterministic(
@@ -748,13 +793,7 @@ extern "C" int ss_raster_bwd_deterministic(
     const float* dimg, const float* t_final, const int32_t* n_contrib, const int32_t* order,
     const int32_t* offsets, const int32_t* bbox, const uint64_t* tile_mask, const float* geom,
     int32_t n, int32_t* rank, float* partial, float* g2d, cudaStream_t stream) {
-  if (n <= 0) return SS_OK;
-  launch_k(rank_kernel, grid_for(n, 256), 256, 0, stream, order, n, rank);
-  DetArgs d{partial, rank, offsets, (const int4*)bbox, tile_mask, geom};
-  int rc = raster_bwd_launch(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, dimg,
-                             t_final, n_contrib, g2d, &d, stream);
-  if (rc) return rc;
-  launch_k(g2d_reduce_kernel, grid_for(n, 128), 128, 0, stream, partial, order, offsets, n,
-                                                           kTile / (2 * g_strip), g2d);
-  return check_launch("ss_raster_bwd_deterministic");
+  return raster_bwd_det_ex(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, dimg,
+                           t_final, n_contrib, order, offsets, bbox, tile_mask, geom, n, rank,
+                           partial, g2d, nullptr, stream);
 }

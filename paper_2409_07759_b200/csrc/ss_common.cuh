@@ -270,17 +270,27 @@ __device__ __forceinline__ double u01_53(uint32_t a, uint32_t b) {
 
 }  // namespace ss
 
-// raster.cu: rasterizer launches with the explicit per-pixel bbox test (the
-// 2D-input path of the view driver, csrc/view.cu)
-int raster_fwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_a,
-                    const void* rec_b, const float* rec_c, int32_t width, int32_t height,
-                    const int32_t* tile_order, float* img, float* t_final, int32_t* n_contrib,
-                    const int32_t* pbox, cudaStream_t stream);
-int raster_bwd_bbox(const int32_t* ranges, const int32_t* vals, const void* rec_a,
-                    const void* rec_b, const float* rec_c, int32_t width, int32_t height,
-                    const int32_t* tile_order, const float* dimg, const float* t_final,
-                    const int32_t* n_contrib, float* g2d, const int32_t* pbox,
-                    cudaStream_t stream);
+// raster.cu: launches used by the view driver (csrc/view.cu).  pbox !=
+// nullptr selects the explicit per-pixel bbox test (2D-input path); used !=
+// nullptr records (forward) / consumes (backward) the entry-use masks
+// (ss_raster_used_words words; only when raster_masks_usable()).
+int raster_fwd_ex(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                  const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                  const int32_t* tile_order, float* img, float* t_final, int32_t* n_contrib,
+                  const int32_t* pbox, uint32_t* used, cudaStream_t stream);
+int raster_bwd_plain_ex(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                        const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                        const int32_t* tile_order, const float* dimg, const float* t_final,
+                        const int32_t* n_contrib, float* g2d, const int32_t* pbox,
+                        const uint32_t* used, cudaStream_t stream);
+int raster_bwd_det_ex(const int32_t* ranges, const int32_t* vals, const void* rec_a,
+                      const void* rec_b, const float* rec_c, int32_t width, int32_t height,
+                      const int32_t* tile_order, const float* dimg, const float* t_final,
+                      const int32_t* n_contrib, const int32_t* order, const int32_t* offsets,
+                      const int32_t* bbox, const uint64_t* tile_mask, const float* geom, int32_t n,
+                      int32_t* rank, float* partial, float* g2d, const uint32_t* used,
+                      cudaStream_t stream);
+bool raster_masks_usable();
 // binning.cu: ss_bin_tiles + the raster launch order from the same tile scan
 int bin_tiles_with_order(const int32_t* order, const int32_t* offsets, const int32_t* bbox,
                          const float* geom, const uint64_t* tile_mask, int32_t n,

@@ -216,13 +216,13 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   if (!tile_order_done &&
       (rc = ss_tile_order(v->ranges, n_tiles, v->tile_order, v->ws, v->ws_bytes, stream)))
     return rc;
+  // entry-use masks for the backward when the caller gave room for them
+  const bool masks = v->used && raster_masks_usable() &&
+                     v->used_cap >= ss_raster_used_words(k_host, n_tiles);
+  v->used_ok = masks ? 1 : 0;
   record(v->events[0], stream);
-  if (pbox)
-    rc = raster_fwd_bbox(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,
-                         v->t_final, v->n_contrib, pbox, stream);
-  else
-    rc = ss_raster_fwd(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,
-                       v->t_final, v->n_contrib, stream);
+  rc = raster_fwd_ex(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,
+                     v->t_final, v->n_contrib, pbox, masks ? v->used : nullptr, stream);
   record(v->events[1], stream);
   return rc;
 }
@@ -254,8 +254,10 @@ extern "C" int ss_render2d_bwd(const ss_splats2d* sp, int32_t width, int32_t hei
   if (v->n == 0 || v->n_pairs == 0) return SS_OK;
   memzero(g2d, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
   const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
-  int rc = raster_bwd_bbox(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, width, height,
-                           v->tile_order, dimg, v->t_final, v->n_contrib, g2d, v->bbox, stream);
+  const uint32_t* used = v->used_ok && raster_masks_usable() ? v->used : nullptr;
+  int rc = raster_bwd_plain_ex(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, width, height,
+                               v->tile_order, dimg, v->t_final, v->n_contrib, g2d, v->bbox, used,
+                               stream);
   if (rc) return rc;
   return ss_basis_to_2d(g2d, sp, v->rec_b, v->depth_key, g_mean2d, g_inv2d, g_alpha, g_color,
                         stream);
@@ -268,16 +270,19 @@ extern "C" int ss_render_bwd(const ss_store* store, const ss_camera* cam, const 
   if (v->n == 0 || v->n_pairs == 0) return SS_OK;
   memzero(g2d, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
   const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
+  // the forward's entry-use masks, when it recorded them for this view
+  const uint32_t* used = v->used_ok && raster_masks_usable() ? v->used : nullptr;
   record(v->events[2], stream);
   int rc;
   if (v->partial)
-    rc = ss_raster_bwd_deterministic(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, cam->width,
-                                     cam->height, v->tile_order, dimg, v->t_final, v->n_contrib,
-                                     v->order, v->offsets, v->bbox, v->tile_mask, v->geom, v->n,
-                                     v->rank, v->partial, g2d, stream);
+    rc = raster_bwd_det_ex(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, cam->width, cam->height,
+                           v->tile_order, dimg, v->t_final, v->n_contrib, v->order, v->offsets,
+                           v->bbox, v->tile_mask, v->geom, v->n, v->rank, v->partial, g2d, used,
+                           stream);
   else
-    rc = ss_raster_bwd(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, cam->width, cam->height,
-                       v->tile_order, dimg, v->t_final, v->n_contrib, g2d, stream);
+    rc = raster_bwd_plain_ex(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, cam->width,
+                             cam->height, v->tile_order, dimg, v->t_final, v->n_contrib, g2d,
+                             nullptr, used, stream);
   record(v->events[3], stream);
   if (rc) return rc;
   return ss_project_bwd(store, v->rows, v->n, cam, g2d, v->depth_key, trainable_mask,

@@ -171,6 +171,15 @@ class ViewPipeline:
             for name in ("keys", "vals", "keys_alt", "vals_alt"):
                 setattr(v, name, L.ptr(self._b[name]))
             v.pair_cap = self._b["keys"].numel()
+            # entry-use masks (forward -> backward), sized for the pair capacity
+            words = int(L.lib().ss_raster_used_words(v.pair_cap, n_tiles))
+            um = self._b.get("used")
+            if um is None or um.numel() < words:
+                if um is not None:
+                    um.record_stream(stream if stream is not None else torch.cuda.current_stream())
+                self._b["used"] = um = torch.empty(words, dtype=torch.int32, device=self.dev)
+            v.used = L.ptr(um)
+            v.used_cap = um.numel()
             v.ws = L.ptr(self._b["ws_bin"])
             v.ws_bytes = self._b["ws_bin"].numel()
             if self.events is not None:
