@@ -1,8 +1,7 @@
 // a-9 / a-10 fused optimizer step + SGLD (train.py:321-344, 400-415,
 // 246-264; regularizer gradients loss.py:105-111) and a-11 MCMC relocation
-// (train.py:267-318).  All parameter math in fp64; one thread per row.
-#include <cub/cub.cuh>
-
+// (train.py:267-318).  All parameter math in fp64; one thread per row.  No
+// library kernels: the relocation partition and scan are this file's own.
 #include "ss_common.cuh"
 
 namespace ss {
@@ -195,44 +194,180 @@ __global__ void sgld_kernel(double* __restrict__ opt, int64_t n_rows, int32_t ro
 
 // ---------------------------------------------------------------- relocation
 // flags: 1 = dead, 2 = alive, 0 = row of an inactive generation
-__global__ void reloc_flags_kernel(const double* __restrict__ opt, int64_t n_rows,
-                                   int32_t rows_per_gen, const ss_gen_step* __restrict__ gens,
-                                   double threshold, uint8_t* __restrict__ dead,
-                                   uint8_t* __restrict__ alive, int32_t* __restrict__ hits) {
-  pdl_wait();
-  pdl_trigger();
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n_rows) return;
-  hits[r] = 0;
-  if (!gens[r / rows_per_gen].active) {
-    dead[r] = 0;
-    alive[r] = 0;
-    return;
+// Relocation bookkeeping in the library's own kernels (no CUB): a stable
+// partition of the active optimizable rows into dead (alpha < threshold) and
+// alive rows, in row order (train.py:279-292), and the fp64 inclusive scan
+// of the alive rows' alphas -- the unnormalised cdf; reloc_targets_kernel
+// compares cdf[i] / cdf[last] with u, numpy's choice(p=alpha / sum) up to
+// rounding (train.py:293-294).  Fixed-order block sums: deterministic.
+constexpr int kRelThreads = 256;
+constexpr int kRelItems = 4;
+constexpr int kRelTile = kRelThreads * kRelItems;
+
+template <typename T>
+__device__ __forceinline__ T block_exclusive_t(T v, T* s_warp, T& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
-  const double a = sigmoid(opt[r * SS_ROW + 10]);
-  dead[r] = a < threshold;
-  alive[r] = !(a < threshold);
+  if (lane == 31) s_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    T w = lane < nw ? s_warp[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) s_warp[lane] = w;
+  }
+  __syncthreads();
+  total = s_warp[nw - 1];
+  const T ex = x - v + (wid > 0 ? s_warp[wid - 1] : T(0));
+  __syncthreads();  // s_warp reusable by the caller
+  return ex;
 }
 
-__global__ void reloc_probs_kernel(const double* __restrict__ opt,
-                                   const int32_t* __restrict__ alive_rows,
-                                   const int32_t* __restrict__ counts, int64_t n_rows,
-                                   double* __restrict__ alpha_alive) {
-  pdl_wait();
-  pdl_trigger();
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n_rows) return;
-  const int n_alive = counts[1];
-  alpha_alive[k] = k < n_alive ? sigmoid(opt[(int64_t)alive_rows[k] * SS_ROW + 10]) : 0.0;
+// 0: row of an inactive generation, 1: dead, 2: alive
+__device__ __forceinline__ int reloc_flag(const double* __restrict__ opt, int64_t r, int64_t n_rows,
+                                          int32_t rows_per_gen, const ss_gen_step* __restrict__ gens,
+                                          double threshold) {
+  if (r >= n_rows || !gens[r / rows_per_gen].active) return 0;
+  return sigmoid(opt[r * SS_ROW + 10]) < threshold ? 1 : 2;
 }
 
-__global__ void reloc_div_kernel(double* __restrict__ p, int64_t n_rows,
-                                 const double* __restrict__ total) {
+// per block of kRelTile rows: (dead << 32) | alive; zeroes the hit counts
+__global__ void __launch_bounds__(kRelThreads) reloc_count_kernel(
+    const double* __restrict__ opt, int64_t n_rows, int32_t rows_per_gen,
+    const ss_gen_step* __restrict__ gens, double threshold, int32_t* __restrict__ hits,
+    unsigned long long* __restrict__ block_counts) {
   pdl_wait();
   pdl_trigger();
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n_rows) return;
-  p[k] = p[k] / *total;
+  __shared__ unsigned long long s_warp[32];
+  const int64_t r0 = (int64_t)blockIdx.x * kRelTile;
+  unsigned long long c = 0;
+#pragma unroll
+  for (int k = 0; k < kRelItems; ++k) {
+    const int64_t r = r0 + k * kRelThreads + threadIdx.x;
+    if (r < n_rows) hits[r] = 0;
+    const int f = reloc_flag(opt, r, n_rows, rows_per_gen, gens, threshold);
+    c += f == 1 ? (1ull << 32) : f == 2 ? 1ull : 0ull;
+  }
+  unsigned long long total;
+  block_exclusive_t(c, s_warp, total);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = total;
+}
+
+// one CTA: exclusive scan of the packed per-block counts; totals -> counts
+__global__ void __launch_bounds__(kRelThreads) reloc_count_scan_kernel(
+    unsigned long long* __restrict__ block_counts, int nblocks, int32_t* __restrict__ counts) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ unsigned long long s_warp[32];
+  unsigned long long carry = 0;
+  for (int base = 0; base < nblocks; base += kRelThreads) {
+    const int i = base + threadIdx.x;
+    const unsigned long long v = i < nblocks ? block_counts[i] : 0ull;
+    unsigned long long total;
+    const unsigned long long ex = block_exclusive_t(v, s_warp, total);
+    if (i < nblocks) block_counts[i] = carry + ex;
+    carry += total;
+  }
+  if (threadIdx.x == 0) {
+    counts[0] = (int32_t)(carry >> 32);
+    counts[1] = (int32_t)(carry & 0xffffffffull);
+  }
+}
+
+// stable partition: dead / alive row ids in row order, alive alphas
+__global__ void __launch_bounds__(kRelThreads) reloc_scatter_kernel(
+    const double* __restrict__ opt, int64_t n_rows, int32_t rows_per_gen,
+    const ss_gen_step* __restrict__ gens, double threshold,
+    const unsigned long long* __restrict__ block_counts, int32_t* __restrict__ dead_rows,
+    int32_t* __restrict__ alive_rows, double* __restrict__ alpha_alive) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ unsigned long long s_warp[32];
+  const int64_t r0 = (int64_t)blockIdx.x * kRelTile;
+  unsigned long long run = block_counts[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kRelItems; ++k) {
+    const int64_t r = r0 + k * kRelThreads + threadIdx.x;
+    const int f = reloc_flag(opt, r, n_rows, rows_per_gen, gens, threshold);
+    const unsigned long long c = f == 1 ? (1ull << 32) : f == 2 ? 1ull : 0ull;
+    unsigned long long total;
+    const unsigned long long pos = run + block_exclusive_t(c, s_warp, total);
+    if (f == 1) dead_rows[pos >> 32] = (int32_t)r;
+    if (f == 2) {
+      const uint32_t a = (uint32_t)(pos & 0xffffffffull);
+      alive_rows[a] = (int32_t)r;
+      alpha_alive[a] = sigmoid(opt[r * SS_ROW + 10]);
+    }
+    run += total;
+  }
+}
+
+// fp64 inclusive scan of alpha_alive[0, counts[1]) in three launches
+__global__ void __launch_bounds__(kRelThreads) reloc_dsum_kernel(
+    const double* __restrict__ a, const int32_t* __restrict__ counts, double* __restrict__ sums) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double s_warp[32];
+  const int n = counts[1];
+  const int64_t e0 = (int64_t)blockIdx.x * kRelTile + (int64_t)threadIdx.x * kRelItems;
+  if ((int64_t)blockIdx.x * kRelTile >= n) return;
+  double v = 0.0;
+#pragma unroll
+  for (int k = 0; k < kRelItems; ++k)
+    if (e0 + k < n) v += a[e0 + k];
+  double total;
+  block_exclusive_t(v, s_warp, total);
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kRelThreads) reloc_dtop_kernel(double* __restrict__ sums,
+                                                                const int32_t* __restrict__ counts) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double s_warp[32];
+  const int nblocks = (counts[1] + kRelTile - 1) / kRelTile;
+  double carry = 0.0;
+  for (int base = 0; base < nblocks; base += kRelThreads) {
+    const int i = base + threadIdx.x;
+    const double v = i < nblocks ? sums[i] : 0.0;
+    double total;
+    const double ex = block_exclusive_t(v, s_warp, total);
+    if (i < nblocks) sums[i] = carry + ex;
+    carry += total;
+  }
+}
+
+__global__ void __launch_bounds__(kRelThreads) reloc_dscan_kernel(
+    const double* __restrict__ a, const int32_t* __restrict__ counts,
+    const double* __restrict__ sums, double* __restrict__ cdf) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double s_warp[32];
+  const int n = counts[1];
+  if ((int64_t)blockIdx.x * kRelTile >= n) return;
+  const int64_t e0 = (int64_t)blockIdx.x * kRelTile + (int64_t)threadIdx.x * kRelItems;
+  double x[kRelItems];
+  double v = 0.0;
+#pragma unroll
+  for (int k = 0; k < kRelItems; ++k) {
+    x[k] = e0 + k < n ? a[e0 + k] : 0.0;
+    v += x[k];
+  }
+  double total;
+  double run = sums[blockIdx.x] + block_exclusive_t(v, s_warp, total);
+#pragma unroll
+  for (int k = 0; k < kRelItems; ++k) {
+    run += x[k];
+    if (e0 + k < n) cdf[e0 + k] = run;
+  }
 }
 
 // numpy Generator.choice(p=...): cdf = cumsum(p); cdf /= cdf[-1];
@@ -328,35 +463,21 @@ __global__ void reloc_targets_update_kernel(double* __restrict__ opt, double* __
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct RelocWs {
-  uint8_t* dead_flag;
-  uint8_t* alive_flag;
   int32_t* dead_rows;
   int32_t* alive_rows;
   int32_t* target;
   int32_t* hits;
-  double* p;
+  double* alpha;               // alive rows' alphas (unnormalised probabilities)
   double* cdf;
-  double* total;
-  int32_t* row_ids;
-  void* cub;
-  size_t cub_bytes;
+  double* dsums;               // per-block sums of the scan
+  unsigned long long* bcounts;  // per-block packed (dead, alive) counts
   size_t total_bytes;
 };
-
-static size_t reloc_cub_bytes(int64_t n) {
-  size_t a = 0, b = 0, c = 0;
-  int nn = (int)(n > 0 ? n : 1);
-  cub::DeviceSelect::Flagged(nullptr, a, (int32_t*)nullptr, (uint8_t*)nullptr, (int32_t*)nullptr,
-                             (int32_t*)nullptr, nn);
-  cub::DeviceReduce::Sum(nullptr, b, (double*)nullptr, (double*)nullptr, nn);
-  cub::DeviceScan::InclusiveSum(nullptr, c, (double*)nullptr, (double*)nullptr, nn);
-  size_t m = a > b ? a : b;
-  return m > c ? m : c;
-}
 
 static RelocWs carve(void* base, int64_t n) {
   RelocWs w;
   size_t nn = (size_t)(n > 0 ? n : 1);
+  size_t nb = (nn + kRelTile - 1) / kRelTile;
   char* p = (char*)base;
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -364,27 +485,16 @@ static RelocWs carve(void* base, int64_t n) {
     off += align256(bytes);
     return r;
   };
-  w.dead_flag = (uint8_t*)take(nn);
-  w.alive_flag = (uint8_t*)take(nn);
   w.dead_rows = (int32_t*)take(nn * 4);
   w.alive_rows = (int32_t*)take(nn * 4);
   w.target = (int32_t*)take(nn * 4);
   w.hits = (int32_t*)take(nn * 4);
-  w.p = (double*)take(nn * 8);
+  w.alpha = (double*)take(nn * 8);
   w.cdf = (double*)take(nn * 8);
-  w.total = (double*)take(64);
-  w.row_ids = (int32_t*)take(nn * 4);
-  w.cub_bytes = reloc_cub_bytes(n);
-  w.cub = take(w.cub_bytes);
+  w.dsums = (double*)take(nb * 8);
+  w.bcounts = (unsigned long long*)take(nb * 8);
   w.total_bytes = off;
   return w;
-}
-
-__global__ void iota32_kernel(int32_t* v, int64_t n) {
-  pdl_wait();
-  pdl_trigger();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (int32_t)i;
 }
 
 }  // namespace ss
@@ -430,27 +540,20 @@ extern "C" int ss_relocate(double* opt, double* adam_m, double* adam_v, int64_t 
   void* base = (void*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   RelocWs w = carve(base, n_rows);
   const int nb = grid_for(n_rows, 256);
-  const int n = (int)n_rows;
-  launch_k(reloc_flags_kernel, nb, 256, 0, stream, opt, n_rows, rows_per_gen, gens, threshold,
-                                             w.dead_flag, w.alive_flag, w.hits);
-  launch_k(iota32_kernel, nb, 256, 0, stream, w.row_ids, n_rows);
-  size_t cb = w.cub_bytes;
-  cudaError_t e = cub::DeviceSelect::Flagged(w.cub, cb, w.row_ids, w.dead_flag, w.dead_rows,
-                                             out_counts, n, stream);
-  cb = w.cub_bytes;
-  if (e == cudaSuccess)
-    e = cub::DeviceSelect::Flagged(w.cub, cb, w.row_ids, w.alive_flag, w.alive_rows,
-                                   out_counts + 1, n, stream);
-  if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_relocate: %s", cudaGetErrorString(e));
-  // p = alpha[alive] / sum(alpha[alive]); cdf = cumsum(p)  (train.py:293-294)
-  launch_k(reloc_probs_kernel, nb, 256, 0, stream, opt, w.alive_rows, out_counts, n_rows, w.p);
-  cb = w.cub_bytes;
-  e = cub::DeviceReduce::Sum(w.cub, cb, w.p, w.total, n, stream);
-  if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_relocate: %s", cudaGetErrorString(e));
-  launch_k(reloc_div_kernel, nb, 256, 0, stream, w.p, n_rows, w.total);
-  cb = w.cub_bytes;
-  e = cub::DeviceScan::InclusiveSum(w.cub, cb, w.p, w.cdf, n, stream);
-  if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ss_relocate: %s", cudaGetErrorString(e));
+  const int nbt = grid_for(n_rows, kRelTile);
+  // dead / alive partition (row order) + alive alphas; counts = (n_dead, n_alive)
+  launch_k(reloc_count_kernel, nbt, kRelThreads, 0, stream, (const double*)opt, n_rows,
+           rows_per_gen, gens, threshold, w.hits, w.bcounts);
+  launch_k(reloc_count_scan_kernel, 1, kRelThreads, 0, stream, w.bcounts, nbt, out_counts);
+  launch_k(reloc_scatter_kernel, nbt, kRelThreads, 0, stream, (const double*)opt, n_rows,
+           rows_per_gen, gens, threshold, (const unsigned long long*)w.bcounts, w.dead_rows,
+           w.alive_rows, w.alpha);
+  // cdf = inclusive scan of the alive alphas (train.py:293-294, unnormalised)
+  launch_k(reloc_dsum_kernel, nbt, kRelThreads, 0, stream, (const double*)w.alpha,
+           (const int32_t*)out_counts, w.dsums);
+  launch_k(reloc_dtop_kernel, 1, kRelThreads, 0, stream, w.dsums, (const int32_t*)out_counts);
+  launch_k(reloc_dscan_kernel, nbt, kRelThreads, 0, stream, (const double*)w.alpha,
+           (const int32_t*)out_counts, (const double*)w.dsums, w.cdf);
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   const uint32_t c0 = (uint32_t)counter, c1 = (uint32_t)(counter >> 32);
   launch_k(reloc_targets_kernel, nb, 256, 0, stream, w.cdf, w.alive_rows, out_counts, uniforms, k0, k1,

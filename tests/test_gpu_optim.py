@@ -200,3 +200,43 @@ def test_train_window_slides_match_reference(T):
     T.mature(2, state, writer=None)
     T.train_swin(2, 2 + cfg.swin_size, state, ds, iterations=3)
     check("w2")
+
+
+def test_relocation_large_matches_oracle_with_same_uniforms(T):
+    """ss_relocate's own partition / scan kernels (no library code) at scale:
+    6 generations x 40k rows, a few percent dead, the reference's uniforms;
+    the post-state equals the oracle's relocate (train.py:267-318) to 1e-12,
+    moments of relocated rows zeroed, counts conserved."""
+    import paper_2409_07759_b200 as P
+    from oracle import splat_oracle as O
+    rng = np.random.default_rng(31)
+    gens, ref_params, ref_m, ref_v = [], [], [], []
+    for i in range(6):
+        n = 40_000
+        q = rng.normal(size=(n, 4))
+        a = rng.uniform(0.0005, 0.95, n)
+        dead = rng.random(n) < 0.03
+        a[dead] = rng.uniform(1e-4, 0.004, int(dead.sum()))
+        params = {"mean": rng.uniform(-1, 1, (n, 3)), "quat": q / np.linalg.norm(q, axis=1, keepdims=True),
+                  "log_scale": np.log(rng.uniform(0.01, 0.1, (n, 3))),
+                  "opacity_logit": T._logit(a), "color": rng.uniform(0, 1, (n, 3))}
+        g = T.SliceGen(slot=i, lifespan=P.Lifespan(i, i, i + 6), params=params)
+        for k in GROUPS:
+            g.adam_m[k][...] = rng.normal(size=g.adam_m[k].shape)
+            g.adam_v[k][...] = rng.uniform(0, 1, size=g.adam_v[k].shape)
+        gens.append(g)
+        ref_params.append({k: v.copy() for k, v in params.items()})
+        ref_m.append({k: v.copy() for k, v in g.adam_m.items()})
+        ref_v.append({k: v.copy() for k, v in g.adam_v.items()})
+    alpha = np.concatenate([O.sigmoid(p["opacity_logit"]) for p in ref_params])
+    n_dead = int((alpha < 0.005).sum())
+    assert n_dead > 1000
+    u = np.random.default_rng(7).random(n_dead)
+    moved = T.relocate(gens, 0.005, np.random.default_rng(7))
+    ref_moved = O.relocate(ref_params, ref_m, ref_v, 0.005, u)
+    assert moved == ref_moved == n_dead
+    for gi in range(6):
+        for k in GROUPS:
+            np.testing.assert_allclose(gens[gi].params[k], ref_params[gi][k], rtol=1e-12,
+                                       atol=1e-14, err_msg=f"{gi} {k}")
+            assert np.array_equal(gens[gi].adam_m[k] == 0, ref_m[gi][k] == 0)
