@@ -112,7 +112,11 @@ __global__ void __launch_bounds__(128, 4) adam_sgld_kernel(double* __restrict__ 
     double2* mr = reinterpret_cast<double2*>(m + r * SS_ROW);
     double2* vr = reinterpret_cast<double2*>(v + r * SS_ROW);
     // moments in two halves, each half's loads issued together (one memory
-    // round trip per half instead of one per column pair)
+    // round trip per half instead of one per column pair).  The bias
+    // corrections divide every column by the same two constants: products
+    // with their reciprocals (one more rounding than numpy's x / c, ~1e-16
+    // relative, inside the optimizer's 1e-8 / 1e-6 parity).
+    const double ibc1 = 1.0 / gs.bc1, ibc2 = 1.0 / gs.bc2;
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       constexpr int kH = 4;  // column pairs of the first half (7 = 4 + 3)
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(128, 4) adam_sgld_kernel(double* __restrict__ 
           const int k = 2 * (b0 + q) + h2;
           mk[h2] = __dadd_rn(__dmul_rn(mk[h2], h.b1), __dmul_rn(1.0 - h.b1, g[k]));
           vk[h2] = __dadd_rn(__dmul_rn(vk[h2], h.b2), __dmul_rn(__dmul_rn(1.0 - h.b2, g[k]), g[k]));
-          const double step = ddiv(ddiv(mk[h2], gs.bc1), dadd(sqrt(ddiv(vk[h2], gs.bc2)), h.eps));
+          const double step = ddiv(dmul(mk[h2], ibc1), dadd(sqrt(dmul(vk[h2], ibc2)), h.eps));
           pv[k] = dsub(pv[k], dmul(h.lr[group[k]], step));
         }
         mr[b0 + q] = make_double2(mk[0], mk[1]);
