@@ -104,6 +104,63 @@ __device__ __forceinline__ void project_one(const CamK& cam, const Gauss64& g, P
   p.keep = in_front && on_image;
 }
 
+// The backward's re-derivation of the projection quantities (raster.py:
+// 86-111): the same formulas as project_one with ordinary (contractible)
+// fp64 arithmetic and shared reciprocals in place of the IEEE-sequenced
+// operations -- the gradient chain needs fp64 accuracy, not numpy's exact
+// rounding (parity is 1e-3 of the max per group), and the exact divides
+// with their slow-path branches dominated this kernel.
+__device__ __forceinline__ void project_basis_fast(const CamK& cam, const Gauss64& g, Proj& p) {
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+    p.t[j] = g.mean[0] * cam.R[j][0] + g.mean[1] * cam.R[j][1] + g.mean[2] * cam.R[j][2] + cam.T[j];
+  p.z = p.t[2];
+  const double* q = g.quat;
+  p.qnorm = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const double iqd = 1.0 / fmax(p.qnorm, 1e-12);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) p.qn[k] = q[k] * iqd;
+  {
+    const double w = p.qn[0], x = p.qn[1], y = p.qn[2], z = p.qn[3];
+    p.rq[0][0] = 1.0 - 2.0 * (y * y + z * z);
+    p.rq[0][1] = 2.0 * (x * y - w * z);
+    p.rq[0][2] = 2.0 * (x * z + w * y);
+    p.rq[1][0] = 2.0 * (x * y + w * z);
+    p.rq[1][1] = 1.0 - 2.0 * (x * x + z * z);
+    p.rq[1][2] = 2.0 * (y * z - w * x);
+    p.rq[2][0] = 2.0 * (x * z - w * y);
+    p.rq[2][1] = 2.0 * (y * z + w * x);
+    p.rq[2][2] = 1.0 - 2.0 * (x * x + y * y);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) p.m3[a][b] = p.rq[a][b] * g.scale[b];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      p.sigma[a][c] = p.m3[a][0] * p.m3[c][0] + p.m3[a][1] * p.m3[c][1] + p.m3[a][2] * p.m3[c][2];
+  const double iz = 1.0 / p.z, iz2 = iz * iz;
+  const double J[2][3] = {{cam.fx * iz, 0.0, -cam.fx * p.t[0] * iz2},
+                          {0.0, cam.fy * iz, -cam.fy * p.t[1] * iz2}};
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      p.mproj[a][c] = J[a][0] * cam.R[0][c] + J[a][1] * cam.R[1][c] + J[a][2] * cam.R[2][c];
+  double ms[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      ms[a][c] = p.mproj[a][0] * p.sigma[0][c] + p.mproj[a][1] * p.sigma[1][c] +
+                 p.mproj[a][2] * p.sigma[2][c];
+  p.a = ms[0][0] * p.mproj[0][0] + ms[0][1] * p.mproj[0][1] + ms[0][2] * p.mproj[0][2];
+  p.b = ms[0][0] * p.mproj[1][0] + ms[0][1] * p.mproj[1][1] + ms[0][2] * p.mproj[1][2];
+  p.c = ms[1][0] * p.mproj[1][0] + ms[1][1] * p.mproj[1][1] + ms[1][2] * p.mproj[1][2];
+}
+
 // Everything a-4 / a-5 need from one kept splat: the fp32 binning geometry,
 // the exact kept-tile count and mask of its bbox, the depth key and the
 // rasterizer record (raster.cu: conic pre-scaled by kappa = -log2(e)/2 so
@@ -275,7 +332,7 @@ __global__ void __launch_bounds__(128, SS_PROJ_BWD_MINB) project_bwd_kernel(Stor
   Gauss64 g;
   load_row(store, row, g);
   Proj p;
-  project_one(cam, g, p);
+  project_basis_fast(cam, g, p);
   // g2d holds the rasterizer's basis sums over every (pixel, entry) of this
   // splat (raster.cu): W = (t dx, t dy, t dx^2, t dx dy, t dy^2, t, colour[3])
   // with t = alpha G d alpha'.  With dm = -t/2 and the conic (i0, i1, i2):
@@ -284,16 +341,17 @@ __global__ void __launch_bounds__(128, SS_PROJ_BWD_MINB) project_bwd_kernel(Stor
   const float* gg = g2d + (int64_t)i * SS_G2D_ROW;
   const double ad = p.a + kDilation, cd = p.c + kDilation, b = p.b;
   const double det = ad * cd - b * b;
-  const double ci0 = cd / det, ci1 = -b / det, ci2 = ad / det;
+  const double idet = 1.0 / det;
+  const double ci0 = cd * idet, ci1 = -b * idet, ci2 = ad * idet;
   const double W0 = gg[0], W1 = gg[1];
   const double gm2x = ci0 * W0 + ci1 * W1, gm2y = ci1 * W0 + ci2 * W1;
   const double gia = -0.5 * gg[2], gib = -(double)gg[3], gic = -0.5 * gg[4];
   const double g_alpha_x_alpha = gg[5];  // d alpha times alpha
-  const double det2 = det * det;
+  const double idet2 = idet * idet;
   // raster.py:262-266
-  const double g_a = (gia * (-cd * cd) + gib * (b * cd) + gic * (-b * b)) / det2;
-  const double g_b = (gia * (2.0 * b * cd) + gib * (-det - 2.0 * b * b) + gic * (2.0 * ad * b)) / det2;
-  const double g_c = (gia * (-b * b) + gib * (ad * b) + gic * (-ad * ad)) / det2;
+  const double g_a = (gia * (-cd * cd) + gib * (b * cd) + gic * (-b * b)) * idet2;
+  const double g_b = (gia * (2.0 * b * cd) + gib * (-det - 2.0 * b * b) + gic * (2.0 * ad * b)) * idet2;
+  const double g_c = (gia * (-b * b) + gib * (ad * b) + gic * (-ad * ad)) * idet2;
   // raster.py:269-280
   double sm0[3], sm1[3];
 #pragma unroll
@@ -321,16 +379,16 @@ __global__ void __launch_bounds__(128, SS_PROJ_BWD_MINB) project_bwd_kernel(Stor
 #pragma unroll
     for (int c = 0; c < 3; ++c)
       gj[r][c] = gm[r][0] * cam.R[c][0] + gm[r][1] * cam.R[c][1] + gm[r][2] * cam.R[c][2];
-  const double z = p.z, z2 = z * z, z3 = z2 * z;
+  const double iz = 1.0 / p.z, iz2 = iz * iz, iz3 = iz2 * iz;
   const double xc = p.t[0], yc = p.t[1];
   double gt[3];
-  gt[0] = gj[0][2] * (-cam.fx / z2);
-  gt[1] = gj[1][2] * (-cam.fy / z2);
-  gt[2] = gj[0][0] * (-cam.fx / z2) + gj[1][1] * (-cam.fy / z2) +
-          gj[0][2] * (2.0 * cam.fx * xc / z3) + gj[1][2] * (2.0 * cam.fy * yc / z3);
-  gt[0] += gm2x * cam.fx / z;
-  gt[1] += gm2y * cam.fy / z;
-  gt[2] += -gm2x * cam.fx * xc / z2 - gm2y * cam.fy * yc / z2;
+  gt[0] = gj[0][2] * (-cam.fx * iz2);
+  gt[1] = gj[1][2] * (-cam.fy * iz2);
+  gt[2] = gj[0][0] * (-cam.fx * iz2) + gj[1][1] * (-cam.fy * iz2) +
+          gj[0][2] * (2.0 * cam.fx * xc * iz3) + gj[1][2] * (2.0 * cam.fy * yc * iz3);
+  gt[0] += gm2x * cam.fx * iz;
+  gt[1] += gm2y * cam.fy * iz;
+  gt[2] += -gm2x * cam.fx * xc * iz2 - gm2y * cam.fy * yc * iz2;
   float* out = grads + (int64_t)row * SS_GRAD_ROW;
 #pragma unroll
   for (int c = 0; c < 3; ++c)
@@ -369,8 +427,9 @@ __global__ void __launch_bounds__(128, SS_PROJ_BWD_MINB) project_bwd_kernel(Stor
     gqn[qi] = acc;
   }
   const double dot = p.qn[0] * gqn[0] + p.qn[1] * gqn[1] + p.qn[2] * gqn[2] + p.qn[3] * gqn[3];
+  const double iqn = 1.0 / p.qnorm;
 #pragma unroll
-  for (int qi = 0; qi < 4; ++qi) out[3 + qi] = (float)((gqn[qi] - p.qn[qi] * dot) / p.qnorm);
+  for (int qi = 0; qi < 4; ++qi) out[3 + qi] = (float)((gqn[qi] - p.qn[qi] * dot) * iqn);
   // raster.py:336-343
   out[10] = (float)(g_alpha_x_alpha * (1.0 - g.opacity));  // d alpha * alpha (1 - alpha)
   out[11] = gg[6];
