@@ -258,7 +258,8 @@ int ss_raster_bwd(const int32_t* ranges, const int32_t* vals, const void* rec_a,
  * trainable (mask ? mask[i] : 1) and row < trainable_rows, writes the
  * optimization-space gradient row grads[out_row] (14 floats: mean[3]
  * quat[4] log_scale[3] opacity_logit color[3]); out_row = row.  Culled
- * rows are left untouched (caller zeroes). */
+ * trainable rows get a zero row; rows that are not active in this view
+ * are left untouched (the caller zeroes them when it steps them). */
 int ss_project_bwd(const ss_store* store, const int32_t* rows, int32_t n, const ss_camera* cam,
                    const float* g2d, const uint64_t* depth_key, const uint8_t* trainable_mask,
                    int64_t trainable_rows, float* grads, ss_stream_t stream);

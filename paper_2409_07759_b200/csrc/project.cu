@@ -325,10 +325,15 @@ __global__ void __launch_bounds__(128, SS_PROJ_BWD_MINB) project_bwd_kernel(Stor
   pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  if (depth_key[i] == ~0ull) return;  // culled
   if (mask && !mask[i]) return;
   const int32_t row = rows ? rows[i] : i;
   if (row >= trainable_rows) return;
+  if (depth_key[i] == ~0ull) {  // culled: a zero gradient row (the step needs no pre-zeroed buffer)
+    float2* out2 = reinterpret_cast<float2*>(grads + (int64_t)row * SS_GRAD_ROW);
+#pragma unroll
+    for (int c = 0; c < SS_GRAD_ROW / 2; ++c) out2[c] = make_float2(0.f, 0.f);
+    return;
+  }
   Gauss64 g;
   load_row(store, row, g);
   Proj p;

@@ -267,8 +267,11 @@ extern "C" int ss_render_bwd(const ss_store* store, const ss_camera* cam, const 
                              const float* dimg, float* g2d, const uint8_t* trainable_mask,
                              int64_t trainable_rows, float* grads, cudaStream_t stream) {
   if (!store || !cam || !v) return set_error(SS_ERR_INVALID, "ss_render_bwd: bad args");
-  if (v->n == 0 || v->n_pairs == 0) return SS_OK;
+  if (v->n == 0) return SS_OK;
   memzero(g2d, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
+  if (v->n_pairs == 0)  // nothing reached a pixel: zero gradients for every active row
+    return ss_project_bwd(store, v->rows, v->n, cam, g2d, v->depth_key, trainable_mask,
+                          trainable_rows, grads, stream);
   const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
   // the forward's entry-use masks, when it recorded them for this view
   const uint32_t* used = v->used_ok && raster_masks_usable() ? v->used : nullptr;

@@ -237,20 +237,28 @@ class DeviceModel:
 
         stepped = stepped_generations(self.state.slices, [f for f, _ in draws])
         self._gen_table(stepped)
-        sums = self.view_gradients(draws[rank], dataset)
+        # one rank, one view: every stepped row is active in this view and
+        # ss_project_bwd writes all of them (zeros for culled rows), so the
+        # gradient buffer needs no zero fill; with several ranks a stepped
+        # generation may be inactive in this rank's frame
+        dp = self.state.dp
+        sums = self.view_gradients(draws[rank], dataset,
+                                   zero_grads=dp is not None and dp.world_size > 1)
         if self.state.dp is not None:
             self.state.dp.allreduce_grads(self.grads)
         self.apply_step(stepped, it)
         return sums
 
-    def view_gradients(self, draw, dataset):
+    def view_gradients(self, draw, dataset, zero_grads: bool = True):
         """Forward, loss and backward of one (frame, view) draw: the
-        optimization-space gradient lands in self.grads (zeroed first).
+        optimization-space gradient lands in self.grads (zeroed first unless
+        the caller knows every row it will read is active in this view).
         Returns the device loss sums."""
         frame, view = draw
         sp = L.stream_ptr()
         rows, n, n_opt_here = self.compact(frame)
-        L.check(L.lib().ss_memzero(L.ptr(self.grads), self.grads.numel() * 4, sp), "memzero")
+        if zero_grads:
+            L.check(L.lib().ss_memzero(L.ptr(self.grads), self.grads.numel() * 4, sp), "memzero")
         cam = dataset.cameras[view]
         # ground truth may still be in flight on a copy stream: only the loss
         # waits for it, the projection / binning / raster run meanwhile

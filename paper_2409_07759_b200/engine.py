@@ -245,13 +245,14 @@ class ViewPipeline:
     def backward(self, dimg: torch.Tensor, grads: torch.Tensor, trainable_mask=None,
                  trainable_rows: int | None = None, stream=None):
         """Accumulate optimization-space gradients of sum(dimg * image) into
-        `grads` (rows x 14 float32, indexed by row id; caller zeroes) with one
-        native call (ss_render_bwd)."""
+        `grads` (rows x 14 float32, indexed by row id) with one native call
+        (ss_render_bwd): every active trainable row is written (zeros when it
+        reaches no pixel); rows outside the view are left to the caller."""
         n = self.n
-        if n == 0 or self.n_pairs == 0:
+        if n == 0:
             return
         g2d = self._buf("g2d", (n, L.SS_G2D_ROW), torch.float32)
-        if self.deterministic:
+        if self.deterministic and self.n_pairs > 0:
             nf = int(L.lib().ss_raster_partial_floats(self.n_pairs))
             part = self._buf("partial", (max(nf, 1),), torch.float32)
             rank = self._buf("rank", (max(n, 1),), torch.int32)
