@@ -102,6 +102,22 @@ int ss_compact_active(const int32_t* row_start, const int32_t* row_expire, int64
                       int32_t frame, int32_t* out_rows, int32_t* out_counts, void* ws,
                       size_t ws_bytes, ss_stream_t stream);
 
+/* fp64 projection of n splats for API callers (raster.py:176-191 `project`):
+ * out[i] = (u, v, cov a, cov b, cov c, z, kept) -- the raw 2D covariance
+ * before the +0.3 dilation; kept = 1.0 when the splat survives the near
+ * plane and the 3-sigma cull, else 0.0 (the other fields are then
+ * meaningless).  Same fp64 sequence as ss_project_fwd. */
+int ss_project_splats(const ss_store* store, const int32_t* rows, int32_t n,
+                      const ss_camera* cam, double* out, ss_stream_t stream);
+
+/* ---- a-8 regularizers (loss.py:105-111): over n optimizable active splats
+ * with direct-space alpha[n] and scales[n*3], writes reg_logit[n] =
+ * w_op alpha (1 - alpha) / n, reg_log_scale[n*3] = w_sc s / n and
+ * terms[2] = (w_op mean(alpha), w_sc mean(sum_k s_k)) (fixed-order sums). */
+int ss_reg_grads(const double* alpha, const double* scales, int32_t n, double w_op,
+                 double w_sc, double* reg_logit, double* reg_log_scale, double* terms,
+                 ss_stream_t stream);
+
 /* ---- a-3 EWA projection / cull / conic / bbox: raster.py:76-173.
  * For active index i (row = rows ? rows[i] : i): rec_a = (u, v, k inv0, k inv1),
  * rec_b = (k inv2, log2 alpha, r, g), rec_c = b (float32, rounded once from fp64;

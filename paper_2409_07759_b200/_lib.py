@@ -91,6 +91,8 @@ _SIGNATURES = {
     "ss_set_alpha_floor": ([I32], c_int),
     "ss_write_small": ([P, P, c_size_t, P], c_int),
     "ss_raster_used_words": ([I64, I32], I64),
+    "ss_project_splats": ([P, P, I32, P, P, P], c_int),
+    "ss_reg_grads": ([P, P, I32, c_double, c_double, P, P, P, P], c_int),
     "ss_poll_wait_ns": ([], c_uint64),
     "ss_get_alpha_floor": ([], I32),
     "ss_bin_tiles_workspace_bytes": ([I64, I32], c_size_t),

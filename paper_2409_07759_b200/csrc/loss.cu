@@ -393,9 +393,64 @@ __global__ void loss_reduce_kernel(const double* __restrict__ partials, int n_bl
   }
 }
 
+// loss.py:105-111 regularizer gradients and terms; one CTA, fixed-order sums
+__global__ void __launch_bounds__(1024) reg_grads_kernel(const double* __restrict__ alpha,
+                                                         const double* __restrict__ scales, int n,
+                                                         double w_op, double w_sc,
+                                                         double* __restrict__ reg_logit,
+                                                         double* __restrict__ reg_log_scale,
+                                                         double* __restrict__ terms) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double s[2][32];
+  double ta = 0.0, ts = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double a = alpha[i];
+    const double s0 = scales[3 * i], s1 = scales[3 * i + 1], s2 = scales[3 * i + 2];
+    reg_logit[i] = w_op * a * (1.0 - a) / n;
+    reg_log_scale[3 * i] = w_sc * s0 / n;
+    reg_log_scale[3 * i + 1] = w_sc * s1 / n;
+    reg_log_scale[3 * i + 2] = w_sc * s2 / n;
+    ta += a;
+    ts += (s0 + s1) + s2;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ta += __shfl_xor_sync(0xffffffffu, ta, o);
+    ts += __shfl_xor_sync(0xffffffffu, ts, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s[0][threadIdx.x >> 5] = ta;
+    s[1][threadIdx.x >> 5] = ts;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += s[0][w];
+      b += s[1][w];
+    }
+    terms[0] = w_op * (a / n);
+    terms[1] = w_sc * (b / n);
+  }
+}
+
 }  // namespace ss
 
 using namespace ss;
+
+extern "C" int ss_reg_grads(const double* alpha, const double* scales, int32_t n, double w_op,
+                            double w_sc, double* reg_logit, double* reg_log_scale, double* terms,
+                            cudaStream_t stream) {
+  if (n < 0 || !terms) return set_error(SS_ERR_INVALID, "ss_reg_grads: bad arguments");
+  if (n == 0) {
+    memzero(terms, 2 * sizeof(double), stream);
+    return check_launch("ss_reg_grads");
+  }
+  launch_k(reg_grads_kernel, 1, 1024, 0, stream, alpha, scales, n, w_op, w_sc, reg_logit,
+           reg_log_scale, terms);
+  return check_launch("ss_reg_grads");
+}
 
 extern "C" size_t ss_loss_workspace_bytes(int32_t width, int32_t height) {
   size_t plane = (size_t)width * height;

@@ -442,6 +442,26 @@ __global__ void __launch_bounds__(128, SS_PROJ_BWD_MINB) project_bwd_kernel(Stor
   out[13] = gg[8];
 }
 
+__global__ void project_splats_kernel(StoreView store, const int32_t* __restrict__ rows,
+                                      int32_t n, CamK cam, double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Gauss64 g;
+  load_row(store, rows ? rows[i] : i, g);
+  Proj p;
+  project_one(cam, g, p);
+  double* o = out + (int64_t)i * 7;
+  o[0] = p.ux;
+  o[1] = p.uy;
+  o[2] = p.a;
+  o[3] = p.b;
+  o[4] = p.c;
+  o[5] = p.z;
+  o[6] = p.keep ? 1.0 : 0.0;
+}
+
 __global__ void to_direct_kernel(const double* __restrict__ src, double* __restrict__ dst,
                                  int64_t n) {
   pdl_wait();
@@ -513,6 +533,16 @@ extern "C" int ss_project_bwd(const ss_store* store, const int32_t* rows, int32_
                                                             depth_key, trainable_mask,
                                                             trainable_rows, grads);
   return check_launch("ss_project_bwd");
+}
+
+extern "C" int ss_project_splats(const ss_store* store, const int32_t* rows, int32_t n,
+                                 const ss_camera* cam, double* out, cudaStream_t stream) {
+  if (!store || !cam || n < 0 || (n > 0 && !out))
+    return set_error(SS_ERR_INVALID, "ss_project_splats: bad arguments");
+  if (n == 0) return SS_OK;
+  StoreView sv{store->opt, store->n_opt, store->mat};
+  launch_k(project_splats_kernel, grid_for(n, 128), 128, 0, stream, sv, rows, n, to_camk(cam), out);
+  return check_launch("ss_project_splats");
 }
 
 extern "C" int ss_to_direct(const double* src, double* dst, int64_t n, cudaStream_t stream) {

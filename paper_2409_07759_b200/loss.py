@@ -83,12 +83,22 @@ def loss(pred, gt, active_optimizable: GaussianArrays, ssim_weight: float = 0.2,
     reg = {"opacity_logit": np.zeros((n,)), "log_scale": np.zeros((n, 3))}
     opacity_term = scale_term = 0.0
     if n > 0:
-        alpha = active_optimizable.opacities
-        scales = active_optimizable.scales
-        opacity_term = opacity_reg * float(np.mean(alpha))
-        scale_term = scale_reg * float(np.mean(np.sum(scales, axis=1)))
-        reg["opacity_logit"] = opacity_reg * alpha * (1.0 - alpha) / n
-        reg["log_scale"] = scale_reg * scales / n
+        # loss.py:105-111 on the GPU (ss_reg_grads)
+        from . import _lib as L
+
+        alpha = torch.from_numpy(np.ascontiguousarray(active_optimizable.opacities,
+                                                      dtype=np.float64)).to(dev)
+        scales = torch.from_numpy(np.ascontiguousarray(active_optimizable.scales,
+                                                       dtype=np.float64)).to(dev)
+        rl = torch.empty(n, dtype=torch.float64, device=dev)
+        rs = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        terms = torch.empty(2, dtype=torch.float64, device=dev)
+        L.check(L.lib().ss_reg_grads(L.ptr(alpha), L.ptr(scales), n, float(opacity_reg),
+                                     float(scale_reg), L.ptr(rl), L.ptr(rs), L.ptr(terms),
+                                     L.stream_ptr()), "reg_grads")
+        opacity_term, scale_term = (float(x) for x in terms.cpu().numpy())
+        reg["opacity_logit"] = rl.cpu().numpy()
+        reg["log_scale"] = rs.cpu().numpy()
     total = photometric + opacity_term + scale_term
     return (LossBreakdown(total=total, l1=l1, ssim=ssim_val, photometric=photometric,
                           opacity_term=opacity_term, scale_term=scale_term), grad_image, reg)

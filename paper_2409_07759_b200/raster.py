@@ -14,6 +14,7 @@ blending and its backward run in fp32.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 from typing import Optional, Sequence, Tuple
@@ -165,30 +166,21 @@ def render_arrays_backward(camera: Camera, arrays: GaussianArrays, grad_image: n
 
 
 def project(gaussian: Gaussian, camera: Camera) -> Optional[Splat2D]:
-    """Project one splat; None when culled (raster.py:176-191).  fp64 on the
-    host: this is a one-splat convenience, not the batched path."""
-    R = camera.rotation
-    t = R @ gaussian.mean + camera.translation
-    z = float(t[2])
-    if not z > NEAR_PLANE:
-        return None
-    u = np.array([camera.fx * t[0] / z + camera.cx, camera.fy * t[1] / z + camera.cy])
-    from .core import quat_to_rotmat
+    """Project one splat; None when culled (raster.py:176-191), through
+    ss_project_splats (the same fp64 sequence as the batched projection)."""
+    from . import _lib as L
 
-    rot = quat_to_rotmat(gaussian.rotation / max(np.linalg.norm(gaussian.rotation), 1e-12))
-    m3 = rot * gaussian.scale[None, :]
-    sigma = m3 @ m3.T
-    jac = np.array([[camera.fx / z, 0.0, -camera.fx * t[0] / (z * z)],
-                    [0.0, camera.fy / z, -camera.fy * t[1] / (z * z)]])
-    mp = jac @ R
-    cov = mp @ sigma @ mp.T
-    a, b, c = cov[0, 0], cov[0, 1], cov[1, 1]
-    mid = 0.5 * (a + c)
-    r3 = 3.0 * math.sqrt(max(mid + math.sqrt(max(mid * mid - (a * c - b * b), 0.0)), 0.0))
-    if (u[0] + r3 < 0.0 or u[0] - r3 > camera.width - 1.0 or u[1] + r3 < 0.0
-            or u[1] - r3 > camera.height - 1.0):
+    arr = GaussianArrays.from_gaussians([gaussian])
+    rows = torch.from_numpy(arr.rows()).to(device())
+    out = torch.empty((1, 7), dtype=torch.float64, device=device())
+    store = Store(opt=None, mat=rows)
+    cam = L.camera_struct(camera)
+    L.check(L.lib().ss_project_splats(ctypes.byref(store.struct()), None, 1, ctypes.byref(cam),
+                                      L.ptr(out), L.stream_ptr()), "project_splats")
+    u, v, a, b, c, z, kept = out[0].cpu().numpy()
+    if kept == 0.0:
         return None
-    return Splat2D(mean2d=u, cov2d=np.array([[a, b], [b, c]]), depth=z,
+    return Splat2D(mean2d=np.array([u, v]), cov2d=np.array([[a, b], [b, c]]), depth=float(z),
                    color=gaussian.color.copy(), opacity=float(gaussian.opacity), source_index=0)
 
 

@@ -537,3 +537,40 @@ def test_alpha_floor_error_bound_on_deep_translucent_stack(ss):
     assert ref["t_final"].min() > 1e-4      # nothing saturates
     img = R.render_arrays(cam, arr).pixels
     assert np.abs(img - ref["image"]).max() <= IMG_TOL
+
+
+def test_project_one_splat_api(ss):
+    """raster.project (one splat, raster.py:176-191) through ss_project_splats:
+    the reference's fp64 formulas for centre, raw covariance and depth
+    (test_raster.py:64-117 style: on-axis, isotropic, culled cases)."""
+    P, R = ss
+    cam = P.Camera(128, 96, 100.0, 110.0, 64.0, 48.0, np.eye(3), np.zeros(3))
+    g = P.Gaussian([0.0, 0.0, 3.0], [1, 0, 0, 0], [0.05] * 3, 0.5, [0.2, 0.3, 0.4])
+    sp = R.project(g, cam)
+    np.testing.assert_allclose(sp.mean2d, [64.0, 48.0], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(sp.cov2d, np.diag([(100 * 0.05 / 3) ** 2, (110 * 0.05 / 3) ** 2]),
+                               rtol=1e-12)
+    assert sp.depth == 3.0 and sp.opacity == 0.5
+    assert R.project(P.Gaussian([0.0, 0.0, -1.0], [1, 0, 0, 0], [0.05] * 3, 0.5, [0, 0, 0]),
+                     cam) is None                      # behind the camera
+    assert R.project(P.Gaussian([50.0, 0.0, 3.0], [1, 0, 0, 0], [0.05] * 3, 0.5, [0, 0, 0]),
+                     cam) is None                      # outside the 3-sigma cull
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        mean = rng.uniform([-0.3, -0.3, 2.0], [0.3, 0.3, 4.0])
+        s = rng.uniform(0.01, 0.1, 3)
+        rot = np.array([[0.96, -0.28, 0.0], [0.28, 0.96, 0.0], [0.0, 0.0, 1.0]])
+        cam2 = P.Camera(128, 96, 100.0, 110.0, 64.0, 48.0, rot, np.array([0.05, -0.02, 0.1]))
+        sp = R.project(P.Gaussian(mean, q, s, 0.7, [0.5] * 3), cam2)
+        t = rot @ mean + cam2.translation
+        from paper_2409_07759_b200.core import quat_to_rotmat
+        m3 = quat_to_rotmat(q) * s[None, :]
+        J = np.array([[100.0 / t[2], 0, -100.0 * t[0] / t[2] ** 2],
+                      [0, 110.0 / t[2], -110.0 * t[1] / t[2] ** 2]]) @ rot
+        cov = J @ (m3 @ m3.T) @ J.T
+        np.testing.assert_allclose(sp.mean2d, [100 * t[0] / t[2] + 64, 110 * t[1] / t[2] + 48],
+                                   rtol=1e-12)
+        np.testing.assert_allclose(sp.cov2d, cov, rtol=1e-10, atol=1e-14)
+        assert sp.depth == pytest.approx(t[2], rel=1e-15)
