@@ -483,6 +483,9 @@ __device__ __forceinline__ int nth_set_bit(uint64_t mask, int j) {
   return pos;
 }
 
+// pairs a warp stages per 32-splat batch in the emit's common path
+constexpr int kEmitStage = 512;
+
 __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
     const int32_t* __restrict__ order, const int32_t* __restrict__ offsets,
     const int4* __restrict__ bbox, const float* __restrict__ geom,
@@ -491,7 +494,9 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
     int32_t* __restrict__ counts) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ int32_t s_hist[];
+  extern __shared__ int32_t s_hist[];  // n_tiles counts, then the warps' stages
+  int32_t* stage_v = s_hist + ((n_tiles + 3) & ~3);
+  uint16_t* stage_t = reinterpret_cast<uint16_t*>(stage_v + kBinWarps * kEmitStage);
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_hist[t] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -525,6 +530,37 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
     }
     const int excl = incl - nm;
     const int P = __shfl_sync(0xffffffffu, incl, 31);
+    uint32_t far = __ballot_sync(0xffffffffu, total > 64);
+    if (!far && P <= kEmitStage) {
+      // common case: the batch's pairs are exactly its in-mask pairs, one
+      // contiguous emit range.  Each lane walks its own splat's mask bits
+      // (no per-pair search / shuffles) into the warp's shared stage, which
+      // the warp then writes out coalesced.
+      uint16_t* st_t = stage_t + warp * kEmitStage;
+      int32_t* st_v = stage_v + warp * kEmitStage;
+      int pos = excl;
+      uint64_t m = mask;
+      while (m) {
+        const int bit = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        const int r = div_small(bit, rw);
+        const int t = (ty0 + r) * tiles_x + tx0 + bit - r * w;
+        SS_DCHECK(t >= 0 && t < n_tiles && pos < kEmitStage);
+        st_t[pos] = (uint16_t)t;
+        st_v[pos] = i;
+        atomicAdd(&s_hist[t], 1);
+        ++pos;
+      }
+      __syncwarp();
+      const int obase = __shfl_sync(0xffffffffu, o0, 0);
+      SS_DCHECK(obase + P <= offsets[bounds[gridDim.x]]);
+      for (int p = lane; p < P; p += 32) {
+        keys[obase + p] = st_t[p];
+        vals[obase + p] = st_v[p];
+      }
+      __syncwarp();
+      continue;
+    }
     for (int q = 0; q < P; q += 32) {
       const int p = q + lane;
       int src = 0;  // last lane with excl <= p
@@ -554,7 +590,6 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
     }
     // tiles past the 64-bit mask of large splats: splat by splat, lanes over
     // the bbox tiles, emit positions by ballot prefix (bbox order)
-    uint32_t far = __ballot_sync(0xffffffffu, total > 64);
     while (far) {
       const int src = __ffs(far) - 1;
       far &= far - 1;
@@ -960,15 +995,16 @@ int bin_tiles_with_order(const int32_t* order, const int32_t* offsets, const int
   int32_t* totals = (int32_t*)(w + align256((size_t)C * n_tiles * 4));
   int32_t* start = (int32_t*)((char*)totals + align256((size_t)n_tiles * 4));
   int32_t* bounds = (int32_t*)((char*)start + align256((size_t)n_tiles * 4));
-  const size_t smem = (size_t)n_tiles * 4;
+  const size_t smem = (size_t)n_tiles * 4;  // tile scan
+  const size_t smem_emit = (size_t)((n_tiles + 3) & ~3) * 4 + (size_t)kBinWarps * kEmitStage * 6;
   const size_t smem_scatter = (size_t)n_tiles * 12;
   int rc;
-  if ((rc = ensure_smem((const void*)bin_emit_kernel, smem)) ||
+  if ((rc = ensure_smem((const void*)bin_emit_kernel, smem_emit)) ||
       (rc = ensure_smem((const void*)bin_tile_scan_kernel, smem)) ||
       (rc = ensure_smem((const void*)bin_scatter_kernel, smem_scatter)))
     return rc;
   launch_k(bin_bounds_kernel, (32 * (C + 1) + 127) / 128, 128, 0, stream, offsets, n, C, bounds);
-  launch_k(bin_emit_kernel, C, kBinThreads, smem, stream, order, offsets, (const int4*)bbox, geom,
+  launch_k(bin_emit_kernel, C, kBinThreads, smem_emit, stream, order, offsets, (const int4*)bbox, geom,
                                                     tile_mask, bounds, n_tiles, tiles_x, keys,
                                                     vals, counts);
   launch_k(bin_col_scan_kernel, (n_tiles + 31) / 32, kBinThreads, 0, stream, counts, C, n_tiles, totals);
