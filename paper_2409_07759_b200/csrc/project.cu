@@ -165,7 +165,7 @@ __device__ __forceinline__ void project_basis_fast(const CamK& cam, const Gauss6
 // the exact kept-tile count and mask of its bbox, the depth key and the
 // rasterizer record (raster.cu: conic pre-scaled by kappa = -log2(e)/2 so
 // alpha G = 2^(kappa m + log2 alpha); alpha floored at 2^-100).
-__device__ __forceinline__ void write_record(int i, double ux, double uy, double i0, double i1,
+__device__ __forceinline__ int write_record(int i, double ux, double uy, double i0, double i1,
                                              double i2, int x0, int x1, int y0, int y1,
                                              double opacity, const double* color, uint64_t key,
                                              float4* __restrict__ rec_a, float4* __restrict__ rec_b,
@@ -212,6 +212,7 @@ __device__ __forceinline__ void write_record(int i, double ux, double uy, double
   rec_a[i] = make_float4((float)ux, (float)uy, (float)(kappa * i0), (float)(kappa * i1));
   rec_b[i] = make_float4((float)(kappa * i2), (float)l2a, (float)color[0], (float)color[1]);
   rec_c[i] = (float)color[2];
+  return nt;
 }
 
 __device__ __forceinline__ void write_culled(int i, float4* rec_a, float4* rec_b, float* rec_c,
@@ -226,15 +227,13 @@ __device__ __forceinline__ void write_culled(int i, float4* rec_a, float4* rec_b
   rec_c[i] = 0.f;
 }
 
-__global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ rows, int32_t n,
-                                   CamK cam, float4* __restrict__ rec_a,
-                                   float4* __restrict__ rec_b, float* __restrict__ rec_c,
-                                   uint64_t* __restrict__ depth_key, int4* __restrict__ bbox,
-                                   int32_t* __restrict__ n_tiles, float* __restrict__ geom,
-                                   uint64_t* __restrict__ tile_mask, int lf) {
-  pdl_wait();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+// One splat of the projection; returns its kept-tile count (0 when culled).
+__device__ __forceinline__ int project_splat(const StoreView& store, const int32_t* __restrict__ rows,
+                                             int i, const CamK& cam, float4* __restrict__ rec_a,
+                                             float4* __restrict__ rec_b, float* __restrict__ rec_c,
+                                             uint64_t* __restrict__ depth_key, int4* __restrict__ bbox,
+                                             int32_t* __restrict__ n_tiles, float* __restrict__ geom,
+                                             uint64_t* __restrict__ tile_mask, int lf) {
   const int32_t row = rows ? rows[i] : i;
   Gauss64 g;
   load_row(store, row, g);
@@ -242,7 +241,7 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
   project_one(cam, g, p);
   if (!p.keep) {
     write_culled(i, rec_a, rec_b, rec_c, depth_key, bbox, n_tiles, tile_mask);
-    return;
+    return 0;
   }
   // raster.py:139-150  dilation, conic, 8-sigma bbox of the dilated covariance
   const double ad = dadd(p.a, kDilation), cd = dadd(p.c, kDilation);
@@ -256,9 +255,52 @@ __global__ void project_fwd_kernel(StoreView store, const int32_t* __restrict__ 
   const int y0 = (int)fmax(ceil(dsub(p.uy, r8)), 0.0);
   const int y1 = (int)fmin(dadd(floor(dadd(p.uy, r8)), 1.0), (double)cam.height);
   // z > 0.01: the fp64 bits are monotone
-  write_record(i, p.ux, p.uy, i0, i1, i2, x0, x1, y0, y1, g.opacity, g.color,
-               (uint64_t)__double_as_longlong(p.z), rec_a, rec_b, rec_c, depth_key, bbox, n_tiles,
-               geom, tile_mask, lf);
+  return write_record(i, p.ux, p.uy, i0, i1, i2, x0, x1, y0, y1, g.opacity, g.color,
+                      (uint64_t)__double_as_longlong(p.z), rec_a, rec_b, rec_c, depth_key, bbox,
+                      n_tiles, geom, tile_mask, lf);
+}
+
+// kp.out != nullptr: the kernel also sums the kept-tile counts -- per-CTA
+// partial, one atomic add per CTA, and the last CTA (done counter) writes
+// K = sum to kp.out and, with a system-scope store, (seq, K) to the host
+// word the view driver polls (what a separate sum kernel did; integer sums,
+// so the result does not depend on the CTA order), then re-arms both words.
+__global__ void __launch_bounds__(128) project_fwd_kernel(StoreView store, const int32_t* __restrict__ rows, int32_t n,
+                                   CamK cam, float4* __restrict__ rec_a,
+                                   float4* __restrict__ rec_b, float* __restrict__ rec_c,
+                                   uint64_t* __restrict__ depth_key, int4* __restrict__ bbox,
+                                   int32_t* __restrict__ n_tiles, float* __restrict__ geom,
+                                   uint64_t* __restrict__ tile_mask, int lf, KPublish kp) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int nt = 0;
+  if (i < n)
+    nt = project_splat(store, rows, i, cam, rec_a, rec_b, rec_c, depth_key, bbox, n_tiles, geom,
+                       tile_mask, lf);
+  if (!kp.out) return;
+  __shared__ int s_part[4];
+  __shared__ bool s_last;
+  const int wsum = __reduce_add_sync(0xffffffffu, nt);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = wsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int bsum = s_part[0] + s_part[1] + s_part[2] + s_part[3];
+    atomicAdd(&kp.acc_done[0], (unsigned int)bsum);
+    __threadfence();
+    s_last = atomicAdd(&kp.acc_done[1], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    const int32_t K = (int32_t)atomicAdd(&kp.acc_done[0], 0u);
+    *kp.out = K;
+    kp.acc_done[0] = 0u;  // re-armed before the host can see K and launch the next view
+    kp.acc_done[1] = 0u;
+    __threadfence();
+    *(volatile unsigned long long*)kp.host =
+        ((unsigned long long)kp.seq << 32) | (unsigned long long)(uint32_t)K;
+    __threadfence_system();
+  }
 }
 
 // _kernels.blend_forward's inputs (already projected 2D splats, the blend
@@ -281,7 +323,7 @@ __global__ void records2d_kernel(const double* __restrict__ mean2d, const double
   }
   const int4 b = bbox_in[i];
   const int x0 = max(b.x, 0), x1 = min(b.y, width), y0 = max(b.z, 0), y1 = min(b.w, height);
-  write_record(i, mean2d[2 * i], mean2d[2 * i + 1], inv2d[3 * i], inv2d[3 * i + 1], inv2d[3 * i + 2],
+  (void)write_record(i, mean2d[2 * i], mean2d[2 * i + 1], inv2d[3 * i], inv2d[3 * i + 1], inv2d[3 * i + 2],
                x0, max(x0, x1), y0, max(y0, y1), alpha[i], color + 3 * i,
                // rank as a positive double key (same form as fp64 z bits)
                (uint64_t)__double_as_longlong(1.0 + (double)rank[i] * 0x1p-22), rec_a,
@@ -483,19 +525,28 @@ __global__ void to_direct_kernel(const double* __restrict__ src, double* __restr
 
 using namespace ss;
 
-extern "C" int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_t n,
-                              const ss_camera* cam, void* rec_a, void* rec_b, float* rec_c,
-                              uint64_t* depth_key, int32_t* bbox, int32_t* n_tiles,
-                              float* geom, uint64_t* tile_mask, cudaStream_t stream) {
+int project_fwd_publish(const ss_store* store, const int32_t* rows, int32_t n,
+                        const ss_camera* cam, void* rec_a, void* rec_b, float* rec_c,
+                        uint64_t* depth_key, int32_t* bbox, int32_t* n_tiles, float* geom,
+                        uint64_t* tile_mask, const KPublish* kp, cudaStream_t stream) {
   if (!store || !cam || n < 0) return set_error(SS_ERR_INVALID, "ss_project_fwd: bad arguments");
   if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0) || !(cam->fy > 0))
     return set_error(SS_ERR_INVALID, "ss_project_fwd: bad camera");
   if (n == 0) return SS_OK;
   StoreView sv{store->opt, store->n_opt, store->mat};
-  launch_k(project_fwd_kernel, grid_for(n, 128), 128, 0, stream, 
+  const KPublish none{nullptr, nullptr, nullptr, 0u};
+  launch_k(project_fwd_kernel, grid_for(n, 128), 128, 0, stream,
       sv, rows, n, to_camk(cam), (float4*)rec_a, (float4*)rec_b, rec_c, depth_key, (int4*)bbox,
-      n_tiles, geom, tile_mask, (int)alpha_floor_log2());
+      n_tiles, geom, tile_mask, (int)alpha_floor_log2(), kp ? *kp : none);
   return check_launch("ss_project_fwd");
+}
+
+extern "C" int ss_project_fwd(const ss_store* store, const int32_t* rows, int32_t n,
+                              const ss_camera* cam, void* rec_a, void* rec_b, float* rec_c,
+                              uint64_t* depth_key, int32_t* bbox, int32_t* n_tiles,
+                              float* geom, uint64_t* tile_mask, cudaStream_t stream) {
+  return project_fwd_publish(store, rows, n, cam, rec_a, rec_b, rec_c, depth_key, bbox, n_tiles,
+                             geom, tile_mask, nullptr, stream);
 }
 
 extern "C" int ss_records_2d(const ss_splats2d* sp, int32_t width, int32_t height, void* rec_a,

@@ -291,6 +291,20 @@ int raster_bwd_det_ex(const int32_t* ranges, const int32_t* vals, const void* re
                       int32_t* rank, float* partial, float* g2d, const uint32_t* used,
                       cudaStream_t stream);
 bool raster_masks_usable();
+// project.cu: ss_project_fwd that also publishes K = sum of the kept-tile
+// counts (kp: K's device slot, the host-mapped (seq, K) word, two re-armed
+// device counters) -- the view driver's pair-count readback without a
+// separate sum kernel
+struct KPublish {
+  int32_t* out;
+  unsigned long long* host;
+  unsigned int* acc_done;
+  uint32_t seq;
+};
+int project_fwd_publish(const ss_store* store, const int32_t* rows, int32_t n,
+                        const ss_camera* cam, void* rec_a, void* rec_b, float* rec_c,
+                        uint64_t* depth_key, int32_t* bbox, int32_t* n_tiles, float* geom,
+                        uint64_t* tile_mask, const KPublish* kp, cudaStream_t stream);
 // binning.cu: ss_bin_tiles + the raster launch order from the same tile scan
 int bin_tiles_with_order(const int32_t* order, const int32_t* offsets, const int32_t* bbox,
                          const float* geom, const uint64_t* tile_mask, int32_t n,

@@ -119,7 +119,6 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
     v->ws_needed = need_ws;
     return set_error(SS_ERR_WORKSPACE, "ss_render_fwd: workspace %zu < %zu", v->ws_bytes, need_ws);
   }
-  if ((rc = make_records())) return rc;
   // K = sum of the per-splat tile counts, read back early: the host waits on
   // it (to size the binning) while the GPU runs the depth sort and offsets.
   // It is parked in offsets[n], which ss_tile_offsets rewrites with K.
@@ -139,8 +138,9 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   KRead& kr = k_tab[devid];
   if (!kr.host) {
     if (cudaHostAlloc(&kr.host, sizeof(unsigned long long), cudaHostAllocMapped) != cudaSuccess ||
-        cudaMalloc(&kr.partial, kSumBlocks * sizeof(int32_t) + sizeof(unsigned int)) != cudaSuccess ||
-        cudaMemsetAsync(kr.partial, 0, kSumBlocks * sizeof(int32_t) + sizeof(unsigned int),
+        cudaMalloc(&kr.partial, kSumBlocks * sizeof(int32_t) + 4 * sizeof(unsigned int)) !=
+            cudaSuccess ||
+        cudaMemsetAsync(kr.partial, 0, kSumBlocks * sizeof(int32_t) + 4 * sizeof(unsigned int),
                         stream) != cudaSuccess)
       return check_launch("ss_render_fwd: pair count readback");
     kr.done = reinterpret_cast<unsigned int*>(kr.partial + kSumBlocks);
@@ -150,8 +150,14 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   // earlier (abandoned) view can never be taken for this view's K
   volatile unsigned long long* k_poll = kr.host;
   const uint32_t seq = ++kr.seq;
-  launch_k(sum_kernel, std::max(1, std::min(kSumBlocks, (n + 255) / 256)), 256, 0, stream,
-           (const int32_t*)v->n_tiles, n, v->offsets + n, kr.host, seq, kr.partial, kr.done);
+  // records (+ K for the 3D path: the projection publishes it); the 2D path
+  // sums the counts with sum_kernel
+  const KPublish kp{v->offsets + n, kr.host, kr.done + 1, seq};
+  bool published = false;
+  if ((rc = make_records(&kp, published))) return rc;
+  if (!published)
+    launch_k(sum_kernel, std::max(1, std::min(kSumBlocks, (n + 255) / 256)), 256, 0, stream,
+             (const int32_t*)v->n_tiles, n, v->offsets + n, kr.host, seq, kr.partial, kr.done);
   if ((rc = ss_depth_order(v->depth_key, n, v->order, v->ws, v->ws_bytes, stream))) return rc;
   if ((rc = ss_tile_offsets(v->order, v->n_tiles, n, v->offsets, v->ws, v->ws_bytes, stream)))
     return rc;
@@ -230,9 +236,12 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
 extern "C" int ss_render_fwd(const ss_store* store, const ss_camera* cam, ss_view* v,
                              cudaStream_t stream) {
   if (!store || !cam || !v || v->n < 0) return set_error(SS_ERR_INVALID, "ss_render_fwd: bad args");
-  return render_fwd_common(cam->width, cam->height, v, nullptr, [&]() {
-    return ss_project_fwd(store, v->rows, v->n, cam, v->rec_a, v->rec_b, v->rec_c, v->depth_key,
-                          v->bbox, v->n_tiles, v->geom, v->tile_mask, stream);
+  return render_fwd_common(cam->width, cam->height, v, nullptr,
+                           [&](const KPublish* kp, bool& published) {
+    published = true;
+    return project_fwd_publish(store, v->rows, v->n, cam, v->rec_a, v->rec_b, v->rec_c,
+                               v->depth_key, v->bbox, v->n_tiles, v->geom, v->tile_mask, kp,
+                               stream);
   }, stream);
 }
 
@@ -240,7 +249,8 @@ extern "C" int ss_render2d_fwd(const ss_splats2d* sp, int32_t width, int32_t hei
                                cudaStream_t stream) {
   if (!sp || !v || sp->n < 0) return set_error(SS_ERR_INVALID, "ss_render2d_fwd: bad args");
   v->n = sp->n;
-  return render_fwd_common(width, height, v, v->bbox, [&]() {
+  return render_fwd_common(width, height, v, v->bbox, [&](const KPublish*, bool& published) {
+    published = false;
     return ss_records_2d(sp, width, height, v->rec_a, v->rec_b, v->rec_c, v->depth_key, v->bbox,
                          v->n_tiles, v->geom, v->tile_mask, stream);
   }, stream);
