@@ -1078,6 +1078,39 @@ __global__ void __launch_bounds__(1024) tile_order_bucket_kernel(const int2* __r
   }
 }
 
+// The same counting sort keyed by a per-tile work count (the backward's
+// walked entries, accumulated by the forward).
+__global__ void __launch_bounds__(1024) tile_order_work_kernel(const int32_t* __restrict__ work,
+                                                               int n_tiles,
+                                                               int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int hist[kBuckets];
+  __shared__ int cursor[kBuckets];
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&hist[len_bucket(work[t])], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < kBuckets; ++b) {
+      cursor[b] = acc;
+      acc += hist[b];
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
+    out[atomicAdd(&cursor[len_bucket(work[t])], 1)] = t;
+}
+
+int tile_order_from_work(const int32_t* work, int32_t n_tiles, int32_t* tile_order,
+                         cudaStream_t stream) {
+  if (n_tiles <= 0 || n_tiles > kOrderMax)
+    return set_error(SS_ERR_INVALID, "tile_order_from_work: %d tiles", n_tiles);
+  launch_k(tile_order_work_kernel, 1, 1024, 0, stream, work, n_tiles, tile_order);
+  return check_launch("tile_order_from_work");
+}
+
 static size_t tile_order_cub_bytes(int32_t n_tiles) {
   size_t b = 0;
   cub::DeviceRadixSort::SortPairsDescending(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr,

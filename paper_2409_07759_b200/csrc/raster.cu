@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(kWarpsF * 32)
                       float* __restrict__ img, float* __restrict__ t_final,
                       int32_t* __restrict__ n_contrib, float lfloor,
                       const int4* __restrict__ pbox = nullptr,
-                      uint32_t* __restrict__ used = nullptr) {
+                      uint32_t* __restrict__ used = nullptr,
+                      int32_t* __restrict__ tile_work = nullptr) {
   pdl_wait();
   pdl_trigger();
   __shared__ WarpStage s_stage[kWarpsF];
@@ -280,6 +281,15 @@ __global__ void __launch_bounds__(kWarpsF * 32)
       t_final[q] = h ? hi2(T[p]) : lo2(T[p]);
       n_contrib[q] = last[k];
     }
+  }
+  if (tile_work) {
+    // the entries this warp's backward will walk (its pixels' longest
+    // contributor prefix), summed per tile: the backward's launch order
+    int mx = 0;
+#pragma unroll
+    for (int k = 0; k < STRIP; ++k) mx = max(mx, last[k]);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0 && mx > 0) atomicAdd(&tile_work[tile], mx);
   }
 }
 
@@ -672,7 +682,7 @@ extern "C" int ss_set_raster_strips(int32_t strip_fwd, int32_t strip_bwd) {
 int raster_fwd_ex(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                   const void* rec_b, const float* rec_c, int32_t width, int32_t height,
                   const int32_t* tile_order, float* img, float* t_final, int32_t* n_contrib,
-                  const int32_t* pbox, uint32_t* used, cudaStream_t stream) {
+                  const int32_t* pbox, uint32_t* used, int32_t* tile_work, cudaStream_t stream) {
   if (width <= 0 || height <= 0) return set_error(SS_ERR_INVALID, "ss_raster_fwd: bad size");
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int n_tiles = tiles_x * tiles_y;
@@ -683,7 +693,7 @@ int raster_fwd_ex(const int32_t* ranges, const int32_t* vals, const void* rec_a,
   launch_k(raster_fwd_kernel<S, B>, blocks, kWarpsF * 32, 0, stream,                          \
       (const int2*)ranges, vals, (const float4*)rec_a, (const float4*)rec_b, rec_c, width,  \
       height, tiles_x, n_tiles, tile_order, img, t_final, n_contrib, floor_threshold(),     \
-      (const int4*)pbox, used)
+      (const int4*)pbox, used, tile_work)
   if (pbox) SS_FWD(4, true);
   else if (strip == 8) SS_FWD(8, false);
   else if (strip == 4) SS_FWD(4, false);
@@ -697,7 +707,7 @@ extern "C" int ss_raster_fwd(const int32_t* ranges, const int32_t* vals, const v
                              const int32_t* tile_order, float* img, float* t_final,
                              int32_t* n_contrib, cudaStream_t stream) {
   return raster_fwd_ex(ranges, vals, rec_a, rec_b, rec_c, width, height, tile_order, img, t_final,
-                       n_contrib, nullptr, nullptr, stream);
+                       n_contrib, nullptr, nullptr, nullptr, stream);
 }
 
 // Backward launch; det selects the deterministic partials, pbox the bbox

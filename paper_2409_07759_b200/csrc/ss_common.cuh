@@ -277,7 +277,10 @@ __device__ __forceinline__ double u01_53(uint32_t a, uint32_t b) {
 int raster_fwd_ex(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                   const void* rec_b, const float* rec_c, int32_t width, int32_t height,
                   const int32_t* tile_order, float* img, float* t_final, int32_t* n_contrib,
-                  const int32_t* pbox, uint32_t* used, cudaStream_t stream);
+                  const int32_t* pbox, uint32_t* used, int32_t* tile_work, cudaStream_t stream);
+// binning.cu: longest-first tile order from per-tile work counts (one CTA)
+int tile_order_from_work(const int32_t* work, int32_t n_tiles, int32_t* tile_order,
+                         cudaStream_t stream);
 int raster_bwd_plain_ex(const int32_t* ranges, const int32_t* vals, const void* rec_a,
                         const void* rec_b, const float* rec_c, int32_t width, int32_t height,
                         const int32_t* tile_order, const float* dimg, const float* t_final,

@@ -226,9 +226,18 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   const bool masks = v->used && raster_masks_usable() &&
                      v->used_cap >= ss_raster_used_words(k_host, n_tiles);
   v->used_ok = masks ? 1 : 0;
+  // per-tile backward work (walked entries), accumulated by the forward into
+  // the binning workspace (dead once the lists exist); the backward then
+  // runs in that longest-first order (v->tile_order is rewritten after the
+  // forward has used it)
+  int32_t* tile_work = n_tiles <= (1 << 20) && v->ws_bytes >= sizeof(int32_t) * (size_t)n_tiles
+                           ? (int32_t*)v->ws
+                           : nullptr;
+  if (tile_work) memzero(tile_work, sizeof(int32_t) * (size_t)n_tiles, stream);
   record(v->events[0], stream);
   rc = raster_fwd_ex(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,
-                     v->t_final, v->n_contrib, pbox, masks ? v->used : nullptr, stream);
+                     v->t_final, v->n_contrib, pbox, masks ? v->used : nullptr, tile_work, stream);
+  if (!rc && tile_work) rc = tile_order_from_work(tile_work, n_tiles, v->tile_order, stream);
   record(v->events[1], stream);
   return rc;
 }
