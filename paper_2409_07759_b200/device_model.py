@@ -244,8 +244,13 @@ class DeviceModel:
         dp = self.state.dp
         sums = self.view_gradients(draws[rank], dataset,
                                    zero_grads=dp is not None and dp.world_size > 1)
-        if self.state.dp is not None:
-            self.state.dp.allreduce_grads(self.grads)
+        if dp is not None:
+            # only the stepped generations' rows are read by the step: reduce
+            # their contiguous span (generation i = rows [i sl, (i+1) sl))
+            gens = [i for i, st in enumerate(stepped) if st]
+            if gens:
+                lo, hi = gens[0] * self.sl, (gens[-1] + 1) * self.sl
+                dp.allreduce_grads(self.grads[lo:hi])
         self.apply_step(stepped, it)
         return sums
 
