@@ -223,7 +223,10 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
       (rc = ss_tile_order(v->ranges, n_tiles, v->tile_order, v->ws, v->ws_bytes, stream)))
     return rc;
   // entry-use masks for the backward when the caller gave room for them
-  const bool masks = v->used && raster_masks_usable() &&
+#ifndef SS_USE_MASKS
+#define SS_USE_MASKS 1
+#endif
+  const bool masks = SS_USE_MASKS && v->used && raster_masks_usable() &&
                      v->used_cap >= ss_raster_used_words(k_host, n_tiles);
   v->used_ok = masks ? 1 : 0;
   // per-tile backward work (walked entries), accumulated by the forward into
