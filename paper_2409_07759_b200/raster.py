@@ -118,6 +118,15 @@ def set_binning(mode: str = "counting") -> None:
     L.check(L.lib().ss_set_binning(modes[mode]), "set_binning")
 
 
+def set_strips(forward: int = 4, backward: int = 4) -> None:
+    """Pixels per lane of the raster kernels (2, 4 or 8; default 4): a warp
+    covers 16 x (2 strip) pixels.  A tuning knob; results are unchanged
+    within the fp32 tolerance (unequal strips disable the entry-use masks)."""
+    from . import _lib as L
+
+    L.check(L.lib().ss_set_raster_strips(int(forward), int(backward)), "set_raster_strips")
+
+
 def _upload(arrays: GaussianArrays) -> Store:
     rows = torch.from_numpy(arrays.rows()).to(device())
     return Store(opt=None, mat=rows)

@@ -574,3 +574,27 @@ def test_project_one_splat_api(ss):
                                    rtol=1e-12)
         np.testing.assert_allclose(sp.cov2d, cov, rtol=1e-10, atol=1e-14)
         assert sp.depth == pytest.approx(t[2], rel=1e-15)
+
+
+@pytest.mark.parametrize("strips", [(2, 2), (8, 8), (4, 2), (8, 4)])
+def test_raster_strips_vs_oracle(ss, strips):
+    """Every strip mapping (2 / 4 / 8 pixels per lane), equal and unequal
+    forward / backward strips (unequal: the entry-use masks are off), gives
+    the reference's image and gradients within tolerance."""
+    P, R = ss
+    arr = _synth_scene(P, 12_000, (300.0 / 20_000) ** (1 / 3), seed=14)
+    ocam = arc_camera(3, 6, 200, 152)
+    cam = cam_from(P, ocam)
+    gdir = np.random.default_rng(15).normal(size=(152, 200, 3))
+    try:
+        R.set_strips(*strips)
+        img = R.render_arrays(cam, arr).pixels
+        g = R.render_arrays_backward(cam, arr, gdir)
+    finally:
+        R.set_strips(4, 4)
+    ref = O.render_arrays(ocam, arr.means, arr.quats, arr.scales, arr.opacities, arr.colors,
+                          nthreads=8, tiled=True)
+    assert np.abs(img - ref).max() <= IMG_TOL
+    gref = O.render_arrays_backward(ocam, arr.means, arr.quats, arr.scales, arr.opacities,
+                                    arr.colors, gdir, tiled=True, nthreads=8)
+    grad_check(g, gref, what=f"strips {strips}")
