@@ -19,6 +19,10 @@
 // (full-rate FFMA with an immediate operand).
 #include "ss_common.cuh"
 
+#ifndef SS_SSIM_PDL
+#define SS_SSIM_PDL 1
+#endif
+
 namespace ss {
 
 constexpr int kLT = 32;               // output tile edge
@@ -473,8 +477,8 @@ extern "C" int ss_loss_l1_ssim(const float* pred, const uint8_t* gt_u8, const fl
   const size_t plane = (size_t)width * height;
   LossArgs a{pred, gt_u8, lut, gt_f32, width, height, (float*)ws,
              (double*)((char*)ws + ((9 * plane * sizeof(float) + 255) & ~(size_t)255))};
-  launch_k(ssim_fwd_kernel, grid, kLossThreads, 0, stream, a);
-  launch_k(ssim_bwd_kernel, grid, kLossThreads, 0, stream, a, (float)ssim_weight, dimg);
+  launch_kx(SS_SSIM_PDL, ssim_fwd_kernel, grid, kLossThreads, 0, stream, a);
+  launch_kx(SS_SSIM_PDL, ssim_bwd_kernel, grid, kLossThreads, 0, stream, a, (float)ssim_weight, dimg);
   launch_k(loss_reduce_kernel, 1, 1024, 0, stream, a.partials, grid.x * grid.y * grid.z, out_sums);
   return check_launch("ss_loss_l1_ssim");
 }

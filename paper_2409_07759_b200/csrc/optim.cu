@@ -4,6 +4,10 @@
 // library kernels: the relocation partition and scan are this file's own.
 #include "ss_common.cuh"
 
+#ifndef SS_ADAM_PDL
+#define SS_ADAM_PDL 1
+#endif
+
 namespace ss {
 
 struct HyperK {
@@ -512,7 +516,7 @@ extern "C" int ss_adam_sgld_step(double* opt, const float* grads, double* adam_m
   if (n_rows < 0 || rows_per_gen <= 0 || !hyper)
     return set_error(SS_ERR_INVALID, "ss_adam_sgld_step: bad arguments");
   if (n_rows == 0) return SS_OK;
-  launch_k(adam_sgld_kernel, grid_for(n_rows, 128), 128, 0, stream, 
+  launch_kx(SS_ADAM_PDL, adam_sgld_kernel, grid_for(n_rows, 128), 128, 0, stream,
       opt, grads, adam_m, adam_v, n_rows, rows_per_gen, gens, to_hyper(hyper), eta);
   return check_launch("ss_adam_sgld_step");
 }

@@ -4,6 +4,10 @@
 // the rasterizer record is rounded to fp32 once.
 #include "ss_common.cuh"
 
+#ifndef SS_PBWD_PDL
+#define SS_PBWD_PDL 1
+#endif
+
 namespace ss {
 
 struct CamK {
@@ -580,7 +584,7 @@ extern "C" int ss_project_bwd(const ss_store* store, const int32_t* rows, int32_
   if (!store || !cam || n < 0) return set_error(SS_ERR_INVALID, "ss_project_bwd: bad arguments");
   if (n == 0) return SS_OK;
   StoreView sv{store->opt, store->n_opt, store->mat};
-  launch_k(project_bwd_kernel, grid_for(n, 128), 128, 0, stream, sv, rows, n, to_camk(cam), g2d,
+  launch_kx(SS_PBWD_PDL, project_bwd_kernel, grid_for(n, 128), 128, 0, stream, sv, rows, n, to_camk(cam), g2d,
                                                             depth_key, trainable_mask,
                                                             trainable_rows, grads);
   return check_launch("ss_project_bwd");
