@@ -432,10 +432,13 @@ __global__ void bin_bounds_kernel(const int32_t* __restrict__ offsets, int32_t n
   // warp per boundary, 32-ary search: first k with offsets[k] >= target
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (c > n_chunks) return;
-  if (c == 0 || c == n_chunks) {
-    if (lane == 0) bounds[c] = c == 0 ? 0 : n;
+  if (c == 0) {
+    if (lane == 0) bounds[c] = 0;
     return;
   }
+  // c == n_chunks searches for K: the trailing ranks with no pair (the culled
+  // splats, whose depth key sorts last) belong to no chunk -- as the last
+  // chunk's tail they made one CTA walk up to ~25k empty ranks (config 5)
   const int64_t K = offsets[n];
   const int32_t target = (int32_t)(K * c / n_chunks);
   int lo = 0, hi = n;  // answer in [lo, hi]
@@ -483,7 +486,8 @@ __device__ __forceinline__ int nth_set_bit(uint64_t mask, int j) {
   return pos;
 }
 
-// pairs a warp stages per 32-splat batch in the emit's common path
+// pairs a warp stages per 32-splat batch in the emit's common path (at most;
+// the launch picks `stage` <= this so that the grid fits one wave, below)
 constexpr int kEmitStage = 512;
 
 __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
@@ -491,12 +495,12 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
     const int4* __restrict__ bbox, const float* __restrict__ geom,
     const uint64_t* __restrict__ tile_mask, const int32_t* __restrict__ bounds, int32_t n_tiles,
     int32_t tiles_x, uint16_t* __restrict__ keys, int32_t* __restrict__ vals,
-    int32_t* __restrict__ counts) {
+    int32_t* __restrict__ counts, int stage) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ int32_t s_hist[];  // n_tiles counts, then the warps' stages
   int32_t* stage_v = s_hist + ((n_tiles + 3) & ~3);
-  uint16_t* stage_t = reinterpret_cast<uint16_t*>(stage_v + kBinWarps * kEmitStage);
+  uint16_t* stage_t = reinterpret_cast<uint16_t*>(stage_v + kBinWarps * stage);
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_hist[t] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -531,13 +535,13 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
     const int excl = incl - nm;
     const int P = __shfl_sync(0xffffffffu, incl, 31);
     uint32_t far = __ballot_sync(0xffffffffu, total > 64);
-    if (!far && P <= kEmitStage) {
+    if (!far && P <= stage) {
       // common case: the batch's pairs are exactly its in-mask pairs, one
       // contiguous emit range.  Each lane walks its own splat's mask bits
       // (no per-pair search / shuffles) into the warp's shared stage, which
       // the warp then writes out coalesced.
-      uint16_t* st_t = stage_t + warp * kEmitStage;
-      int32_t* st_v = stage_v + warp * kEmitStage;
+      uint16_t* st_t = stage_t + warp * stage;
+      int32_t* st_v = stage_v + warp * stage;
       int pos = excl;
       uint64_t m = mask;
       while (m) {
@@ -545,7 +549,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
         m &= m - 1;
         const int r = div_small(bit, rw);
         const int t = (ty0 + r) * tiles_x + tx0 + bit - r * w;
-        SS_DCHECK(t >= 0 && t < n_tiles && pos < kEmitStage);
+        SS_DCHECK(t >= 0 && t < n_tiles && pos < stage);
         st_t[pos] = (uint16_t)t;
         st_v[pos] = i;
         atomicAdd(&s_hist[t], 1);
@@ -773,46 +777,80 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t* brow = base + (int64_t)c * n_tiles;
   const int q0 = offsets[bounds[c]], q1 = offsets[bounds[c + 1]];
-  // software pipelined: the next wave's pair is loaded while this one is placed
-  int q = q0 + threadIdx.x;
-  int t_next = q < q1 ? keys[q] : n_tiles;  // n_tiles: no tile
-  int32_t v_next = q < q1 ? vals[q] : 0;
-#pragma unroll 4
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    s_cur[t] = start[t] + brow[t];
-    s_wc[t] = 0ull;
+  // software pipelined: the pairs of the next kAhead waves are in flight
+  // while this one is placed (one wave of lookahead left the loop waiting
+  // on L2 latency: long_scoreboard was the top stall)
+  constexpr int kAhead = 4;
+  int tq[kAhead];
+  int32_t vq[kAhead];
+#pragma unroll
+  for (int d = 0; d < kAhead; ++d) {
+    const int q = q0 + d * kBinThreads + threadIdx.x;
+    tq[d] = q < q1 ? keys[q] : n_tiles;  // n_tiles: no tile
+    vq[d] = q < q1 ? vals[q] : 0;
+  }
+  // cursor init, 8 tiles per thread in flight (written as separate load
+  // and store phases: ptxas otherwise serialised load -> add -> store)
+  for (int t0 = threadIdx.x; t0 < n_tiles; t0 += 8 * kBinThreads) {
+    int32_t a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u * kBinThreads;
+      a[u] = t < n_tiles ? start[t] + brow[t] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u * kBinThreads;
+      if (t < n_tiles) {
+        s_cur[t] = a[u];
+        s_wc[t] = 0ull;
+      }
+    }
   }
   const uint32_t lt = (1u << lane) - 1u;
   const unsigned long long below_mask = (1ull << (8 * warp)) - 1ull;
   unsigned char* s_wc8 = reinterpret_cast<unsigned char*>(s_wc);
-  for (int qb = q0; qb < q1; qb += kBinThreads) {
-    const bool ok = qb + threadIdx.x < q1;
-    const int t = t_next;
-    const int32_t v = v_next;
-    q = qb + kBinThreads + threadIdx.x;
-    t_next = q < q1 ? keys[q] : n_tiles;
-    v_next = q < q1 ? vals[q] : 0;
-    const uint32_t peers = __match_any_sync(0xffffffffu, t);
-    const int leader = __ffs(peers) - 1;
-    const int cnt = __popc(peers), rin = __popc(peers & lt);
-    __syncthreads();  // previous wave's cursor updates / clears are done
-    if (ok && lane == leader) s_wc8[(size_t)t * 8 + warp] = (unsigned char)cnt;
-    __syncthreads();
-    int prefix = 0;
-    bool last = false;
-    if (ok) {
-      const unsigned long long word = s_wc[t];
-      // byte sum of the lower warps' counts (each <= 32, sum <= 224 < 256)
-      prefix = (int)(((word & below_mask) * 0x0101010101010101ull) >> 56);
-      last = warp == 7 || (word >> (8 * (warp + 1))) == 0ull;
-      SS_DCHECK(t >= 0 && t < n_tiles && s_cur[t] + prefix + rin >= start[t] &&
-                s_cur[t] + prefix + rin < (t + 1 < n_tiles ? start[t + 1] : offsets[bounds[gridDim.x]]));
-      out[s_cur[t] + prefix + rin] = v;
-    }
-    __syncthreads();
-    if (ok && lane == leader && last) {
-      s_cur[t] += prefix + cnt;
-      s_wc[t] = 0ull;
+  for (int qr = q0; qr < q1; qr += kAhead * kBinThreads) {
+#pragma unroll
+    for (int d = 0; d < kAhead; ++d) {
+      const int qb = qr + d * kBinThreads;
+      if (qb >= q1) break;  // uniform over the CTA
+      const bool ok = qb + threadIdx.x < q1;
+      const int t = tq[d];
+      const int32_t v = vq[d];
+      const uint32_t peers = __match_any_sync(0xffffffffu, t);
+      const int leader = __ffs(peers) - 1;
+      const int cnt = __popc(peers), rin = __popc(peers & lt);
+      __syncthreads();  // previous wave's cursor updates / clears are done
+      if (ok && lane == leader) s_wc8[(size_t)t * 8 + warp] = (unsigned char)cnt;
+      __syncthreads();
+      int prefix = 0;
+      bool last = false;
+      if (ok) {
+        const unsigned long long word = s_wc[t];
+        // byte sum of the lower warps' counts (each <= 32, sum <= 224 < 256)
+        prefix = (int)(((word & below_mask) * 0x0101010101010101ull) >> 56);
+        last = warp == 7 || (word >> (8 * (warp + 1))) == 0ull;
+        SS_DCHECK(t >= 0 && t < n_tiles && s_cur[t] + prefix + rin >= start[t] &&
+                  s_cur[t] + prefix + rin < (t + 1 < n_tiles ? start[t + 1] : offsets[bounds[gridDim.x]]));
+#ifdef SS_DIAG_SCATTER_NOSTORE
+        if (v == -12345) out[s_cur[t] + prefix + rin] = v;
+#else
+        out[s_cur[t] + prefix + rin] = v;
+#endif
+      }
+      __syncthreads();
+      if (ok && lane == leader && last) {
+        s_cur[t] += prefix + cnt;
+        s_wc[t] = 0ull;
+      }
+      // refill this slot only now that t and v are dead: the load can then
+      // target their registers (a refill at the top of the section made
+      // ptxas load into a temporary and MOV it back at the end -- a MOV
+      // that waited on the load, i.e. one wave of lookahead, not kAhead)
+      const int qn = qb + kAhead * kBinThreads + threadIdx.x;
+      tq[d] = qn < q1 ? keys[qn] : n_tiles;
+      vq[d] = qn < q1 ? vals[qn] : 0;
     }
   }
 }
@@ -950,6 +988,22 @@ static int bin_chunks(int64_t n_pairs, int n_tiles) {
   return (int)(c > kBinChunksCap ? kBinChunksCap : c);
 }
 
+// Stage entries per emit warp: the largest multiple of 32 (<= kEmitStage)
+// that lets the C emit CTAs run in ONE wave (a grid of 1.33 waves -- e.g. 592
+// chunks at 3 CTAs per SM at 1920x1080 -- leaves a quarter of the SMs
+// running a second chunk alone: 2x the kernel time).  Batches with more
+// pairs than the stage take the lane-per-pair path.  Below 256 entries the
+// full stage is kept (too many batches would fall off the fast path).
+static int emit_stage(int C, int n_tiles) {
+  const int per_sm = (C + 147) / 148;
+  const size_t hist = (size_t)((n_tiles + 3) & ~3) * 4;
+  if (per_sm > 4) return kEmitStage;  // the register limit (57 regs x 256 threads) is 4 CTAs/SM
+  const size_t per_cta = (size_t)228 * 1024 / per_sm - 1024;  // 1 KB reserved per CTA
+  if (per_cta <= hist) return kEmitStage;
+  const size_t s = (per_cta - hist) / ((size_t)kBinWarps * 6) / 32 * 32;
+  return s >= (size_t)kEmitStage ? kEmitStage : (s >= 256 ? (int)s : kEmitStage);
+}
+
 extern "C" size_t ss_bin_tiles_workspace_bytes(int64_t n_pairs, int32_t n_tiles) {
   const size_t nt = (size_t)(n_tiles > 0 ? n_tiles : 1);
   const size_t C = (size_t)bin_chunks(n_pairs, (int)nt);
@@ -996,7 +1050,8 @@ int bin_tiles_with_order(const int32_t* order, const int32_t* offsets, const int
   int32_t* start = (int32_t*)((char*)totals + align256((size_t)n_tiles * 4));
   int32_t* bounds = (int32_t*)((char*)start + align256((size_t)n_tiles * 4));
   const size_t smem = (size_t)n_tiles * 4;  // tile scan
-  const size_t smem_emit = (size_t)((n_tiles + 3) & ~3) * 4 + (size_t)kBinWarps * kEmitStage * 6;
+  const int stage = emit_stage(C, n_tiles);
+  const size_t smem_emit = (size_t)((n_tiles + 3) & ~3) * 4 + (size_t)kBinWarps * stage * 6;
   const size_t smem_scatter = (size_t)n_tiles * 12;
   int rc;
   if ((rc = ensure_smem((const void*)bin_emit_kernel, smem_emit)) ||
@@ -1006,7 +1061,7 @@ int bin_tiles_with_order(const int32_t* order, const int32_t* offsets, const int
   launch_k(bin_bounds_kernel, (32 * (C + 1) + 127) / 128, 128, 0, stream, offsets, n, C, bounds);
   launch_k(bin_emit_kernel, C, kBinThreads, smem_emit, stream, order, offsets, (const int4*)bbox, geom,
                                                     tile_mask, bounds, n_tiles, tiles_x, keys,
-                                                    vals, counts);
+                                                    vals, counts, stage);
   launch_k(bin_col_scan_kernel, (n_tiles + 31) / 32, kBinThreads, 0, stream, counts, C, n_tiles, totals);
   launch_k(bin_tile_scan_kernel, 1, 1024, (size_t)n_tiles * 4, stream, totals, n_tiles, start,
            (int2*)ranges, tile_order);
