@@ -297,38 +297,77 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, floa
   const float* m0 = a.maps + (0 * 3 + ch) * plane;
   const float* m1 = a.maps + (1 * 3 + ch) * plane;
   const float* m2 = a.maps + (2 * 3 + ch) * plane;
-  constexpr int kRW = (kLR + kWarpsL - 1) / kWarpsL;  // rows per warp
-  const int gx0 = x0 - kHalo + lane;
-  const bool col_in[2] = {(unsigned)gx0 < (unsigned)W,
-                          lane + 32 < kLR && (unsigned)(gx0 + 32) < (unsigned)W};
-  const int gy0 = y0 - kHalo + warp;
-  const int base = gy0 * W + gx0;
-  float u[kRW][2][3];
-#pragma unroll
-  for (int k = 0; k < kRW; ++k) {
-    const bool row_in = warp + kWarpsL * k < kLR && (unsigned)(gy0 + kWarpsL * k) < (unsigned)H;
-#pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const bool in = row_in && col_in[m];
-      const int e = base + k * kWarpsL * W + 32 * m;
-      u[k][m][0] = in ? m0[e] : 0.f;
-      u[k][m][1] = in ? m1[e] : 0.f;
-      u[k][m][2] = in ? m2[e] : 0.f;
-    }
-  }
   const int r = threadIdx.x / (kLT / kHC), c0 = (threadIdx.x % (kLT / kHC)) * kHC;
   const int gy = y0 + r;
   const int eo = (gy * W + x0 + c0) * 3 + ch;
-
+  if ((W & 3) == 0) {
+    // rows of 48 floats from x0 - 8 as 12 float4 (W % 4 == 0: a float4 is
+    // wholly inside or outside the image; tile origins are multiples of 32),
+    // every load of the thread issued before the first store.  Region
+    // column j (x0 - 5 + j) is float 3 + j of the row.  The scalar path's
+    // per-element address and bounds arithmetic was half the kernel.
+    constexpr int kQ = 12, kItems = kLR * kQ;  // 504 float4 per map
+    constexpr int kPer = (kItems + kLossThreads - 1) / kLossThreads;
+    float4 u[kPer][3];
 #pragma unroll
-  for (int k = 0; k < kRW; ++k) {
-    const int rr = warp + kWarpsL * k;
+    for (int it = 0; it < kPer; ++it) {
+      const int idx = threadIdx.x + it * kLossThreads;
+      const int rr = idx / kQ, qq = idx - rr * kQ;
+      const int gyy = y0 - kHalo + rr, gxx = x0 - 8 + 4 * qq;
+      const bool in = idx < kItems && (unsigned)gyy < (unsigned)H && (unsigned)gxx < (unsigned)W;
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int e = gyy * W + gxx;
+      u[it][0] = in ? *reinterpret_cast<const float4*>(m0 + e) : z;
+      u[it][1] = in ? *reinterpret_cast<const float4*>(m1 + e) : z;
+      u[it][2] = in ? *reinterpret_cast<const float4*>(m2 + e) : z;
+    }
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const int q = lane + 32 * m;
-      if (rr < kLR && q < kLR) {
-        s_m2[rr][q] = pk2(u[k][m][0], u[k][m][1]);
-        s_m1[rr][q] = u[k][m][2];
+    for (int it = 0; it < kPer; ++it) {
+      const int idx = threadIdx.x + it * kLossThreads;
+      if (idx >= kItems) continue;
+      const int rr = idx / kQ, qq = idx - rr * kQ;
+      const float a0[4] = {u[it][0].x, u[it][0].y, u[it][0].z, u[it][0].w};
+      const float a1[4] = {u[it][1].x, u[it][1].y, u[it][1].z, u[it][1].w};
+      const float a2[4] = {u[it][2].x, u[it][2].y, u[it][2].z, u[it][2].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = 4 * qq + j - 3;
+        if (col >= 0 && col < kLR) {
+          s_m2[rr][col] = pk2(a0[j], a1[j]);
+          s_m1[rr][col] = a2[j];
+        }
+      }
+    }
+  } else {
+    constexpr int kRW = (kLR + kWarpsL - 1) / kWarpsL;  // rows per warp
+    const int gx0 = x0 - kHalo + lane;
+    const bool col_in[2] = {(unsigned)gx0 < (unsigned)W,
+                            lane + 32 < kLR && (unsigned)(gx0 + 32) < (unsigned)W};
+    const int gy0 = y0 - kHalo + warp;
+    const int base = gy0 * W + gx0;
+    float u[kRW][2][3];
+#pragma unroll
+    for (int k = 0; k < kRW; ++k) {
+      const bool row_in = warp + kWarpsL * k < kLR && (unsigned)(gy0 + kWarpsL * k) < (unsigned)H;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const bool in = row_in && col_in[m];
+        const int e = base + k * kWarpsL * W + 32 * m;
+        u[k][m][0] = in ? m0[e] : 0.f;
+        u[k][m][1] = in ? m1[e] : 0.f;
+        u[k][m][2] = in ? m2[e] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kRW; ++k) {
+      const int rr = warp + kWarpsL * k;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int q = lane + 32 * m;
+        if (rr < kLR && q < kLR) {
+          s_m2[rr][q] = pk2(u[k][m][0], u[k][m][1]);
+          s_m1[rr][q] = u[k][m][2];
+        }
       }
     }
   }
