@@ -199,12 +199,31 @@ __device__ __forceinline__ int write_record(int i, double ux, double uy, double 
     for (int ty = ty0; ty < ty1; ++ty) {
       float L, R;
       if (!row_span(gl, ty, bb, L, R)) continue;
-      const int j0 = (ty - ty0) * w - tx0;
-      for (int tx = tx0; tx < tx1; ++tx) {
-        if (!col_meets(gl, tx, bb, L, R)) continue;
-        ++nt;
-        const int j = j0 + tx;
-        if (j < 64) mask |= 1ull << j;
+      // col_meets(tx) = (bx(tx) >= L) && (ax(tx) <= R) with the tile's
+      // clipped pixel-centre columns ax <= bx, both non-decreasing in tx
+      // (rounded subtraction of a fixed u is monotone): the kept tiles of
+      // the row are one run [a, b].  Its ends are estimated from L and R and
+      // settled with the exact tests -- the same decisions as testing every
+      // tile, without the per-tile loop.
+      const float u = gl[0];
+      const auto left_ok = [&](int tx) {  // bx(tx) >= L
+        return fsr((float)min(tx * kTile + kTile - 1, bb.y - 1), u) >= L;
+      };
+      const auto right_ok = [&](int tx) {  // ax(tx) <= R
+        return fsr((float)max(tx * kTile, bb.x), u) <= R;
+      };
+      int a = min(max((int)floorf((L + u - (float)(kTile - 1)) * (1.f / kTile)), tx0), tx1 - 1);
+      while (a > tx0 && left_ok(a - 1)) --a;
+      while (a < tx1 && !left_ok(a)) ++a;
+      int b = min(max((int)floorf((R + u) * (1.f / kTile)), tx0), tx1 - 1);
+      while (b < tx1 - 1 && right_ok(b + 1)) ++b;
+      while (b >= tx0 && !right_ok(b)) --b;
+      if (a > b) continue;
+      nt += b - a + 1;
+      const int ja = (ty - ty0) * w + (a - tx0);
+      if (ja < 64) {
+        const int nb = min(b - a + 1, 64 - ja);
+        mask |= (nb >= 64 ? ~0ull : ((1ull << nb) - 1ull)) << ja;
       }
     }
   }
