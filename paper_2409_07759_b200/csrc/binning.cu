@@ -419,6 +419,11 @@ __global__ void tile_len_kernel(const int2* __restrict__ ranges, int n_tiles,
 //            in that tile), ranked stably inside the wave (see below).
 // Chunks are rank ranges laid out in chunk order inside every tile list and
 // each step is stable, so the lists equal the stable global pair sort's.
+// equal-tile lanes by a ballot per tile-id bit instead of __match_any
+// (whose result latency was the scatter's top short-scoreboard stall)
+#ifndef SS_SCATTER_BALLOT_MATCH
+#define SS_SCATTER_BALLOT_MATCH 1
+#endif
 constexpr int kBinThreads = 256;
 constexpr int kBinWarps = kBinThreads / 32;
 
@@ -810,6 +815,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(
   const uint32_t lt = (1u << lane) - 1u;
   const unsigned long long below_mask = (1ull << (8 * warp)) - 1ull;
   unsigned char* s_wc8 = reinterpret_cast<unsigned char*>(s_wc);
+  const int tbits = 32 - __clz(n_tiles);  // t <= n_tiles (n_tiles: no tile)
   for (int qr = q0; qr < q1; qr += kAhead * kBinThreads) {
 #pragma unroll
     for (int d = 0; d < kAhead; ++d) {
@@ -818,7 +824,15 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(
       const bool ok = qb + threadIdx.x < q1;
       const int t = tq[d];
       const int32_t v = vq[d];
+#if SS_SCATTER_BALLOT_MATCH
+      uint32_t peers = 0xffffffffu;  // lanes with the same t, by ballots over t's bits
+      for (int b = 0; b < tbits; ++b) {
+        const uint32_t ones = __ballot_sync(0xffffffffu, (t >> b) & 1);
+        peers &= ((t >> b) & 1) ? ones : ~ones;
+      }
+#else
       const uint32_t peers = __match_any_sync(0xffffffffu, t);
+#endif
       const int leader = __ffs(peers) - 1;
       const int cnt = __popc(peers), rin = __popc(peers & lt);
       __syncthreads();  // previous wave's cursor updates / clears are done
