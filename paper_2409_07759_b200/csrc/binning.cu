@@ -547,13 +547,17 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
       // the warp then writes out coalesced.
       uint16_t* st_t = stage_t + warp * stage;
       int32_t* st_v = stage_v + warp * stage;
+      // 32-bit halves of the mask; tile = t0 + bit + r (tiles_x - w) with
+      // r = bit / w by the float reciprocal
       int pos = excl;
-      uint64_t m = mask;
-      while (m) {
-        const int bit = __ffsll((long long)m) - 1;
-        m &= m - 1;
-        const int r = div_small(bit, rw);
-        const int t = (ty0 + r) * tiles_x + tx0 + bit - r * w;
+      uint32_t mlo = (uint32_t)mask, mhi = (uint32_t)(mask >> 32);
+      const int t0 = ty0 * tiles_x + tx0, dt = tiles_x - w;
+      while (mlo | mhi) {
+        const bool in_lo = mlo != 0;
+        const uint32_t cur = in_lo ? mlo : mhi;
+        const int bit = (in_lo ? 0 : 32) + __ffs(cur) - 1;
+        if (in_lo) mlo &= mlo - 1u; else mhi &= mhi - 1u;
+        const int t = t0 + bit + div_small(bit, rw) * dt;
         SS_DCHECK(t >= 0 && t < n_tiles && pos < stage);
         st_t[pos] = (uint16_t)t;
         st_v[pos] = i;
