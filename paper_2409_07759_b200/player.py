@@ -50,6 +50,7 @@ class _Slot:
         self._arrays = arrays
         self._make = make_arrays
         self.valid = valid
+        self.n_valid = int(np.count_nonzero(valid))  # counted once, not per rendered frame
         self.lifespan = lifespan
 
     @property
@@ -219,7 +220,7 @@ class PlayerBuffer:
         with self._lock:
             frame = self.frame if frame is None else frame
             order = self._order(frame)
-            n = sum(int(self.slots[i].valid.sum()) for i in order)
+            n = sum(self.slots[i].n_valid for i in order)
             return dev.render(order, n, frame, camera)
 
 
