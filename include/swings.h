@@ -366,7 +366,8 @@ typedef struct {
                         /*   reached each warp's pixels, the backward walks only those */
   int64_t used_cap;     /* words in used                                               */
   int32_t used_ok;      /* out (forward): masks valid for this view's backward         */
-  int32_t pad2;
+  int32_t fwd_only;     /* in: 1 = no backward follows (playback): the forward skips  */
+                        /*   the backward's aids (entry-use masks, per-tile work order) */
 } ss_view;
 
 /* Projection -> depth order -> tile offsets -> [one stream sync for K] ->

@@ -226,14 +226,15 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
 #ifndef SS_USE_MASKS
 #define SS_USE_MASKS 1
 #endif
-  const bool masks = SS_USE_MASKS && v->used && raster_masks_usable() &&
+  const bool masks = SS_USE_MASKS && !v->fwd_only && v->used && raster_masks_usable() &&
                      v->used_cap >= ss_raster_used_words(k_host, n_tiles);
   v->used_ok = masks ? 1 : 0;
   // per-tile backward work (walked entries), accumulated by the forward into
   // the binning workspace (dead once the lists exist); the backward then
   // runs in that longest-first order (v->tile_order is rewritten after the
   // forward has used it)
-  int32_t* tile_work = n_tiles <= (1 << 20) && v->ws_bytes >= sizeof(int32_t) * (size_t)n_tiles
+  int32_t* tile_work = !v->fwd_only && n_tiles <= (1 << 20) &&
+                               v->ws_bytes >= sizeof(int32_t) * (size_t)n_tiles
                            ? (int32_t*)v->ws
                            : nullptr;
   if (tile_work) memzero(tile_work, sizeof(int32_t) * (size_t)n_tiles, stream);

@@ -82,6 +82,7 @@ class ViewPipeline:
         self.sel = 0
         self.events = None  # name -> [(start, end)] CUDA events when timing
         self.deterministic = False  # fixed-order gradient sums (no float atomics)
+        self.forward_only = False  # playback: no backward follows (ss_view.fwd_only)
         L.lib()
 
     def enable_timing(self, on: bool = True, sample: float = 1.0, seed: int = 0):
@@ -172,6 +173,7 @@ class ViewPipeline:
                 self._b[name] = torch.empty(cap, dtype=torch.int32, device=self.dev)
             self._b["ws_bin"] = torch.empty(1 << 20, dtype=torch.uint8, device=self.dev)
         v = L.SSView()
+        v.fwd_only = 1 if self.forward_only else 0
         timed = self.events is not None and (self._sample >= 1.0
                                              or self._sample_rng.random() < self._sample)
         for _ in range(4):

@@ -81,6 +81,7 @@ class _DeviceSlots:
         self.ws = torch.empty(int(L.lib().ss_compact_workspace_bytes(n)), dtype=torch.uint8,
                               device=dev)
         self.pipe = ViewPipeline()
+        self.pipe.forward_only = True  # playback renders never run a backward
 
     def set_slot(self, slot: int, rows, kept: int, lifespan: Lifespan):
         r0 = slot * self.sl
