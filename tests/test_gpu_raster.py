@@ -308,6 +308,30 @@ def test_deterministic_backward_bit_identical(ss):
     grad_check(ga, g1, tol=1e-5, what="atomic vs deterministic")
 
 
+def test_forward_only_view_still_differentiable(ss):
+    """ss_view.fwd_only (playback) skips the backward's aids -- entry-use
+    masks and the per-tile work order: the image is bit-identical, and a
+    backward run anyway (region test, the binning's tile order) matches the
+    masked one up to float-atomic order."""
+    P, R = ss
+    rng = np.random.default_rng(9)
+    arr = _synth_scene(P, 20_000, (300.0 / 30_000) ** (1 / 3), seed=5)
+    cam = cam_from(P, arc_camera(2, 5, 320, 240))
+    gdir = rng.normal(size=(240, 320, 3))
+    img = R.render_arrays(cam, arr).pixels
+    g = R.render_arrays_backward(cam, arr, gdir)
+    pipe = R.pipeline()
+    pipe.forward_only = True
+    try:
+        img_f = R.render_arrays(cam, arr).pixels
+        g_f = R.render_arrays_backward(cam, arr, gdir)
+        assert pipe.view.used_ok == 0
+    finally:
+        pipe.forward_only = False
+    assert np.array_equal(img, img_f)
+    grad_check(g_f, g, tol=1e-5, what="fwd_only vs masked")
+
+
 @pytest.mark.parametrize("n_culled", [5000, 160_000])
 def test_depth_order_exact_on_adversarial_keys(n_culled):
     """ss_depth_order (range-normalised buckets + per-bucket sort) equals the
