@@ -549,7 +549,9 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
         }
         any |= valid[2 * p] | valid[2 * p + 1];
       }
-      if (!__any_sync(0xffffffffu, any)) {
+      // an entry the forward marked used has a valid pixel here (same
+      // exponents, pos < last of the pixel that used it): no vote needed
+      if ((DET || !used) && !__any_sync(0xffffffffu, any)) {
         if (DET && slot_ok) det.partial[(s_epos[warp][j] * WPT + sub) * 9 + slot] = 0.f;
         continue;
       }
@@ -609,9 +611,12 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
       v[3] = dx * s_dy;
       v[4] = s_dyy;
       v[5] = s_t;
-      v[6] = -(lo2(nsc0) + hi2(nsc0));
-      v[7] = -(lo2(nsc1) + hi2(nsc1));
-      v[8] = -(lo2(nsc2) + hi2(nsc2));
+      // -(a + b) written as (-a) - b: one FADD with both operands negated
+      // (the compiler may not fold the negation itself: the two differ only
+      // in the sign of a zero sum, which no gradient sees)
+      v[6] = -lo2(nsc0) - hi2(nsc0);
+      v[7] = -lo2(nsc1) - hi2(nsc1);
+      v[8] = -lo2(nsc2) - hi2(nsc2);
       if (DET) {
         const float tot = reduce9(v, lane);
         if (slot_ok) det.partial[(s_epos[warp][j] * WPT + sub) * 9 + slot] = tot;
