@@ -356,29 +356,24 @@ static_assert(kRedE * 9 <= 32, "one sum per lane");
 constexpr int kRedWarpTotal = kRedWarpFloats + 4;  // + entry ids; keeps 16-B alignment
 static_assert(kRedWarpFloats % 4 == 0 && kRedE <= 4, "16-B aligned per-warp buffers");
 
-__device__ __forceinline__ void red_park(float* buf, int k, int lane, const float v[9]) {
-  float* col = buf + k * kRedStride + lane;
-#pragma unroll
-  for (int c = 0; c < 9; ++c) col[c * kRedCompPitch] = v[c];
-}
-
 __device__ __forceinline__ void red_flush(const float* buf, const int* gid, int nacc, int lane,
                                           float* __restrict__ g2d) {
   __syncwarp();
   if (lane < 9 * nacc) {
     const int e = lane / 9, c = lane - 9 * e;
     const float4* row = reinterpret_cast<const float4*>(buf + e * kRedStride + c * kRedCompPitch);
-    float4 s = row[0];
+    // the 32 values as 8 float4, summed as packed pairs (FADD2)
+    float4 q = row[0];
+    f2 sa = pk2(q.x, q.y), sb = pk2(q.z, q.w);
 #pragma unroll
     for (int k = 1; k < 8; ++k) {
-      const float4 q = row[k];
-      s.x += q.x;
-      s.y += q.y;
-      s.z += q.z;
-      s.w += q.w;
+      q = row[k];
+      sa = add2(sa, pk2(q.x, q.y));
+      sb = add2(sb, pk2(q.z, q.w));
     }
+    sa = add2(sa, sb);
     SS_DCHECK(gid[e] >= 0);
-    atomicAdd(g2d + (int64_t)gid[e] * SS_G2D_ROW + c, (s.x + s.y) + (s.z + s.w));
+    atomicAdd(g2d + (int64_t)gid[e] * SS_G2D_ROW + c, lo2(sa) + hi2(sa));
   }
   __syncwarp();
 }
@@ -484,6 +479,9 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
   float* rbuf = s_red + warp * kRedWarpTotal;
   int* rgid = reinterpret_cast<int*>(rbuf + kRedWarpFloats);
   int nacc = 0;  // entries parked in rbuf (warp-uniform)
+  float* park = rbuf + lane;  // this lane's column of the next parked entry
+  int* gidp = rgid;           // and the next entry's splat id
+  const bool lane0 = lane == 0;
   if (DET) {
     // entries this warp never visits contribute zero partials
     for (int idx = walk_end + lane; idx < rg.y; idx += 32) {
@@ -621,11 +619,18 @@ __global__ void __launch_bounds__(kWarps * 32, SS_BWD_MINB)
         const float tot = reduce9(v, lane);
         if (slot_ok) det.partial[(s_epos[warp][j] * WPT + sub) * 9 + slot] = tot;
       } else {
-        red_park(rbuf, nacc, lane, v);
-        if (lane == 0) rgid[nacc] = st.g[j];
+        // park through a running pointer (one add per entry instead of the
+        // entry-index multiply-add)
+#pragma unroll
+        for (int c = 0; c < 9; ++c) park[c * kRedCompPitch] = v[c];
+        park += kRedStride;
+        if (lane0) *gidp = st.g[j];
+        ++gidp;
         if (++nacc == kRedE) {
           red_flush(rbuf, rgid, nacc, lane, g2d);
           nacc = 0;
+          park = rbuf + lane;
+          gidp = rgid;
         }
       }
     }
