@@ -10,7 +10,7 @@
 //           per-block fp64 sums of |x - y| and of the SSIM map.
 //   pass 2: separable blur of the three partial maps, combine into
 //           dL/dx = (1-w) sign(x-y)/N - w (B(ds_dmu) + 2x B(ds_dmxx) + y B(ds_dmxy))/N.
-//   pass 3: one block reduces the per-block sums in a fixed order.
+//   pass 3 (pass 2's first CTA): the per-block sums reduced in a fixed order.
 //
 // The blurs are register-blocked: a thread produces 8 consecutive outputs of
 // a column (vertical pass) or 4 of a row (horizontal pass) from a sliding
@@ -278,10 +278,47 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(LossArgs a) {
 }
 
 // pass 2: blur of the partial maps as the pair (ds/dmu, ds/dmxx) + ds/dmxy
+// Fixed-order sums of the forward's per-block (L1, SSIM) partials into out
+// (one CTA; deterministic).
+__device__ __forceinline__ void reduce_partials(const double* __restrict__ partials, int n_blocks,
+                                                double* __restrict__ out) {
+  __shared__ double s[2][kLossThreads / 32];
+  double t0 = 0.0, t1 = 0.0;
+  for (int i = threadIdx.x; i < n_blocks; i += blockDim.x) {
+    t0 += partials[2 * i];
+    t1 += partials[2 * i + 1];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+    t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s[0][threadIdx.x >> 5] = t0;
+    s[1][threadIdx.x >> 5] = t1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      x += s[0][i];
+      y += s[1][i];
+    }
+    out[0] = x;
+    out[1] = y;
+  }
+}
+
+// pass 2 also holds pass 3: its first CTA reduces the forward's partials
+// (complete once pdl_wait returns) before its own tile -- no separate
+// one-CTA launch at the end of the loss.
 __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, float w_ssim,
-                                                                 float* __restrict__ dimg) {
+                                                                 float* __restrict__ dimg,
+                                                                 double* __restrict__ out_sums) {
   pdl_wait();
   pdl_trigger();
+  if (out_sums && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+    reduce_partials(a.partials, gridDim.x * gridDim.y * gridDim.z, out_sums);
   __shared__ f2 s_m2[kLR][kLP];
   __shared__ float s_m1[kLR][kLP];
   __shared__ f2 s_v2[kLT][kLP];
@@ -405,37 +442,6 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(LossArgs a, floa
   }
 }
 
-__global__ void loss_reduce_kernel(const double* __restrict__ partials, int n_blocks,
-                                   double* __restrict__ out) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ double s[2][32];
-  double t0 = 0.0, t1 = 0.0;
-  for (int i = threadIdx.x; i < n_blocks; i += blockDim.x) {
-    t0 += partials[2 * i];
-    t1 += partials[2 * i + 1];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    t0 += __shfl_xor_sync(0xffffffffu, t0, o);
-    t1 += __shfl_xor_sync(0xffffffffu, t1, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    s[0][threadIdx.x >> 5] = t0;
-    s[1][threadIdx.x >> 5] = t1;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
-      a += s[0][i];
-      b += s[1][i];
-    }
-    out[0] = a;
-    out[1] = b;
-  }
-}
-
 // loss.py:105-111 regularizer gradients and terms; one CTA, fixed-order sums
 __global__ void __launch_bounds__(1024) reg_grads_kernel(const double* __restrict__ alpha,
                                                          const double* __restrict__ scales, int n,
@@ -517,7 +523,7 @@ extern "C" int ss_loss_l1_ssim(const float* pred, const uint8_t* gt_u8, const fl
   LossArgs a{pred, gt_u8, lut, gt_f32, width, height, (float*)ws,
              (double*)((char*)ws + ((9 * plane * sizeof(float) + 255) & ~(size_t)255))};
   launch_kx(SS_SSIM_PDL, ssim_fwd_kernel, grid, kLossThreads, 0, stream, a);
-  launch_kx(SS_SSIM_PDL, ssim_bwd_kernel, grid, kLossThreads, 0, stream, a, (float)ssim_weight, dimg);
-  launch_k(loss_reduce_kernel, 1, 1024, 0, stream, a.partials, grid.x * grid.y * grid.z, out_sums);
+  launch_kx(SS_SSIM_PDL, ssim_bwd_kernel, grid, kLossThreads, 0, stream, a, (float)ssim_weight, dimg,
+            out_sums);
   return check_launch("ss_loss_l1_ssim");
 }
