@@ -368,6 +368,9 @@ typedef struct {
   int32_t used_ok;      /* out (forward): masks valid for this view's backward         */
   int32_t fwd_only;     /* in: 1 = no backward follows (playback): the forward skips  */
                         /*   the backward's aids (entry-use masks, per-tile work order) */
+  void* order_ready;    /* out (forward): the event after which the backward's tile   */
+                        /*   order (computed on a library side stream, overlapping the */
+                        /*   loss) is ready; ss_render_bwd waits on it; NULL: none     */
 } ss_view;
 
 /* Projection -> depth order -> tile offsets -> [one stream sync for K] ->
@@ -391,6 +394,10 @@ int ss_render2d_bwd(const ss_splats2d* splats, int32_t width, int32_t height, co
 int ss_render_bwd(const ss_store* store, const ss_camera* cam, const ss_view* v,
                   const float* dimg, float* g2d, const uint8_t* trainable_mask,
                   int64_t trainable_rows, float* grads, ss_stream_t stream);
+/* Make `stream` wait for the calling thread's pending side-stream work of
+ * its last forward (the backward tile order; see ss_view.order_ready) --
+ * call before freeing or regrowing a view's buffers. */
+int ss_side_sync(ss_stream_t stream);
 /* CUDA event helpers for the optional raster timing in ss_view. */
 int ss_event_create(void** ev);
 int ss_event_destroy(void* ev);

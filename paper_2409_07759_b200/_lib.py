@@ -59,7 +59,7 @@ class SSView(Structure):
                 ("ws_bytes", c_size_t), ("ws_needed", c_size_t), ("n_pairs", c_int64),
                 ("sorted_sel", c_int32), ("pad1", c_int32), ("events", P * 4),
                 ("partial", P), ("rank", P), ("used", P), ("used_cap", c_int64),
-                ("used_ok", c_int32), ("fwd_only", c_int32)]
+                ("used_ok", c_int32), ("fwd_only", c_int32), ("order_ready", P)]
 
 class SSSplats2D(Structure):
     _fields_ = [("mean2d", P), ("inv2d", P), ("alpha", P), ("color", P), ("bbox", P),
@@ -120,6 +120,7 @@ _SIGNATURES = {
     "ss_basis_to_2d": ([P, POINTER(SSSplats2D), P, P, P, P, P, P, P], c_int),
     "ss_render_bwd": ([POINTER(SSStore), POINTER(SSCamera), POINTER(SSView), P, P, P, I64, P, P],
                       c_int),
+    "ss_side_sync": ([P], c_int),
     "ss_event_create": ([POINTER(P)], c_int),
     "ss_event_destroy": ([P], c_int),
     "ss_event_elapsed_ms": ([P, P, POINTER(ctypes.c_float)], c_int),

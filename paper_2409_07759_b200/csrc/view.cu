@@ -75,6 +75,34 @@ static void record(void* ev, cudaStream_t stream) {
   if (ev) cudaEventRecord((cudaEvent_t)ev, stream);
 }
 
+// The backward's tile order (tile_order_from_work, one CTA) runs on a side
+// stream per host thread and device, overlapping the loss on the caller's
+// stream instead of sitting between the forward and the loss.  The next
+// forward from this thread and the view's backward wait for it (order_done).
+struct SideOrder {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fwd_done = nullptr, order_done = nullptr;
+  bool pending = false;
+};
+
+static SideOrder* side_order() {
+  constexpr int kMaxDev = 64;
+  thread_local SideOrder tab[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  SideOrder& so = tab[dev];
+  if (!so.s) {
+    if (cudaStreamCreateWithFlags(&so.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&so.fwd_done, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&so.order_done, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      so.s = nullptr;
+      return nullptr;
+    }
+  }
+  return &so;
+}
+
 extern "C" int ss_event_create(void** ev) {
   cudaEvent_t e;
   if (cudaEventCreate(&e) != cudaSuccess) return check_launch("ss_event_create");
@@ -93,6 +121,19 @@ extern "C" int ss_event_elapsed_ms(void* start, void* end, float* ms) {
   return SS_OK;
 }
 
+// Make `stream` wait for this thread's pending side-stream tile order (the
+// forward does it itself; callers that free or regrow a view's buffers call
+// it first, so the side kernel never touches reused memory).
+extern "C" int ss_side_sync(cudaStream_t stream) {
+  SideOrder* so = side_order();
+  if (so && so->pending) {
+    if (cudaStreamWaitEvent(stream, so->order_done, 0) != cudaSuccess)
+      return check_launch("ss_side_sync");
+    so->pending = false;
+  }
+  return SS_OK;
+}
+
 // Shared by the 3D (store + camera) and 2D (_kernels) entries: workspace
 // check, records (via `make_records`), depth order, offsets, K, binning,
 // tile order, raster forward.  pbox != nullptr selects the per-pixel bbox test.
@@ -105,7 +146,12 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   const int n = v->n;
   v->n_pairs = 0;
   v->sorted_sel = 0;
+  v->order_ready = nullptr;
   int rc;
+  if (SideOrder* so = side_order(); so && so->pending) {
+    cudaStreamWaitEvent(stream, so->order_done, 0);
+    so->pending = false;
+  }
   if (n == 0) {
     memzero(v->img, sizeof(float) * 3 * (size_t)W * H, stream);
     memzero(v->n_contrib, sizeof(int32_t) * (size_t)W * H, stream);
@@ -241,8 +287,20 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
   record(v->events[0], stream);
   rc = raster_fwd_ex(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,
                      v->t_final, v->n_contrib, pbox, masks ? v->used : nullptr, tile_work, stream);
-  if (!rc && tile_work) rc = tile_order_from_work(tile_work, n_tiles, v->tile_order, stream);
   record(v->events[1], stream);
+  if (!rc && tile_work) {
+    SideOrder* so = side_order();
+    if (so) {
+      cudaEventRecord(so->fwd_done, stream);
+      cudaStreamWaitEvent(so->s, so->fwd_done, 0);
+      rc = tile_order_from_work(tile_work, n_tiles, v->tile_order, so->s);
+      cudaEventRecord(so->order_done, so->s);
+      so->pending = true;
+      v->order_ready = (void*)so->order_done;
+    } else {
+      rc = tile_order_from_work(tile_work, n_tiles, v->tile_order, stream);
+    }
+  }
   return rc;
 }
 
@@ -278,6 +336,7 @@ extern "C" int ss_render2d_bwd(const ss_splats2d* sp, int32_t width, int32_t hei
   memzero(g2d, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
   const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
   const uint32_t* used = v->used_ok && raster_masks_usable() ? v->used : nullptr;
+  if (v->order_ready) cudaStreamWaitEvent(stream, (cudaEvent_t)v->order_ready, 0);
   int rc = raster_bwd_plain_ex(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, width, height,
                                v->tile_order, dimg, v->t_final, v->n_contrib, g2d, v->bbox, used,
                                stream);
@@ -298,6 +357,7 @@ extern "C" int ss_render_bwd(const ss_store* store, const ss_camera* cam, const 
   const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
   // the forward's entry-use masks, when it recorded them for this view
   const uint32_t* used = v->used_ok && raster_masks_usable() ? v->used : nullptr;
+  if (v->order_ready) cudaStreamWaitEvent(stream, (cudaEvent_t)v->order_ready, 0);
   record(v->events[2], stream);
   int rc;
   if (v->partial)

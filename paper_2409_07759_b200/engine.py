@@ -151,6 +151,9 @@ class ViewPipeline:
         return self._run_forward(splats.n, int(width), int(height), call, stream)
 
     def _run_forward(self, n: int, W: int, H: int, call, stream=None):
+        # the previous forward's side-stream tile order may still read / write
+        # buffers this call regrows: order it before any of them is freed
+        L.check(L.lib().ss_side_sync(L.stream_ptr(stream)), "side_sync")
         tiles_x, tiles_y = (W + TILE - 1) // TILE, (H + TILE - 1) // TILE
         n_tiles = tiles_x * tiles_y
         self.n, self.width, self.height, self.n_tiles = n, W, H, n_tiles
