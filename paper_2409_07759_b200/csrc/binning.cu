@@ -689,12 +689,38 @@ __global__ void __launch_bounds__(kBinThreads) bin_col_scan_kernel(int32_t* __re
 // One CTA: exclusive scan of the tile totals -> start[t], ranges[t].
 constexpr int kOrderMax = 1 << 20;
 constexpr int kBuckets = 128;
+static_assert(kBuckets == 4 * 32, "scan_buckets: 4 buckets per lane of one warp");
 
 __device__ __forceinline__ int len_bucket(int len) {
   // 4 * log2(len + 1) without a log: exponent and the top two mantissa bits
   const float f = (float)(len + 1);
   const int b = ((__float_as_int(f) >> 21) - (127 << 2));  // 4 * floor-ish(log2)
   return kBuckets - 1 - min(max(b, 0), kBuckets - 1);
+}
+
+// Exclusive scan of the kBuckets (= 128) length-bucket counts by warp 0
+// (4 per lane + one warp scan) instead of a serial loop on thread 0.
+__device__ __forceinline__ void scan_buckets(const int* hist, int* cursor) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  int v[4], run = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[k] = hist[4 * lane + k];
+    run += v[k];
+  }
+  int incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int acc = incl - run;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    cursor[4 * lane + k] = acc;
+    acc += v[k];
+  }
 }
 
 __global__ void __launch_bounds__(1024) bin_tile_scan_kernel(const int32_t* __restrict__ totals,
@@ -753,14 +779,7 @@ __global__ void __launch_bounds__(1024) bin_tile_scan_kernel(const int32_t* __re
   __syncthreads();
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&s_hist[len_bucket(s_tot[t])], 1);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int b = 0; b < kBuckets; ++b) {
-      const int c = s_hist[b];
-      s_hist[b] = acc;
-      acc += c;
-    }
-  }
+  scan_buckets(s_hist, s_hist);  // in place: each lane reads its 4 before writing them
   __syncthreads();
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
     tile_order[atomicAdd(&s_hist[len_bucket(s_tot[t])], 1)] = t;
@@ -1137,13 +1156,7 @@ __global__ void __launch_bounds__(1024) tile_order_bucket_kernel(const int2* __r
     atomicAdd(&hist[len_bucket(r.y - r.x)], 1);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int b = 0; b < kBuckets; ++b) {
-      cursor[b] = acc;
-      acc += hist[b];
-    }
-  }
+  scan_buckets(hist, cursor);
   __syncthreads();
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
     const int2 r = ranges[t];
@@ -1164,13 +1177,7 @@ __global__ void __launch_bounds__(1024) tile_order_work_kernel(const int32_t* __
   __syncthreads();
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&hist[len_bucket(work[t])], 1);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int b = 0; b < kBuckets; ++b) {
-      cursor[b] = acc;
-      acc += hist[b];
-    }
-  }
+  scan_buckets(hist, cursor);
   __syncthreads();
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
     out[atomicAdd(&cursor[len_bucket(work[t])], 1)] = t;
