@@ -393,6 +393,11 @@ __global__ void __launch_bounds__(128, SS_PROJ_BWD_MINB) project_bwd_kernel(Stor
   if (mask && !mask[i]) return;
   const int32_t row = rows ? rows[i] : i;
   if (row >= trainable_rows) return;
+  static_assert(SS_G2D_ROW == 12, "three float4 per basis-sum row");
+  // this splat's basis sums, loaded up front (48-B rows: three float4) so
+  // their latency overlaps the parameter row's
+  const float4* g4 = reinterpret_cast<const float4*>(g2d + (int64_t)i * SS_G2D_ROW);
+  const float4 ga = g4[0], gb4 = g4[1], gc4 = g4[2];
   if (depth_key[i] == ~0ull) {  // culled: a zero gradient row (the step needs no pre-zeroed buffer)
     float2* out2 = reinterpret_cast<float2*>(grads + (int64_t)row * SS_GRAD_ROW);
 #pragma unroll
@@ -408,7 +413,7 @@ __global__ void __launch_bounds__(128, SS_PROJ_BWD_MINB) project_bwd_kernel(Stor
   // with t = alpha G d alpha'.  With dm = -t/2 and the conic (i0, i1, i2):
   //   d mean2d = (i0 W0 + i1 W1, i1 W0 + i2 W1),  d inv2d = -(W2/2, W3, W4/2),
   //   d alpha = W5 / alpha, so d logit = W5 (1 - alpha)   (raster.py:231-246)
-  const float* gg = g2d + (int64_t)i * SS_G2D_ROW;
+  const float gg[9] = {ga.x, ga.y, ga.z, ga.w, gb4.x, gb4.y, gb4.z, gb4.w, gc4.x};
   const double ad = p.a + kDilation, cd = p.c + kDilation, b = p.b;
   const double det = ad * cd - b * b;
   const double idet = 1.0 / det;
