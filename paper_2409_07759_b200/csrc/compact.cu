@@ -22,32 +22,43 @@ struct CandMap {
   int32_t frame;
 };
 
-// Active row id of candidate c (or -1 when inactive).
-__device__ __forceinline__ int32_t cand_row(const CandMap& m, int64_t c) {
+// Physical row of candidate c (optimizable rows in order, then matured rows
+// through the block map), or -1 past the end.
+__device__ __forceinline__ int64_t cand_phys(const CandMap& m, int64_t c) {
   if (c >= m.n_cand) return -1;
-  int64_t phys;
-  int32_t row;
-  if (c < m.n_opt) {
-    phys = c;
-    row = (int32_t)c;
-  } else {
-    int64_t lc = c - m.n_opt;
-    int64_t pb = m.blk_map ? m.blk_map[lc / m.block_rows] : lc / m.block_rows;
-    phys = m.n_opt + pb * m.block_rows + lc % m.block_rows;
-    row = (int32_t)phys;
+  if (c < m.n_opt) return c;
+  const int64_t lc = c - m.n_opt;
+  const int64_t pb = m.blk_map ? m.blk_map[lc / m.block_rows] : lc / m.block_rows;
+  return m.n_opt + pb * m.block_rows + lc % m.block_rows;
+}
+
+// Active row ids of a thread's kCompactItems candidates (-1: inactive): the
+// physical rows first, then every lifespan load in flight together (one
+// memory round trip instead of one per candidate).
+__device__ __forceinline__ void cand_rows(const CandMap& m, int64_t base, int32_t out[kCompactItems]) {
+  int64_t phys[kCompactItems];
+#pragma unroll
+  for (int k = 0; k < kCompactItems; ++k) phys[k] = cand_phys(m, base + k * kCompactBlock + threadIdx.x);
+  int32_t s[kCompactItems], e[kCompactItems];
+#pragma unroll
+  for (int k = 0; k < kCompactItems; ++k) {
+    s[k] = phys[k] >= 0 ? m.start[phys[k]] : 1;
+    e[k] = phys[k] >= 0 ? m.expire[phys[k]] : 0;
   }
-  int32_t s = m.start[phys], e = m.expire[phys];
-  return (s <= m.frame && m.frame < e) ? row : -1;
+#pragma unroll
+  for (int k = 0; k < kCompactItems; ++k)
+    out[k] = (s[k] <= m.frame && m.frame < e[k]) ? (int32_t)phys[k] : -1;
 }
 
 __global__ void compact_count(CandMap m, int32_t* block_counts) {
   pdl_wait();
   pdl_trigger();
   int64_t base = (int64_t)blockIdx.x * kCompactTile;
+  int32_t rowv[kCompactItems];
+  cand_rows(m, base, rowv);
   int cnt = 0;
 #pragma unroll
-  for (int k = 0; k < kCompactItems; ++k)
-    cnt += cand_row(m, base + k * kCompactBlock + threadIdx.x) >= 0;
+  for (int k = 0; k < kCompactItems; ++k) cnt += rowv[k] >= 0;
   __shared__ int s_sum[kCompactBlock / 32];
   int w = __reduce_add_sync(0xffffffffu, cnt);
   if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = w;
@@ -109,9 +120,12 @@ __global__ void compact_scatter(CandMap m, const int32_t* block_offsets, int32_t
   if (threadIdx.x == 0) s_base = block_offsets[blockIdx.x];
   __syncthreads();
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int32_t rowv[kCompactItems];
+  cand_rows(m, base, rowv);
+#pragma unroll
   for (int k = 0; k < kCompactItems; ++k) {
     int64_t c = base + k * kCompactBlock + threadIdx.x;
-    int32_t row = cand_row(m, c);
+    int32_t row = rowv[k];
     unsigned ball = __ballot_sync(0xffffffffu, row >= 0);
     int wpre = __popc(ball & ((1u << lane) - 1));
     if (lane == 0) s_warp[wid] = __popc(ball);
