@@ -510,16 +510,26 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int k0 = bounds[blockIdx.x], k1 = bounds[blockIdx.x + 1];
+  // the next batch's (offsets, order) are loaded while this batch is
+  // walked: only the bbox / mask gathers stay on a batch's critical path
+  int pk = k0 + warp * 32 + lane;
+  int32_t p_o0 = pk < k1 ? offsets[pk] : 0, p_o1 = pk < k1 ? offsets[pk + 1] : 0;
+  int32_t p_i = pk < k1 ? order[pk] : 0;
   for (int kb = k0 + warp * 32; kb < k1; kb += kBinWarps * 32) {
     const int k = kb + lane;
     int32_t i = 0, o0 = 0, cnt = 0, tx0 = 0, ty0 = 0, w = 1, total = 0;
     int4 bb = make_int4(0, 0, 0, 0);
     uint64_t mask = 0;
+    const int32_t c_o0 = p_o0, c_o1 = p_o1, c_i = p_i;
+    pk = k + kBinWarps * 32;
+    p_o0 = pk < k1 ? offsets[pk] : 0;
+    p_o1 = pk < k1 ? offsets[pk + 1] : 0;
+    p_i = pk < k1 ? order[pk] : 0;
     if (k < k1) {
-      o0 = offsets[k];
-      cnt = offsets[k + 1] - o0;
+      o0 = c_o0;
+      cnt = c_o1 - o0;
       if (cnt > 0) {
-        i = order[k];
+        i = c_i;
         bb = bbox[i];
         mask = tile_mask[i];
         tx0 = bb.x / kTile;
