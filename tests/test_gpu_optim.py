@@ -240,3 +240,71 @@ def test_relocation_large_matches_oracle_with_same_uniforms(T):
             np.testing.assert_allclose(gens[gi].params[k], ref_params[gi][k], rtol=1e-12,
                                        atol=1e-14, err_msg=f"{gi} {k}")
             assert np.array_equal(gens[gi].adam_m[k] == 0, ref_m[gi][k] == 0)
+
+
+def test_adam_tma_blocks_straddling_generations():
+    """The shared-memory (TMA bulk copy) optimizer kernel: 64-row CTAs that
+    straddle generations of 100 rows, half of them frozen, a tail CTA, and
+    gamma^w and bias corrections that differ per generation.  Stepped rows
+    match the reference step (oracle.optimizer_step: 1e-8 on parameters,
+    1e-6 relative on moments); frozen rows stay bit-identical."""
+    import ctypes
+
+    import torch
+
+    from oracle import splat_oracle as O
+    from paper_2409_07759_b200 import _lib as L
+    from paper_2409_07759_b200.device_model import GEN_DTYPE, _hyper, device
+    from paper_2409_07759_b200.train import TrainConfig
+
+    rng = np.random.default_rng(31)
+    n_gen, sl = 10, 100
+    n = n_gen * sl
+    cols = {"mean": slice(0, 3), "quat": slice(3, 7), "log_scale": slice(7, 10),
+            "opacity_logit": slice(10, 11), "color": slice(11, 14)}
+    p = np.empty((n, 14))
+    p[:, 0:3] = rng.normal(size=(n, 3))
+    q = rng.normal(size=(n, 4))
+    p[:, 3:7] = q / np.linalg.norm(q, axis=1, keepdims=True)
+    p[:, 7:10] = rng.uniform(-5, -2, size=(n, 3))
+    p[:, 10] = rng.normal(size=n)
+    p[:, 11:14] = rng.uniform(0, 1, size=(n, 3))
+    m = rng.normal(scale=1e-3, size=(n, 14))
+    v = rng.uniform(1e-8, 1e-6, size=(n, 14))
+    g = rng.normal(scale=1e-2, size=(n, 14)).astype(np.float32)
+    active = np.array([1, 0, 1, 1, 0, 0, 0, 1, 0, 1], dtype=np.int32)
+    ts = rng.integers(0, 20, size=n_gen)
+    gscale = 0.5 ** rng.integers(0, 4, size=n_gen)
+    cfg = TrainConfig(swin_size=n_gen, num_gs=n)
+    ocfg = dict(O.DEFAULT_CFG)
+    tab = np.zeros(n_gen, dtype=GEN_DTYPE)
+    for gi in range(n_gen):
+        t = int(ts[gi]) + 1
+        tab[gi] = (int(active[gi]), 0, 1.0 - ocfg["adam_beta1"] ** t,
+                   1.0 - ocfg["adam_beta2"] ** t, float(gscale[gi]))
+    dev = device()
+    tp, tm, tv = (torch.from_numpy(a.copy()).to(dev) for a in (p, m, v))
+    tg = torch.from_numpy(g).to(dev)
+    ttab = torch.from_numpy(tab.view(np.uint8).copy()).to(dev)
+    h = _hyper(cfg, 1, False, 0, 0)
+    h.opacity_reg = h.scale_reg = 0.0
+    L.check(L.lib().ss_adam_sgld_step(L.ptr(tp), L.ptr(tg), L.ptr(tm), L.ptr(tv), n, sl,
+                                      L.ptr(ttab), ctypes.byref(h), None, L.stream_ptr()),
+            "adam_sgld_step")
+    gp, gm, gv = (t.cpu().numpy() for t in (tp, tm, tv))
+    for gi in range(n_gen):
+        r = slice(gi * sl, (gi + 1) * sl)
+        if not active[gi]:
+            assert np.array_equal(gp[r], p[r]) and np.array_equal(gm[r], m[r])
+            assert np.array_equal(gv[r], v[r])
+            continue
+        grads = {k: g[r, c].astype(np.float64) for k, c in cols.items()}
+        grads["mean"] = grads["mean"] * gscale[gi]
+        params = {k: p[r, c].copy() for k, c in cols.items()}
+        mm = {k: m[r, c].copy() for k, c in cols.items()}
+        vv = {k: v[r, c].copy() for k, c in cols.items()}
+        O.optimizer_step(params, mm, vv, int(ts[gi]), grads, ocfg)
+        for k, c in cols.items():
+            np.testing.assert_allclose(gp[r, c], params[k], rtol=0, atol=1e-8)
+            np.testing.assert_allclose(gm[r, c], mm[k], rtol=1e-6, atol=1e-6 * np.abs(mm[k]).max())
+            np.testing.assert_allclose(gv[r, c], vv[k], rtol=1e-6, atol=1e-6 * np.abs(vv[k]).max())
