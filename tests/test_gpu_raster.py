@@ -332,6 +332,29 @@ def test_forward_only_view_still_differentiable(ss):
     grad_check(g_f, g, tol=1e-5, what="fwd_only vs masked")
 
 
+def test_side_stream_tile_order_between_views(ss):
+    """The backward's tile order runs on a side stream after each forward
+    (ss_view.order_ready): a forward-only render of another view in between
+    must not disturb the next view's backward (deterministic sums: bit
+    equal to the same backward without the interleaved view)."""
+    P, R = ss
+    rng = np.random.default_rng(12)
+    arr = _synth_scene(P, 20_000, (300.0 / 30_000) ** (1 / 3), seed=6)
+    cam_a = cam_from(P, arc_camera(0, 5, 320, 240))
+    cam_b = cam_from(P, arc_camera(3, 5, 256, 192))
+    gdir = rng.normal(size=(192, 256, 3))
+    R.set_deterministic(True)
+    try:
+        g_ref = R.render_arrays_backward(cam_b, arr, gdir)
+        for _ in range(3):
+            R.render_arrays(cam_a, arr)
+        g = R.render_arrays_backward(cam_b, arr, gdir)
+    finally:
+        R.set_deterministic(False)
+    for k in g_ref:
+        assert np.array_equal(g[k], g_ref[k]), k
+
+
 @pytest.mark.parametrize("n_culled", [5000, 160_000])
 def test_depth_order_exact_on_adversarial_keys(n_culled):
     """ss_depth_order (range-normalised buckets + per-bucket sort) equals the
