@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(1024) bin_tile_scan_kernel(const int32_t* __re
 __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(
     const int32_t* __restrict__ offsets, const int32_t* __restrict__ bounds,
     const uint16_t* __restrict__ keys, const int32_t* __restrict__ vals, int32_t n_tiles,
-    const int32_t* __restrict__ base, const int32_t* __restrict__ start,
+    int32_t* __restrict__ base, const int32_t* __restrict__ start,
     int32_t* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
@@ -813,7 +813,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(
   int32_t* s_cur = reinterpret_cast<int32_t*>(s_wc + n_tiles);              // n_tiles
   const int c = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int32_t* brow = base + (int64_t)c * n_tiles;
+  int32_t* brow = base + (int64_t)c * n_tiles;
   const int q0 = offsets[bounds[c]], q1 = offsets[bounds[c + 1]];
   // software pipelined: the pairs of the next kAhead waves are in flight
   // while this one is placed (one wave of lookahead left the loop waiting
@@ -842,6 +842,10 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(
       if (t < n_tiles) {
         s_cur[t] = a[u];
         s_wc[t] = 0ull;
+        // chunk 0's base row is dead once read: it becomes the zeroed
+        // per-tile work counts of the raster forward (view.cu aliases them
+        // to the workspace start), which then needs no memset launch
+        if (c == 0) brow[t] = 0;
       }
     }
   }

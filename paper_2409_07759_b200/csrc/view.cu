@@ -283,7 +283,8 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
                                v->ws_bytes >= sizeof(int32_t) * (size_t)n_tiles
                            ? (int32_t*)v->ws
                            : nullptr;
-  if (tile_work) memzero(tile_work, sizeof(int32_t) * (size_t)n_tiles, stream);
+  // the chunked binning's scatter leaves them zeroed (its chunk-0 base row)
+  if (tile_work && !tile_order_done) memzero(tile_work, sizeof(int32_t) * (size_t)n_tiles, stream);
   record(v->events[0], stream);
   rc = raster_fwd_ex(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, W, H, v->tile_order, v->img,
                      v->t_final, v->n_contrib, pbox, masks ? v->used : nullptr, tile_work, stream);
