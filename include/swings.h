@@ -371,6 +371,9 @@ typedef struct {
   void* order_ready;    /* out (forward): the event after which the backward's tile   */
                         /*   order (computed on a library side stream, overlapping the */
                         /*   loss) is ready; ss_render_bwd waits on it; NULL: none     */
+  float* g2d_pre;       /* in, optional: the g2d buffer the backward will be given;    */
+                        /*   the forward zero-fills it on the same side stream, and    */
+                        /*   ss_render_bwd then skips its own fill                     */
 } ss_view;
 
 /* Projection -> depth order -> tile offsets -> [one stream sync for K] ->

@@ -59,7 +59,7 @@ class SSView(Structure):
                 ("ws_bytes", c_size_t), ("ws_needed", c_size_t), ("n_pairs", c_int64),
                 ("sorted_sel", c_int32), ("pad1", c_int32), ("events", P * 4),
                 ("partial", P), ("rank", P), ("used", P), ("used_cap", c_int64),
-                ("used_ok", c_int32), ("fwd_only", c_int32), ("order_ready", P)]
+                ("used_ok", c_int32), ("fwd_only", c_int32), ("order_ready", P), ("g2d_pre", P)]
 
 class SSSplats2D(Structure):
     _fields_ = [("mean2d", P), ("inv2d", P), ("alpha", P), ("color", P), ("bbox", P),

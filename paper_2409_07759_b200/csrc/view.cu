@@ -295,6 +295,7 @@ static int render_fwd_common(int W, int H, ss_view* v, const int32_t* pbox,
       cudaEventRecord(so->fwd_done, stream);
       cudaStreamWaitEvent(so->s, so->fwd_done, 0);
       rc = tile_order_from_work(tile_work, n_tiles, v->tile_order, so->s);
+      if (!rc && v->g2d_pre) rc = memzero(v->g2d_pre, sizeof(float) * SS_G2D_ROW * (size_t)n, so->s);
       cudaEventRecord(so->order_done, so->s);
       so->pending = true;
       v->order_ready = (void*)so->order_done;
@@ -334,10 +335,12 @@ extern "C" int ss_render2d_bwd(const ss_splats2d* sp, int32_t width, int32_t hei
                                cudaStream_t stream) {
   if (!sp || !v) return set_error(SS_ERR_INVALID, "ss_render2d_bwd: bad args");
   if (v->n == 0 || v->n_pairs == 0) return SS_OK;
-  memzero(g2d, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
+  // zero-filled by the forward's side stream when it was given this buffer
+  if (v->order_ready) cudaStreamWaitEvent(stream, (cudaEvent_t)v->order_ready, 0);
+  if (!(v->order_ready && v->g2d_pre == g2d))
+    memzero(g2d, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
   const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
   const uint32_t* used = v->used_ok && raster_masks_usable() ? v->used : nullptr;
-  if (v->order_ready) cudaStreamWaitEvent(stream, (cudaEvent_t)v->order_ready, 0);
   int rc = raster_bwd_plain_ex(v->ranges, sv, v->rec_a, v->rec_b, v->rec_c, width, height,
                                v->tile_order, dimg, v->t_final, v->n_contrib, g2d, v->bbox, used,
                                stream);
@@ -351,14 +354,17 @@ extern "C" int ss_render_bwd(const ss_store* store, const ss_camera* cam, const 
                              int64_t trainable_rows, float* grads, cudaStream_t stream) {
   if (!store || !cam || !v) return set_error(SS_ERR_INVALID, "ss_render_bwd: bad args");
   if (v->n == 0) return SS_OK;
-  memzero(g2d, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
+  // zero-filled by the forward's side stream when it was given this buffer
+  // (ordered by the wait on order_ready below)
+  const bool pre = v->order_ready && v->g2d_pre == g2d;
+  if (v->order_ready) cudaStreamWaitEvent(stream, (cudaEvent_t)v->order_ready, 0);
+  if (!pre) memzero(g2d, sizeof(float) * SS_G2D_ROW * (size_t)v->n, stream);
   if (v->n_pairs == 0)  // nothing reached a pixel: zero gradients for every active row
     return ss_project_bwd(store, v->rows, v->n, cam, g2d, v->depth_key, trainable_mask,
                           trainable_rows, grads, stream);
   const int32_t* sv = v->sorted_sel ? v->vals_alt : v->vals;
   // the forward's entry-use masks, when it recorded them for this view
   const uint32_t* used = v->used_ok && raster_masks_usable() ? v->used : nullptr;
-  if (v->order_ready) cudaStreamWaitEvent(stream, (cudaEvent_t)v->order_ready, 0);
   record(v->events[2], stream);
   int rc;
   if (v->partial)

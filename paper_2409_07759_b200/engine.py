@@ -177,6 +177,11 @@ class ViewPipeline:
             self._b["ws_bin"] = torch.empty(1 << 20, dtype=torch.uint8, device=self.dev)
         v = L.SSView()
         v.fwd_only = 1 if self.forward_only else 0
+        if not self.forward_only:
+            # the backward's basis-sum buffer: zero-filled by the forward on
+            # the library's side stream (ss_view.g2d_pre), not at the
+            # backward's start
+            v.g2d_pre = L.ptr(self._buf("g2d", (nn, L.SS_G2D_ROW), torch.float32))
         timed = self.events is not None and (self._sample >= 1.0
                                              or self._sample_rng.random() < self._sample)
         for _ in range(4):
