@@ -142,6 +142,8 @@ class DeviceModel:
         self.seed = philox_seed(cfg.rng_seed)
         self.store = Store(opt=self.opt, mat=self.mat)
         self.dirty = True
+        self._rows_free = None  # event: the last view's backward no longer reads active_rows
+        self._side = None       # side stream of the overlapped compaction
         self._life_sig = None
         self.last_sums = None
         self.last_counts = (0, 0)
@@ -210,19 +212,37 @@ class DeviceModel:
     def compact(self, frame: int):
         """Active row ids of `frame` (a-2): optimizable rows of generations in
         state.slices order, then matured rows in archive order.  Returns
-        (rows device tensor, n_active, n_active_optimizable)."""
+        (rows device tensor, n_active, n_active_optimizable).
+
+        When the lifespan tables are unchanged since the previous view, the
+        compaction runs on a side stream from the point where that view's
+        backward released the row list (`_rows_free`), i.e. beside the
+        previous step's optimizer; the caller's stream waits for it before
+        the projection."""
         state, sl = self.state, self.sl
+        side_ok = self._rows_free is not None and not self.dirty
+        rows_free, self._rows_free = self._rows_free, None  # one use: set again by the next backward
         if self.dirty:
             self.sync_lifespans()
         live = lambda ls: ls.start <= frame < ls.expire  # noqa: E731
         n_opt = sl * sum(live(g.lifespan) for g in state.slices)
         n_mat = sl * sum(live(m.lifespan) for m in state.matured)
         lib = L.lib()
+        main = torch.cuda.current_stream()
+        if side_ok:
+            if self._side is None:
+                self._side = torch.cuda.Stream()
+            self._side.wait_event(rows_free)
+        s = self._side if side_ok else main
         L.check(lib.ss_compact_active(L.ptr(self.row_start), L.ptr(self.row_expire), self.num_gs,
                                       len(state.matured) * sl, L.ptr(self.blk_map), sl, frame,
                                       L.ptr(self.active_rows), L.ptr(self.counts),
                                       L.ptr(self.ws_compact), self.ws_compact.numel(),
-                                      L.stream_ptr()), "compact_active")
+                                      L.stream_ptr(s)), "compact_active")
+        if side_ok:
+            done = torch.cuda.Event()
+            done.record(self._side)
+            main.wait_event(done)
         n = n_opt + n_mat
         # recomputed every view, as the reference does (train.py:380-386);
         # the buffer is rewritten, in stream order, by the next view's call
@@ -279,6 +299,10 @@ class DeviceModel:
         dimg, sums = self.lossbuf.run(img, cam.height, cam.width, gt_u8=gt, lut=self.lut,
                                       ssim_weight=self.cfg.ssim_weight)
         self.pipe.backward(dimg, self.grads, trainable_rows=self.num_gs)
+        # the row list is no longer read past this point: the next view's
+        # compaction may start here (beside this step's optimizer)
+        self._rows_free = torch.cuda.Event()
+        self._rows_free.record()
         self.last_sums = sums
         self.last_counts = (n, n_opt_here)
         return sums
