@@ -40,15 +40,22 @@ __device__ __forceinline__ uint32_t depth_bucket(uint64_t k, uint64_t kmin, uint
   return b < nb - 1 ? b : nb - 1;
 }
 
-// zero the histogram and reduce the kept keys' range (range[0] = ~kmin,
-// range[1] = kmax, both max-reduced from 0)
+// zero the histogram and reduce the kept keys' range per CTA: partial[2b] =
+// ~kmin, partial[2b + 1] = kmax of CTA b (max-reduced from 0); CTA 0 also
+// clears the long-run count.  No pre-zeroed accumulator: depth_hist
+// reduces the partials itself (a memset launch fewer per view).
+constexpr int kRangeBlocks = 296;
+
 __global__ void depth_range_kernel(const uint64_t* __restrict__ key64, int32_t n,
-                                   unsigned long long* __restrict__ range,
-                                   int32_t* __restrict__ hist, int32_t nb_total) {
+                                   unsigned long long* __restrict__ partial,
+                                   int32_t* __restrict__ hist, int32_t nb_total,
+                                   int32_t* __restrict__ n_long) {
   pdl_wait();
   pdl_trigger();
+  __shared__ unsigned long long s_r[2][8];
   const int stride = gridDim.x * blockDim.x;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid == 0) *n_long = 0;
   for (int i = tid; i < nb_total; i += stride) hist[i] = 0;
   unsigned long long inv_min = 0ull, mx = 0ull;
   for (int i = tid; i < n; i += stride) {
@@ -66,19 +73,69 @@ __global__ void depth_range_kernel(const uint64_t* __restrict__ key64, int32_t n
     mx = mx > b ? mx : b;
   }
   if ((threadIdx.x & 31) == 0) {
-    atomicMax(&range[0], inv_min);
-    atomicMax(&range[1], mx);
+    s_r[0][threadIdx.x >> 5] = inv_min;
+    s_r[1][threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long a = 0ull, b = 0ull;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a = a > s_r[0][w] ? a : s_r[0][w];
+      b = b > s_r[1][w] ? b : s_r[1][w];
+    }
+    partial[2 * blockIdx.x] = a;
+    partial[2 * blockIdx.x + 1] = b;
   }
 }
 
+// (~kmin, kmax) from depth_range's per-CTA partials, by every CTA of the
+// histogram (a few KB of L2 reads each); CTA 0 stores it for the scatter.
+__device__ __forceinline__ void reduce_range(const unsigned long long* __restrict__ partial,
+                                             int n_part, unsigned long long* __restrict__ range,
+                                             unsigned long long& kmin, unsigned long long& kmax) {
+  __shared__ unsigned long long s_r[2][8];
+  unsigned long long a = 0ull, b = 0ull;
+  for (int i = threadIdx.x; i < n_part; i += blockDim.x) {
+    const unsigned long long x = partial[2 * i], y = partial[2 * i + 1];
+    a = a > x ? a : x;
+    b = b > y ? b : y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, a, o);
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, b, o);
+    a = a > x ? a : x;
+    b = b > y ? b : y;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_r[0][threadIdx.x >> 5] = a;
+    s_r[1][threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  a = 0ull;
+  b = 0ull;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    a = a > s_r[0][w] ? a : s_r[0][w];
+    b = b > s_r[1][w] ? b : s_r[1][w];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    range[0] = a;
+    range[1] = b;
+  }
+  kmin = ~a;
+  kmax = b;
+}
+
 __global__ void depth_hist_kernel(const uint64_t* __restrict__ key64, int32_t n,
-                                  const unsigned long long* __restrict__ range, uint32_t nb,
+                                  const unsigned long long* __restrict__ partial, int n_part,
+                                  unsigned long long* __restrict__ range, uint32_t nb,
                                   int32_t* __restrict__ hist) {
   pdl_wait();
   pdl_trigger();
   __shared__ int32_t s_culled;
   if (threadIdx.x == 0) s_culled = 0;
-  __syncthreads();
+  unsigned long long kmin, kmax;
+  reduce_range(partial, n_part, range, kmin, kmax);  // (its barrier also covers s_culled)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t k = i < n ? key64[i] : 0ull;
   // culled keys all land in bucket nb: counted per CTA in shared memory and
@@ -88,7 +145,7 @@ __global__ void depth_hist_kernel(const uint64_t* __restrict__ key64, int32_t n,
   const bool culled = i < n && k == ~0ull;
   const uint32_t cm = __ballot_sync(0xffffffffu, culled);
   if (culled && (threadIdx.x & 31) == __ffs(cm) - 1) atomicAdd(&s_culled, __popc(cm));
-  if (i < n && !culled) atomicAdd(&hist[depth_bucket(k, ~range[0], range[1], nb)], 1);
+  if (i < n && !culled) atomicAdd(&hist[depth_bucket(k, kmin, kmax, nb)], 1);
   __syncthreads();
   if (threadIdx.x == 0 && s_culled) atomicAdd(&hist[nb], s_culled);
 }
@@ -967,10 +1024,16 @@ extern "C" int ss_depth_order(const uint64_t* depth_key, int32_t n, int32_t* ord
   int2* long_runs = (int2*)((char*)u64a + align256(nn * 4));
   const uint32_t nb = (uint32_t)(kBucketsPerKey * nn);
   int32_t* hist = big;  // nb + 1 counts, scanned in place into the bucket cursors
-  memzero(scratch32, 2 * sizeof(int32_t) + 2 * sizeof(unsigned long long), stream);
-  launch_k(depth_range_kernel, min(296, (n + 255) / 256), 256, 0, stream, depth_key, n, range, hist,
-                                                                      (int32_t)nb + 1);
-  launch_k(depth_hist_kernel, grid_for(n, 256), 256, 0, stream, depth_key, n, range, nb, hist);
+  // per-CTA range partials at the end of the scratch32 region (n + 1 int32;
+  // its head holds n_long, range and the histogram scan's block sums:
+  // ~n / 256 + 8 ints, the partials n / 16 + 16 bytes at most)
+  const int n_range = min(kRangeBlocks, (n + 255) / 256);
+  unsigned long long* partial =
+      (unsigned long long*)((char*)scratch32 + align256((nn + 1) * 4) - (size_t)n_range * 16);
+  launch_k(depth_range_kernel, n_range, 256, 0, stream, depth_key, n, partial, hist,
+           (int32_t)nb + 1, scratch32);
+  launch_k(depth_hist_kernel, grid_for(n, 256), 256, 0, stream, depth_key, n,
+           (const unsigned long long*)partial, n_range, range, nb, hist);
   // block sums after n_long / pad / range in the scratch32 region
   int rc = exclusive_scan<false>(hist, nullptr, 0, (int64_t)nb + 1, hist, scratch32 + 8, stream);
   if (rc) return rc;
