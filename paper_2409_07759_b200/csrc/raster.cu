@@ -2,7 +2,7 @@
 // (_kernels.py:56-130) as 16x16-tile rasterizers.
 //
 // Work mapping: a warp covers 16 x (2 STRIP) pixels of a tile (8 / STRIP
-// warps per tile, 4 warps per CTA, warps independent).  Lane l owns the
+// warps per tile, 4 warps per CTA in both passes, warps independent).  Lane l owns the
 // STRIP-pixel column strip x = l % 16, y = y0 + STRIP (l / 16) + k.  The
 // tile's list (already in the reference's global (z, src) order, see
 // binning.cu) is staged 32 records at a time through a warp-private shared
@@ -30,9 +30,12 @@
 // With t = alpha G d alpha' (zero when clamped), g_alpha = sum t / alpha and
 // dm = -t/2, and the strip sums sum t, sum t k, sum t k^2 give every
 // footprint gradient.  g2d receives the 9 linear basis sums (see the strip
-// epilogue) that ss_project_bwd turns into mean2d / conic / alpha gradients;
-// one 12-shuffle transposed warp reduction and one 9-lane float atomic per
-// (warp, entry).
+// epilogue) that ss_project_bwd turns into mean2d / conic / alpha gradients:
+// a warp parks each entry's 32 x 9 lane values in shared memory and every
+// 3 entries sums them (one lane per (entry, component)) into one float
+// atomic per (warp, entry, component); the deterministic mode instead
+// reduces each entry in registers (12-shuffle transposed reduction) into
+// fixed-order partials.
 #include "ss_common.cuh"
 
 namespace ss {
